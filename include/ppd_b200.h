@@ -1,0 +1,124 @@
+/* ppd_b200.h — the C-ABI between the host C++ PPD engine and the sm_100a device
+ * path (libppd_b200.so). Plain pointers and sizes; no torch types; no exception
+ * crosses it. Every entry returns an int status (PPD_OK == 0); on failure
+ * ppd_last_error() returns a thread-local message.
+ *
+ * The reference (/root/reference/proj) has no FFI: its execute path is four
+ * analytic cost functions called from the simulator's event handlers
+ * (SURVEY.md §8b). Each entry below names the reference interface it replaces:
+ *
+ *   ppd_prefill(FULL)    replaces cost::full_prefill_time     costmodel.hpp:85, costmodel.cpp:318-322
+ *                        (called simulator.cpp:327)
+ *   ppd_prefill(APPEND)  replaces cost::append_prefill_time   costmodel.hpp:86, costmodel.cpp:324-331
+ *                        (called simulator.cpp:328-329)
+ *   ppd_step             replaces cost::decode_step_time x interference_multiplier
+ *                        costmodel.hpp:97-100, costmodel.cpp:347-379 (called simulator.cpp:397):
+ *                        one fused iteration = decode rows + an optional append/prefill chunk
+ *   ppd_kv_copy          replaces cost::kv_transfer_time      costmodel.hpp:88-91, costmodel.cpp:333-345
+ *                        (called simulator.cpp:354)
+ *   ppd_kv_pool_init     replaces Node::prefix_cache           simulator.cpp:125 (token counts only)
+ *                        with a paged HBM pool; block tables stay host-side
+ *
+ * Errors the reference reports with std::invalid_argument (costmodel.cpp:319,
+ * :325-327, :335, :374-375) return PPD_ERR_INVALID with the same condition text.
+ */
+#ifndef PPD_B200_H
+#define PPD_B200_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPD_OK 0
+#define PPD_ERR_INVALID (-1) /* invalid argument (reference: std::invalid_argument) */
+#define PPD_ERR_CUDA (-2)    /* CUDA / driver failure */
+#define PPD_ERR_OOM (-3)     /* device memory exhausted */
+#define PPD_ERR_STATE (-4)   /* call out of order (e.g. step before weights/pool) */
+
+#define PPD_PREFILL_FULL 0   /* cost::PrefillKind::full   (costmodel.hpp:12) */
+#define PPD_PREFILL_APPEND 1 /* cost::PrefillKind::append */
+
+typedef struct ppd_model_cfg {
+  int32_t n_layers, d_model, n_q_heads, n_kv_heads, head_dim, d_ff, vocab;
+  float rms_eps, rope_theta;
+  int32_t qkv_bias; /* Qwen2.5: 1 */
+} ppd_model_cfg;
+
+typedef struct ppd_dev ppd_dev; /* one GPU worker: weights, KV pool, streams */
+
+const char* ppd_last_error(void);
+int ppd_version(void);
+int ppd_device_count(int32_t* n);
+
+/* max_step_tokens: largest sum(q_len) of one ppd_step; max_step_seqs: largest n_seqs. */
+int ppd_dev_open(int32_t gpu, const ppd_model_cfg* cfg, int32_t max_step_tokens,
+                 int32_t max_step_seqs, ppd_dev** out);
+int ppd_dev_close(ppd_dev* dev);
+int ppd_load_random_weights(ppd_dev* dev, uint64_t seed);
+int ppd_kv_pool_init(ppd_dev* dev, int32_t block_tokens, int32_t num_blocks);
+/* bytes of one KV block (all layers, K and V, all kv heads) */
+int ppd_kv_block_bytes(const ppd_model_cfg* cfg, int32_t block_tokens, uint64_t* bytes);
+int ppd_kv_pool_ptr(ppd_dev* dev, void** ptr, uint64_t* bytes);
+
+/* One fused iteration over n_seqs sequences. Sequence s contributes q_len[s]
+ * new tokens at positions ctx[s] .. ctx[s]+q_len[s]-1; their K/V are written
+ * into the pool through its block table row, then every new token attends to
+ * positions 0..its own (causal). q_len[s] == 1 is a decode row. For every s
+ * with want_token[s] != 0 (all s when want_token is NULL) the greedy next
+ * token after its last new token is written to out_tokens[s]. All arrays are
+ * HOST arrays; the call copies them in, runs, and copies the tokens out. */
+typedef struct ppd_batch {
+  int32_t n_seqs;
+  const int32_t* q_len;        /* [n_seqs] */
+  const int32_t* ctx;          /* [n_seqs] */
+  const int32_t* tokens;       /* [sum q_len] */
+  const int32_t* block_tables; /* [n_seqs * max_blocks] */
+  int32_t max_blocks;
+  const int32_t* want_token;   /* [n_seqs] or NULL */
+} ppd_batch;
+
+/* Synchronous: returns when out_tokens is filled. *out_ms (may be NULL) is the
+ * device time of the step (CUDA events on the compute stream). */
+int ppd_step(ppd_dev* dev, const ppd_batch* batch, int32_t* out_tokens, float* out_ms);
+/* Asynchronous pair: submit enqueues H2D + kernels + D2H into pinned staging. */
+int ppd_step_submit(ppd_dev* dev, const ppd_batch* batch);
+int ppd_step_wait(ppd_dev* dev, int32_t* out_tokens, float* out_ms);
+/* fp32 logits of the last step's want_token rows, [n_seqs][vocab] (host). */
+int ppd_last_logits(ppd_dev* dev, float* out, int64_t max_floats);
+
+/* Prefill seam. FULL: n_ctx must be 0 and tokens holds the whole history
+ * (the P node's full recompute, simulator.cpp:309-311). APPEND: tokens holds
+ * the n_new new tokens, attending n_ctx cached ones (simulator.cpp:282-289). */
+int ppd_prefill(ppd_dev* dev, int32_t kind, const int32_t* tokens, int32_t n_new, int32_t n_ctx,
+                const int32_t* block_table, int32_t n_blocks, int32_t* out_token, float* out_ms);
+
+/* Token-granular KV transfer of positions [start, start+n_tokens) of one
+ * sequence from src's pool to dst's pool (the P->D hop, simulator.cpp:349-356).
+ * Runs on dst's transfer stream over peer pointers (NVLink when src/dst are
+ * different GPUs), fenced after src's compute stream; dst's next step waits on
+ * it. *out_ms: device time of the copy. Bytes moved = n_tokens * kv bytes/token. */
+int ppd_kv_copy(ppd_dev* src, ppd_dev* dst, const int32_t* src_block_table,
+                const int32_t* dst_block_table, int32_t n_blocks, int32_t start,
+                int32_t n_tokens, float* out_ms);
+
+/* ---- kernel-level entry points (device pointers; used by parity tests) ----
+ * stream: cudaStream_t or NULL for the legacy default stream. */
+/* attention over a paged pool (num_blocks blocks) for one layer, through the
+ * same work-item builder and kernel as ppd_step. q [total_q][Hq][Dh] bf16
+ * (roped, device), out same shape bf16 (device). q_start [n_seqs+1], ctx
+ * [n_seqs], block_tables [n_seqs*max_blocks] are HOST int32. Synchronous. */
+int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_pool,
+                     int32_t num_blocks, int32_t block_tokens, int32_t layer, int32_t n_seqs,
+                     const int32_t* q_start, const int32_t* ctx, const int32_t* block_tables,
+                     int32_t max_blocks, void* out, void* stream);
+/* C[M][N] = A[M][K] . B[N][K]^T ; bf16 in, out_f32 ? fp32 : bf16 out. */
+int ppd_op_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                int32_t out_f32, void* stream);
+/* deterministic random-init fill, identical to the oracle's mo_weight_bf16 */
+int ppd_op_fill_random(void* dst, uint64_t n, uint64_t seed, int32_t tensor, int32_t layer,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,447 @@
+// attention.cu — K1/K2/K3/K4: paged attention over the HBM KV pool, one launch
+// for a mixed batch of decode rows and prefill/append query tiles.
+//
+// Replaces the analytic decode_step_time / append_prefill_time /
+// full_prefill_time service times (reference costmodel.cpp:318-379, called at
+// simulator.cpp:327-329 and :397) with real attention over the cached KV.
+//
+// Work items (one CTA each, grid = items x kv_heads):
+//   DECODE  one query token of sequence s, keys [key_begin, key_end) of a
+//           KV split; the G query heads sharing kv head h are rows 0..G-1 of
+//           a 16-row MMA tile; the 4 consumer warps take interleaved 16-key
+//           blocks of every 64-key stage and merge at the end (and across
+//           splits through a workspace, last CTA merges).
+//   PREFILL TQ = 64/G query tokens x G heads = 64 rows (16 per consumer warp),
+//           causal over keys [0, ctx + last token of the tile].
+// Paged K/V blocks (16 tokens x 128 dims per (block, layer, K|V, kv head)) are
+// staged into shared memory by TMA (2-D tensor map over the pool, 128-byte
+// swizzle) by a dedicated producer warp through a 3-stage mbarrier ring. The
+// QK^T and PV contractions use warp-level mma.sync (bf16 in, fp32 accumulate);
+// softmax is online, fp32, with quad shuffles for the row reductions.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ppdk {
+
+namespace {
+
+constexpr int kBT = 16;          // tokens per KV block
+constexpr int kDh = 128;         // head dim
+constexpr int kStageBlocks = 4;  // blocks per pipeline stage (64 keys)
+constexpr int kStages = 3;
+constexpr int kRows = 64;        // query rows per CTA (prefill)
+constexpr int kConsumerWarps = 4;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kBlockBytes = kBT * kDh * 2;                       // 4 KB
+constexpr int kStageBytes = kStageBlocks * 2 * kBlockBytes;      // 32 KB (K and V)
+constexpr int kQBytes = kRows * kDh * 2;                         // 16 KB
+constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kQBytes + 256;
+
+PPD_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+PPD_DEV void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+PPD_DEV void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// byte offset of (row, dim) inside one 16x128 K/V block laid out by TMA as two
+// 2 KB halves (dims 0-63 | 64-127) of 16 rows x 128 B with the 128-byte swizzle
+PPD_DEV uint32_t kv_off(int row, int dim) {
+  int half = dim >> 6;
+  int chunk = (dim & 63) >> 3;
+  return half * 2048 + row * 128 + ((chunk ^ (row & 7)) << 4) + ((dim & 7) << 1);
+}
+// Q tile: 64 rows x 256 B, 16-byte chunk index XOR (row & 7)
+PPD_DEV uint32_t q_off(int row, int dim) {
+  int chunk = dim >> 3;
+  return row * 256 + ((chunk ^ (row & 7)) << 4) + ((dim & 7) << 1);
+}
+
+PPD_DEV void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 1)
+    paged_attention_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;                                  // kStages * 32 KB
+  uint8_t* q_smem = smem + kStages * kStageBytes;              // 16 KB
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(q_smem + kQBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  int* flag = reinterpret_cast<int*>(empty_bar + kStages);
+
+  const AttnItem it = p.items[blockIdx.x];
+  const int kvh = blockIdx.y;
+  const int G = p.group;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool is_decode = it.kind == 0;
+  const int s = it.seq;
+  const int ctx = p.ctx[s];
+  const int q_base = p.q_start[s];
+
+  // key range
+  int key_begin, key_end;
+  if (is_decode) {
+    key_begin = it.key_begin;
+    key_end = it.key_end;
+  } else {
+    key_begin = 0;
+    key_end = ctx + it.q_tok0 + it.n_q;  // last token of the tile attends up to itself
+  }
+  const int n_stages_total = (key_end - key_begin + kStageBlocks * kBT - 1) / (kStageBlocks * kBT);
+  const int* btab = p.block_tables + (size_t)s * p.max_blocks;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  // Q tile -> shared (swizzled). Rows r: token r / G, head r % G.
+  {
+    const int rows = is_decode ? G : (it.n_q * G);
+    for (int idx = threadIdx.x; idx < kRows * (kDh / 8); idx += kThreads) {
+      int r = idx >> 4, c = idx & 15;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < rows) {
+        int tok = r / G, h = r % G;
+        const bf16* src = p.q + ((size_t)(q_base + it.q_tok0 + tok) * p.n_q_heads + kvh * G + h) * kDh + c * 8;
+        v = *reinterpret_cast<const uint4*>(src);
+      }
+      *reinterpret_cast<uint4*>(q_smem + r * 256 + ((c ^ (r & 7)) << 4)) = v;
+    }
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer warp: TMA loads of paged K/V ----------------
+    if (lane == 0) {
+      const int first_blk = key_begin / kBT;
+      const int last_blk = (key_end - 1) / kBT;  // inclusive
+      for (int st = 0; st < n_stages_total; ++st) {
+        int slot = st % kStages;
+        if (st >= kStages) mbar_wait(&empty_bar[slot], ((st / kStages) - 1) & 1);
+        int b0 = first_blk + st * kStageBlocks;
+        int nb = min(kStageBlocks, last_blk - b0 + 1);
+        mbar_arrive_expect_tx(&full_bar[slot], nb * 2 * kBlockBytes);
+        uint8_t* dst = stage_base + slot * kStageBytes;
+        for (int b = 0; b < nb; ++b) {
+          int blk = btab[b0 + b];
+          // pool row of (blk, layer, K, kvh, token 0)
+          int rowK = (((blk * p.n_layers + p.layer) * 2 + 0) * p.n_kv_heads + kvh) * kBT;
+          int rowV = rowK + p.n_kv_heads * kBT;
+          tma_load_2d(dst + (b * 2 + 0) * kBlockBytes, &kv_map, 0, rowK, &full_bar[slot]);
+          tma_load_2d(dst + (b * 2 + 0) * kBlockBytes + 2048, &kv_map, 64, rowK, &full_bar[slot]);
+          tma_load_2d(dst + (b * 2 + 1) * kBlockBytes, &kv_map, 0, rowV, &full_bar[slot]);
+          tma_load_2d(dst + (b * 2 + 1) * kBlockBytes + 2048, &kv_map, 64, rowV, &full_bar[slot]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int g = lane >> 2, t = lane & 3;
+  const int row_base = is_decode ? 0 : warp * 16;
+  const float sl2 = p.scale_log2;
+
+  // Q fragments for the 8 k-steps (dims 16kk..16kk+15)
+  uint32_t qa[8][4];
+  {
+    int r = row_base + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      int dim = kk * 16 + (lane >> 4) * 8;
+      ldsm_x4(smem_u32(q_smem) + q_off(r, dim), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+    }
+  }
+  // causal limit (position) of this thread's two rows
+  int pos_r0, pos_r1;
+  {
+    int r0 = row_base + g, r1 = row_base + g + 8;
+    if (is_decode) {
+      pos_r0 = pos_r1 = ctx;
+    } else {
+      int lim = it.n_q * G;
+      pos_r0 = r0 < lim ? ctx + it.q_tok0 + r0 / G : -1;
+      pos_r1 = r1 < lim ? ctx + it.q_tok0 + r1 / G : -1;
+    }
+  }
+
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  const int first_blk = key_begin / kBT;
+  for (int st = 0; st < n_stages_total; ++st) {
+    int slot = st % kStages;
+    mbar_wait(&full_bar[slot], (st / kStages) & 1);
+    const uint32_t sbase = smem_u32(stage_base + slot * kStageBytes);
+    const int stage_key0 = (first_blk + st * kStageBlocks) * kBT;
+    // decode: this warp's block within the stage; prefill: all 4 blocks
+    const int stage_blocks_valid = min(kStageBlocks, (key_end - 1) / kBT - (first_blk + st * kStageBlocks) + 1);
+    const int nblk = is_decode ? 1 : stage_blocks_valid;  // never touch blocks not loaded
+    const int blk_lo = is_decode ? warp : 0;
+    if (blk_lo < stage_blocks_valid) {
+      float sc[8][4];  // up to 8 n-tiles of 8 keys
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
+#pragma unroll
+      for (int bi = 0; bi < kStageBlocks; ++bi) {
+        if (bi < nblk) {
+          const int b = blk_lo + bi;
+          const uint32_t kb = sbase + (b * 2 + 0) * kBlockBytes;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            int krow = (lane & 7) + (lane >> 4) * 8;
+            int dim = kk * 16 + ((lane >> 3) & 1) * 8;
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(kb + kv_off(krow, dim), b0, b1, b2, b3);
+            mma16816(sc[bi * 2 + 0], qa[kk], b0, b1);
+            mma16816(sc[bi * 2 + 1], qa[kk], b2, b3);
+          }
+        }
+      }
+      // scale + mask, row max
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        if (nt < nblk * 2) {
+          int key = stage_key0 + (blk_lo + nt / 2) * kBT + (nt & 1) * 8 + 2 * t;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            int k = key + e;
+            bool ok0 = k <= pos_r0 && k >= key_begin && k < key_end;
+            bool ok1 = k <= pos_r1 && k >= key_begin && k < key_end;
+            sc[nt][e] = ok0 ? sc[nt][e] * sl2 : -INFINITY;
+            sc[nt][2 + e] = ok1 ? sc[nt][2 + e] * sl2 : -INFINITY;
+            mx0 = fmaxf(mx0, sc[nt][e]);
+            mx1 = fmaxf(mx1, sc[nt][2 + e]);
+          }
+        }
+      }
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+      float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+      // rows with nothing valid yet keep -inf; use 0 as the exponent base
+      float base0 = mn0 == -INFINITY ? 0.f : mn0;
+      float base1 = mn1 == -INFINITY ? 0.f : mn1;
+      float corr0 = exp2f(m0 - base0), corr1 = exp2f(m1 - base1);
+      m0 = mn0;
+      m1 = mn1;
+      float rs0 = 0.f, rs1 = 0.f;
+      uint32_t pa[4][4];  // P as A fragments, per 16-key block
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        if (nt < nblk * 2) {
+          float p0 = exp2f(sc[nt][0] - base0), p1 = exp2f(sc[nt][1] - base0);
+          float p2 = exp2f(sc[nt][2] - base1), p3 = exp2f(sc[nt][3] - base1);
+          rs0 += p0 + p1;
+          rs1 += p2 + p3;
+          pa[nt / 2][(nt & 1) * 2 + 0] = pack2(p0, p1);
+          pa[nt / 2][(nt & 1) * 2 + 1] = pack2(p2, p3);
+        }
+      }
+      rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
+      rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
+      rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
+      rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
+      l0 = l0 * corr0 + rs0;
+      l1 = l1 * corr1 + rs1;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        o[i][0] *= corr0;
+        o[i][1] *= corr0;
+        o[i][2] *= corr1;
+        o[i][3] *= corr1;
+      }
+      // O += P V
+#pragma unroll
+      for (int bi = 0; bi < kStageBlocks; ++bi) {
+        if (bi < nblk) {
+          const int b = blk_lo + bi;
+          const uint32_t vb = sbase + (b * 2 + 1) * kBlockBytes;
+          uint32_t a[4] = {pa[bi][0], pa[bi][1], pa[bi][2], pa[bi][3]};
+#pragma unroll
+          for (int nt = 0; nt < 16; nt += 2) {
+            int krow = (lane & 7) + ((lane >> 3) & 1) * 8;
+            int dim = nt * 8 + (lane >> 4) * 8;
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(vb + kv_off(krow, dim), b0, b1, b2, b3);
+            mma16816(o[nt], a, b0, b1);
+            mma16816(o[nt + 1], a, b2, b3);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[slot]);
+  }
+
+  if (!is_decode) {
+    // prefill rows: normalise and store bf16
+    const int lim = it.n_q * G;
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      int r = row_base + g + hr * 8;
+      if (r >= lim) continue;
+      float inv = 1.f / (hr ? l1 : l0);
+      int tok = r / G, h = r % G;
+      bf16* dst = p.out + ((size_t)(q_base + it.q_tok0 + tok) * p.n_q_heads + kvh * G + h) * kDh;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+        uint32_t v = pack2(o[nt][hr * 2] * inv, o[nt][hr * 2 + 1] * inv);
+        *reinterpret_cast<uint32_t*>(dst + nt * 8 + 2 * t) = v;
+      }
+    }
+    return;
+  }
+
+  // ---- decode: merge the 4 consumer warps (rows 0..G-1) through shared ----
+  // all TMA traffic has been consumed; reuse the stage buffers
+  named_barrier_sync(1, kConsumerWarps * 32);
+  float* sm_o = reinterpret_cast<float*>(stage_base);           // [4 warps][16 rows][128]
+  float* sm_ml = sm_o + kConsumerWarps * 16 * kDh;               // [4][16][2]
+  {
+    float* ow = sm_o + warp * 16 * kDh;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      ow[g * kDh + nt * 8 + 2 * t] = o[nt][0];
+      ow[g * kDh + nt * 8 + 2 * t + 1] = o[nt][1];
+      ow[(g + 8) * kDh + nt * 8 + 2 * t] = o[nt][2];
+      ow[(g + 8) * kDh + nt * 8 + 2 * t + 1] = o[nt][3];
+    }
+    if (t == 0) {
+      sm_ml[(warp * 16 + g) * 2 + 0] = m0;
+      sm_ml[(warp * 16 + g) * 2 + 1] = l0;
+      sm_ml[(warp * 16 + g + 8) * 2 + 0] = m1;
+      sm_ml[(warp * 16 + g + 8) * 2 + 1] = l1;
+    }
+  }
+  named_barrier_sync(1, kConsumerWarps * 32);
+  const int tid = threadIdx.x;  // 0..127 : one head dim each
+  const bool split = it.n_splits > 1;
+  for (int r = 0; r < G; ++r) {
+    float mm = -INFINITY;
+    for (int w = 0; w < kConsumerWarps; ++w) mm = fmaxf(mm, sm_ml[(w * 16 + r) * 2]);
+    float base = mm == -INFINITY ? 0.f : mm;
+    float ll = 0.f, acc = 0.f;
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      float f = exp2f(sm_ml[(w * 16 + r) * 2] - base);
+      ll += sm_ml[(w * 16 + r) * 2 + 1] * f;
+      acc += sm_o[(w * 16 + r) * kDh + tid] * f;
+    }
+    if (!split) {
+      bf16* dst = p.out + ((size_t)(q_base) * p.n_q_heads + kvh * G + r) * kDh;
+      dst[tid] = f2bf(acc / ll);
+    } else {
+      // partial (unnormalised) result for this split
+      size_t wi = ((size_t)it.ws_index * p.n_kv_heads + kvh) * G + r;
+      p.ws_o[wi * kDh + tid] = acc;
+      if (tid == 0) {
+        p.ws_ml[wi * 2 + 0] = mm;
+        p.ws_ml[wi * 2 + 1] = ll;
+      }
+    }
+  }
+  if (!split) return;
+  // last CTA of this (seq, kv head) merges the splits
+  __threadfence();
+  named_barrier_sync(1, kConsumerWarps * 32);
+  if (tid == 0) {
+    int* ctr = p.counters + (size_t)it.seq * p.n_kv_heads + kvh;
+    int prev = atomicAdd(ctr, 1);
+    int last = prev == it.n_splits - 1;
+    if (last) *ctr = 0;  // self-reset for the next launch
+    *flag = last;
+  }
+  named_barrier_sync(1, kConsumerWarps * 32);
+  if (!*flag) return;
+  __threadfence();
+  const int ws0 = it.ws_index - it.split;  // first split's workspace slot
+  for (int r = 0; r < G; ++r) {
+    float mm = -INFINITY;
+    for (int sp = 0; sp < it.n_splits; ++sp) {
+      size_t wi = ((size_t)(ws0 + sp) * p.n_kv_heads + kvh) * G + r;
+      mm = fmaxf(mm, __ldcg(&p.ws_ml[wi * 2]));
+    }
+    float base = mm == -INFINITY ? 0.f : mm;
+    float ll = 0.f, acc = 0.f;
+    for (int sp = 0; sp < it.n_splits; ++sp) {
+      size_t wi = ((size_t)(ws0 + sp) * p.n_kv_heads + kvh) * G + r;
+      float f = exp2f(__ldcg(&p.ws_ml[wi * 2]) - base);
+      ll += __ldcg(&p.ws_ml[wi * 2 + 1]) * f;
+      acc += __ldcg(&p.ws_o[wi * kDh + tid]) * f;
+    }
+    bf16* dst = p.out + ((size_t)(q_base) * p.n_q_heads + kvh * G + r) * kDh;
+    dst[tid] = f2bf(acc / ll);
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q);
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+int make_kv_tensor_map(void* map_out, const void* pool, uint64_t total_rows) {
+  auto fn = get_encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[2] = {(cuuint64_t)kDh, (cuuint64_t)total_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kDh * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)kBT};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(pool), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -(int)r;
+}
+
+cudaError_t launch_paged_attention(const void* kv_map, const AttnParams& p, int n_items,
+                                   cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(paged_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr = true;
+  }
+  if (n_items == 0) return cudaSuccess;
+  dim3 grid(n_items, p.n_kv_heads);
+  paged_attention_kernel<<<grid, kThreads, kSmemBytes, stream>>>(
+      *reinterpret_cast<const CUtensorMap*>(kv_map), p);
+  return cudaGetLastError();
+}
+
+}  // namespace ppdk

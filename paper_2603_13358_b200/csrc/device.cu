@@ -1,0 +1,731 @@
+// device.cu — the C-ABI device worker (include/ppd_b200.h): weights resident in
+// HBM, the paged KV pool, per-step metadata staging, and the fused forward step
+// that replaces the reference's analytic service times (costmodel.cpp:318-379).
+//
+// One ppd_step = one iteration of a node's engine loop: every sequence in the
+// batch contributes q_len new tokens (1 for a decode row, m for an append /
+// prefill chunk). All rows go through the same projection GEMMs, so an append
+// chunk rides inside the decode step (the paper's PPD argument);
+// attention for decode rows and prefill tiles is ONE launch (attention.cu).
+#include <cublas_v2.h>
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ppd_b200.h"
+#include "gemm.h"
+#include "kernels.h"
+
+using namespace ppdk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(expr)                                                                         \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(_e == cudaErrorMemoryAllocation ? PPD_ERR_OOM : PPD_ERR_CUDA,          \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));                   \
+  } while (0)
+
+#define CHECK_ARG(cond, msg) \
+  do {                       \
+    if (!(cond)) return fail(PPD_ERR_INVALID, msg); \
+  } while (0)
+
+constexpr int kMaxRope = 1 << 17;  // positions covered by the RoPE table
+constexpr int kAttnTargetCtas = 148 * 2 * 2;
+
+struct Layer {
+  bf16 *wqkv, *wo, *wgu, *wdown;
+  float* bqkv;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+int validate_cfg(const ppd_model_cfg* c) {
+  CHECK_ARG(c, "null model cfg");
+  CHECK_ARG(c->n_layers > 0 && c->d_model > 0 && c->n_q_heads > 0 && c->n_kv_heads > 0 &&
+                c->d_ff > 0 && c->vocab > 0,
+            "model cfg: sizes must be > 0");
+  CHECK_ARG(c->head_dim == 128, "model cfg: head_dim must be 128 (sm_100a kernels)");
+  CHECK_ARG(c->n_q_heads % c->n_kv_heads == 0, "model cfg: n_q_heads % n_kv_heads != 0");
+  CHECK_ARG(c->n_q_heads / c->n_kv_heads <= 16, "model cfg: GQA group > 16");
+  CHECK_ARG(c->d_model % 8 == 0 && c->d_model <= 8192, "model cfg: d_model % 8 or > 8192");
+  CHECK_ARG(c->d_ff % 64 == 0, "model cfg: d_ff must be a multiple of 64");
+  return PPD_OK;
+}
+
+}  // namespace
+
+struct ppd_dev {
+  int gpu = 0;
+  ppd_model_cfg cfg{};
+  int max_T = 0, max_S = 0;
+  cudaStream_t compute = nullptr, xfer = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, xev0 = nullptr, xev1 = nullptr, compute_done = nullptr;
+  GemmContext* gemm = nullptr;
+  // weights
+  void* wmem = nullptr;
+  size_t wbytes = 0;
+  bf16 *embed = nullptr, *lm_head = nullptr, *ones = nullptr;
+  std::vector<Layer> layers;
+  bool weights_ready = false;
+  float *rope_cos = nullptr, *rope_sin = nullptr;
+  // KV pool
+  bf16* kv = nullptr;
+  int bt = 0, nblocks = 0;
+  uint64_t kv_bytes = 0;
+  alignas(128) uint8_t kv_map[128];
+  // activations / workspaces
+  bf16 *x = nullptr, *h = nullptr, *q = nullptr, *attn = nullptr, *m = nullptr, *hl = nullptr;
+  float *qkv32 = nullptr, *proj32 = nullptr, *gu32 = nullptr, *down32 = nullptr, *logits = nullptr;
+  float *ws_o = nullptr, *ws_ml = nullptr;
+  int* counters = nullptr;
+  int ws_slots = 0;
+  // staging (pinned host + device)
+  uint8_t* h_meta = nullptr;
+  uint8_t* d_meta = nullptr;
+  size_t meta_cap = 0;
+  int* h_tokens_out = nullptr;
+  int* d_tokens_out = nullptr;
+  int pending = 0;  // sequences of the in-flight step (0 = none)
+  int last_logit_rows = 0;
+};
+
+namespace {
+
+// ------------------------------------------------------------ metadata
+struct StepLayout {
+  int n, T, maxb, n_out, n_items, n_ws;
+  size_t off_qstart, off_ctx, off_tokens, off_bt, off_rowseq, off_rowpos, off_outrows, off_items,
+      total;
+};
+
+// Builds the attention work list for the batch. Decode rows (q_len == 1) get
+// KV splits when the grid would otherwise under-fill the 148 SMs.
+void build_items(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads, int group,
+                 std::vector<AttnItem>& items, int& n_ws) {
+  items.clear();
+  n_ws = 0;
+  const int tq = std::max(1, 64 / group);
+  long base_ctas = 0;
+  int n_decode = 0;
+  for (int s = 0; s < n; ++s) {
+    if (q_len[s] == 1) {
+      ++n_decode;
+      base_ctas += n_kv_heads;
+    } else if (q_len[s] > 1) {
+      base_ctas += (long)((q_len[s] + tq - 1) / tq) * n_kv_heads;
+    }
+  }
+  int want = 1;
+  if (n_decode > 0 && base_ctas < kAttnTargetCtas)
+    want = (int)((kAttnTargetCtas + base_ctas - 1) / std::max<long>(base_ctas, 1));
+  for (int s = 0; s < n; ++s) {
+    if (q_len[s] <= 0) continue;
+    if (q_len[s] == 1) {
+      int keys = ctx[s] + 1;
+      int splits = std::min(want, (keys + 255) / 256);
+      splits = std::max(splits, 1);
+      int chunk = ((keys + splits - 1) / splits + 63) / 64 * 64;
+      splits = (keys + chunk - 1) / chunk;
+      for (int sp = 0; sp < splits; ++sp) {
+        AttnItem it{};
+        it.kind = 0;
+        it.seq = s;
+        it.q_tok0 = 0;
+        it.n_q = 1;
+        it.key_begin = sp * chunk;
+        it.key_end = std::min(keys, (sp + 1) * chunk);
+        it.split = sp;
+        it.n_splits = splits;
+        it.ws_index = splits > 1 ? n_ws + sp : -1;
+        items.push_back(it);
+      }
+      if (splits > 1) n_ws += splits;
+    } else {
+      for (int t0 = 0; t0 < q_len[s]; t0 += tq) {
+        AttnItem it{};
+        it.kind = 1;
+        it.seq = s;
+        it.q_tok0 = t0;
+        it.n_q = std::min(tq, q_len[s] - t0);
+        it.n_splits = 1;
+        it.ws_index = -1;
+        items.push_back(it);
+      }
+    }
+  }
+}
+
+int ensure_meta(ppd_dev* d, size_t bytes) {
+  if (bytes <= d->meta_cap) return PPD_OK;
+  size_t cap = align_up(bytes * 2, 1 << 20);
+  if (d->h_meta) cudaFreeHost(d->h_meta);
+  if (d->d_meta) cudaFree(d->d_meta);
+  d->h_meta = nullptr;
+  d->d_meta = nullptr;
+  CU(cudaMallocHost(&d->h_meta, cap));
+  CU(cudaMalloc(&d->d_meta, cap));
+  d->meta_cap = cap;
+  return PPD_OK;
+}
+
+int ensure_ws(ppd_dev* d, int slots) {
+  if (slots <= d->ws_slots) return PPD_OK;
+  int cap = std::max(slots, 1024);
+  const int G = d->cfg.n_q_heads / d->cfg.n_kv_heads;
+  if (d->ws_o) cudaFree(d->ws_o);
+  if (d->ws_ml) cudaFree(d->ws_ml);
+  d->ws_o = nullptr;
+  d->ws_ml = nullptr;
+  CU(cudaMalloc(&d->ws_o, (size_t)cap * d->cfg.n_kv_heads * G * 128 * sizeof(float)));
+  CU(cudaMalloc(&d->ws_ml, (size_t)cap * d->cfg.n_kv_heads * G * 2 * sizeof(float)));
+  d->ws_slots = cap;
+  return PPD_OK;
+}
+
+template <typename T>
+T* at(uint8_t* base, size_t off) {
+  return reinterpret_cast<T*>(base + off);
+}
+
+// Packs the batch into the pinned staging buffer (one H2D copy per step).
+int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnItem>& items) {
+  CHECK_ARG(b && b->n_seqs > 0, "batch: n_seqs must be >= 1");
+  CHECK_ARG(b->n_seqs <= d->max_S, "batch: n_seqs exceeds max_step_seqs");
+  CHECK_ARG(b->q_len && b->ctx && b->tokens && b->block_tables, "batch: null array");
+  CHECK_ARG(b->max_blocks > 0, "batch: max_blocks must be >= 1");
+  L.n = b->n_seqs;
+  L.maxb = b->max_blocks;
+  L.T = 0;
+  L.n_out = 0;
+  for (int s = 0; s < L.n; ++s) {
+    CHECK_ARG(b->q_len[s] >= 1, "batch: q_len must be >= 1");
+    CHECK_ARG(b->ctx[s] >= 0, "batch: ctx must be >= 0");
+    long end = (long)b->ctx[s] + b->q_len[s];
+    CHECK_ARG(end <= (long)b->max_blocks * d->bt, "batch: block table too short for ctx + q_len");
+    CHECK_ARG(end <= kMaxRope, "batch: position beyond RoPE table");
+    for (int j = 0; j < (int)((end + d->bt - 1) / d->bt); ++j) {
+      int blk = b->block_tables[(size_t)s * b->max_blocks + j];
+      CHECK_ARG(blk >= 0 && blk < d->nblocks, "batch: block id out of range");
+    }
+    L.T += b->q_len[s];
+    if (!b->want_token || b->want_token[s]) ++L.n_out;
+  }
+  CHECK_ARG(L.T <= d->max_T, "batch: sum(q_len) exceeds max_step_tokens");
+  for (int i = 0; i < L.T; ++i)
+    CHECK_ARG(b->tokens[i] >= 0 && b->tokens[i] < d->cfg.vocab, "batch: token id out of range");
+  const int G = d->cfg.n_q_heads / d->cfg.n_kv_heads;
+  build_items(L.n, b->q_len, b->ctx, d->cfg.n_kv_heads, G, items, L.n_ws);
+  L.n_items = (int)items.size();
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + bytes, 16);
+    return r;
+  };
+  L.off_qstart = take((L.n + 1) * 4);
+  L.off_ctx = take(L.n * 4);
+  L.off_tokens = take(L.T * 4);
+  L.off_bt = take((size_t)L.n * L.maxb * 4);
+  L.off_rowseq = take(L.T * 4);
+  L.off_rowpos = take(L.T * 4);
+  L.off_outrows = take(std::max(L.n_out, 1) * 4);
+  L.off_items = take(items.size() * sizeof(AttnItem));
+  L.total = o;
+  int rc = ensure_meta(d, L.total);
+  if (rc) return rc;
+  rc = ensure_ws(d, L.n_ws);
+  if (rc) return rc;
+  uint8_t* h = d->h_meta;
+  int32_t* qs = at<int32_t>(h, L.off_qstart);
+  int32_t* rs = at<int32_t>(h, L.off_rowseq);
+  int32_t* rp = at<int32_t>(h, L.off_rowpos);
+  int32_t* orow = at<int32_t>(h, L.off_outrows);
+  qs[0] = 0;
+  int k = 0;
+  for (int s = 0; s < L.n; ++s) {
+    qs[s + 1] = qs[s] + b->q_len[s];
+    for (int i = 0; i < b->q_len[s]; ++i) {
+      rs[qs[s] + i] = s;
+      rp[qs[s] + i] = b->ctx[s] + i;
+    }
+    if (!b->want_token || b->want_token[s]) orow[k++] = qs[s + 1] - 1;
+  }
+  std::memcpy(h + L.off_ctx, b->ctx, L.n * 4);
+  std::memcpy(h + L.off_tokens, b->tokens, L.T * 4);
+  std::memcpy(h + L.off_bt, b->block_tables, (size_t)L.n * L.maxb * 4);
+  std::memcpy(h + L.off_items, items.data(), items.size() * sizeof(AttnItem));
+  return PPD_OK;
+}
+
+int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf16* out,
+                  const int* d_qstart, const int* d_ctx, const int* d_bt, int maxb,
+                  const AttnItem* d_items, int n_items, int layer, float* ws_o, float* ws_ml,
+                  int* counters, cudaStream_t s) {
+  AttnParams p{};
+  p.items = d_items;
+  p.q = q;
+  p.out = out;
+  p.q_start = d_qstart;
+  p.ctx = d_ctx;
+  p.block_tables = d_bt;
+  p.max_blocks = maxb;
+  p.n_layers = c.n_layers;
+  p.layer = layer;
+  p.n_q_heads = c.n_q_heads;
+  p.n_kv_heads = c.n_kv_heads;
+  p.group = c.n_q_heads / c.n_kv_heads;
+  p.scale_log2 = (1.0f / std::sqrt((float)c.head_dim)) * 1.4426950408889634f;
+  p.ws_o = ws_o;
+  p.ws_ml = ws_ml;
+  p.counters = counters;
+  CU(launch_paged_attention(kv_map, p, n_items, s));
+  return PPD_OK;
+}
+
+// The forward pass of one step; metadata already staged in d->d_meta.
+int forward(ppd_dev* d, const StepLayout& L) {
+  const ppd_model_cfg& c = d->cfg;
+  cudaStream_t s = d->compute;
+  const int Dh = c.head_dim, d_model = c.d_model, F = c.d_ff;
+  const int qd = c.n_q_heads * Dh, kd = c.n_kv_heads * Dh, W = qd + 2 * kd;
+  uint8_t* m = d->d_meta;
+  const int* qstart = at<int>(m, L.off_qstart);
+  const int* ctx = at<int>(m, L.off_ctx);
+  const int* tokens = at<int>(m, L.off_tokens);
+  const int* bt = at<int>(m, L.off_bt);
+  const int* rowseq = at<int>(m, L.off_rowseq);
+  const int* rowpos = at<int>(m, L.off_rowpos);
+  const int* outrows = at<int>(m, L.off_outrows);
+  const AttnItem* items = at<AttnItem>(m, L.off_items);
+  const int T = L.T;
+
+  CU(launch_embed(tokens, d->embed, d->x, T, d_model, s));
+  for (int l = 0; l < c.n_layers; ++l) {
+    const Layer& w = d->layers[l];
+    // x += down(prev) ; h = norm(x)
+    CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, 1, nullptr, d->ones, d->h, T, d_model,
+                          c.rms_eps, s));
+    CU(gemm_run(d->gemm, d->h, w.wqkv, d->qkv32, T, W, d_model, true, s));
+    CU(launch_rope_kv_write(d->qkv32, 1, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
+                            d->rope_sin, d->q, d->kv, T, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers,
+                            l, d->bt, s));
+    int rc = run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_items, l,
+                           d->ws_o, d->ws_ml, d->counters, s);
+    if (rc) return rc;
+    CU(gemm_run(d->gemm, d->attn, w.wo, d->proj32, T, d_model, qd, true, s));
+    CU(launch_add_rmsnorm(d->x, d->proj32, 1, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
+    CU(gemm_run(d->gemm, d->h, w.wgu, d->gu32, T, 2 * F, d_model, true, s));
+    CU(launch_silu_mul(d->gu32, d->m, T, F, s));
+    CU(gemm_run(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, true, s));
+  }
+  CU(launch_final_norm(d->x, d->down32, 1, nullptr, outrows, L.n_out, d->ones, d->hl, T, d_model,
+                       c.rms_eps, s));
+  CU(gemm_run(d->gemm, d->hl, d->lm_head, d->logits, L.n_out, c.vocab, d_model, true, s));
+  CU(launch_argmax(d->logits, L.n_out, c.vocab, d->d_tokens_out, s));
+  return PPD_OK;
+}
+
+int alloc_workspaces(ppd_dev* d) {
+  const ppd_model_cfg& c = d->cfg;
+  const size_t T = d->max_T, S = d->max_S;
+  const size_t qd = (size_t)c.n_q_heads * c.head_dim, kd = (size_t)c.n_kv_heads * c.head_dim;
+  CU(cudaMalloc(&d->x, T * c.d_model * 2));
+  CU(cudaMalloc(&d->h, T * c.d_model * 2));
+  CU(cudaMalloc(&d->q, T * qd * 2));
+  CU(cudaMalloc(&d->attn, T * qd * 2));
+  CU(cudaMalloc(&d->m, T * c.d_ff * 2));
+  CU(cudaMalloc(&d->hl, S * c.d_model * 2));
+  CU(cudaMalloc(&d->qkv32, T * (qd + 2 * kd) * 4));
+  CU(cudaMalloc(&d->proj32, T * c.d_model * 4));
+  CU(cudaMalloc(&d->gu32, T * 2 * c.d_ff * 4));
+  CU(cudaMalloc(&d->down32, T * c.d_model * 4));
+  CU(cudaMalloc(&d->logits, S * c.vocab * 4));
+  CU(cudaMalloc(&d->counters, S * c.n_kv_heads * 4));
+  CU(cudaMemset(d->counters, 0, S * c.n_kv_heads * 4));
+  CU(cudaMallocHost(&d->h_tokens_out, S * 4));
+  CU(cudaMalloc(&d->d_tokens_out, S * 4));
+  // RoPE cos/sin table, built in double on the host (same recipe as the oracle)
+  const int half = c.head_dim / 2;
+  std::vector<float> cs((size_t)kMaxRope * half), sn((size_t)kMaxRope * half);
+  std::vector<double> inv(half);
+  for (int i = 0; i < half; ++i) inv[i] = std::pow((double)c.rope_theta, -2.0 * i / (double)c.head_dim);
+  for (int p = 0; p < kMaxRope; ++p)
+    for (int i = 0; i < half; ++i) {
+      double a = (double)p * inv[i];
+      cs[(size_t)p * half + i] = (float)std::cos(a);
+      sn[(size_t)p * half + i] = (float)std::sin(a);
+    }
+  CU(cudaMalloc(&d->rope_cos, cs.size() * 4));
+  CU(cudaMalloc(&d->rope_sin, sn.size() * 4));
+  CU(cudaMemcpy(d->rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d->rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+  return PPD_OK;
+}
+
+void free_all(ppd_dev* d) {
+  void* dev_ptrs[] = {d->wmem, d->kv, d->x, d->h, d->q, d->attn, d->m, d->hl, d->qkv32, d->proj32,
+                      d->gu32, d->down32, d->logits, d->ws_o, d->ws_ml, d->counters, d->d_meta,
+                      d->d_tokens_out, d->rope_cos, d->rope_sin};
+  for (void* p : dev_ptrs)
+    if (p) cudaFree(p);
+  if (d->h_meta) cudaFreeHost(d->h_meta);
+  if (d->h_tokens_out) cudaFreeHost(d->h_tokens_out);
+  if (d->gemm) gemm_destroy(d->gemm);
+  cudaEvent_t evs[] = {d->ev0, d->ev1, d->xev0, d->xev1, d->compute_done};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  if (d->compute) cudaStreamDestroy(d->compute);
+  if (d->xfer) cudaStreamDestroy(d->xfer);
+}
+
+}  // namespace
+
+// ============================================================ C-ABI
+extern "C" {
+
+const char* ppd_last_error(void) { return g_err.c_str(); }
+int ppd_version(void) { return 1; }
+
+int ppd_device_count(int32_t* n) {
+  int c = 0;
+  CU(cudaGetDeviceCount(&c));
+  *n = c;
+  return PPD_OK;
+}
+
+int ppd_kv_block_bytes(const ppd_model_cfg* cfg, int32_t block_tokens, uint64_t* bytes) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  CHECK_ARG(block_tokens == 16, "block_tokens must be 16");
+  *bytes = (uint64_t)cfg->n_layers * 2 * cfg->n_kv_heads * block_tokens * cfg->head_dim * 2;
+  return PPD_OK;
+}
+
+int ppd_dev_open(int32_t gpu, const ppd_model_cfg* cfg, int32_t max_step_tokens,
+                 int32_t max_step_seqs, ppd_dev** out) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  CHECK_ARG(out, "null out");
+  CHECK_ARG(max_step_tokens >= 1 && max_step_seqs >= 1 && max_step_seqs <= max_step_tokens,
+            "max_step_tokens/max_step_seqs invalid");
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  CHECK_ARG(gpu >= 0 && gpu < ndev, "gpu index out of range");
+  CU(cudaSetDevice(gpu));
+  ppd_dev* d = new ppd_dev();
+  d->gpu = gpu;
+  d->cfg = *cfg;
+  d->max_T = max_step_tokens;
+  d->max_S = max_step_seqs;
+  auto bail = [&](int code) {
+    free_all(d);
+    delete d;
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&d->compute, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&d->xfer, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&d->ev0) != cudaSuccess || cudaEventCreate(&d->ev1) != cudaSuccess ||
+      cudaEventCreate(&d->xev0) != cudaSuccess || cudaEventCreate(&d->xev1) != cudaSuccess ||
+      cudaEventCreateWithFlags(&d->compute_done, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(PPD_ERR_CUDA, "stream/event creation failed"));
+  d->gemm = gemm_create();
+  if (!d->gemm) return bail(fail(PPD_ERR_CUDA, "gemm context creation failed"));
+  rc = alloc_workspaces(d);
+  if (rc) return bail(rc);
+  *out = d;
+  return PPD_OK;
+}
+
+int ppd_dev_close(ppd_dev* d) {
+  if (!d) return PPD_OK;
+  cudaSetDevice(d->gpu);
+  cudaDeviceSynchronize();
+  free_all(d);
+  delete d;
+  return PPD_OK;
+}
+
+int ppd_load_random_weights(ppd_dev* d, uint64_t seed) {
+  CHECK_ARG(d, "null dev");
+  CU(cudaSetDevice(d->gpu));
+  const ppd_model_cfg& c = d->cfg;
+  const size_t dm = c.d_model, F = c.d_ff, V = c.vocab;
+  const size_t qd = (size_t)c.n_q_heads * c.head_dim, kd = (size_t)c.n_kv_heads * c.head_dim;
+  const size_t per_layer = align_up((qd + 2 * kd) * dm * 2, 256) + align_up(dm * qd * 2, 256) +
+                           align_up(2 * F * dm * 2, 256) + align_up(dm * F * 2, 256) +
+                           align_up((qd + 2 * kd) * 4, 256);
+  const size_t total = 2 * align_up(V * dm * 2, 256) + align_up(dm * 2, 256) + per_layer * c.n_layers;
+  if (!d->wmem) {
+    CU(cudaMalloc(&d->wmem, total));
+    d->wbytes = total;
+  }
+  uint8_t* p = static_cast<uint8_t*>(d->wmem);
+  auto take = [&](size_t bytes) {
+    uint8_t* r = p;
+    p += align_up(bytes, 256);
+    return r;
+  };
+  cudaStream_t s = d->compute;
+  d->embed = reinterpret_cast<bf16*>(take(V * dm * 2));
+  d->lm_head = reinterpret_cast<bf16*>(take(V * dm * 2));
+  d->ones = reinterpret_cast<bf16*>(take(dm * 2));
+  CU(launch_fill_random(d->embed, V * dm, seed, 0, 0, s));
+  CU(launch_fill_random(d->lm_head, V * dm, seed, 8, 0, s));
+  CU(launch_fill_const(d->ones, dm, 1.0f, s));
+  d->layers.assign(c.n_layers, Layer{});
+  for (int l = 0; l < c.n_layers; ++l) {
+    Layer& w = d->layers[l];
+    w.wqkv = reinterpret_cast<bf16*>(take((qd + 2 * kd) * dm * 2));
+    w.wo = reinterpret_cast<bf16*>(take(dm * qd * 2));
+    w.wgu = reinterpret_cast<bf16*>(take(2 * F * dm * 2));
+    w.wdown = reinterpret_cast<bf16*>(take(dm * F * 2));
+    float* b = reinterpret_cast<float*>(take((qd + 2 * kd) * 4));
+    w.bqkv = c.qkv_bias ? b : nullptr;
+    CU(launch_fill_qkv(w.wqkv, (int)qd, (int)kd, (int)dm, seed, l, s));
+    CU(launch_fill_random(w.wo, dm * qd, seed, 4, l, s));
+    CU(launch_fill_gate_up(w.wgu, (int)F, (int)dm, seed, l, s));
+    CU(launch_fill_random(w.wdown, dm * F, seed, 7, l, s));
+    if (c.qkv_bias) CU(launch_fill_bias(w.bqkv, (int)qd, (int)kd, seed, l, s));
+  }
+  CU(cudaStreamSynchronize(s));
+  d->weights_ready = true;
+  return PPD_OK;
+}
+
+int ppd_kv_pool_init(ppd_dev* d, int32_t block_tokens, int32_t num_blocks) {
+  CHECK_ARG(d, "null dev");
+  CHECK_ARG(block_tokens == 16, "block_tokens must be 16");
+  CHECK_ARG(num_blocks >= 1, "num_blocks must be >= 1");
+  CU(cudaSetDevice(d->gpu));
+  uint64_t bb = 0;
+  int rc = ppd_kv_block_bytes(&d->cfg, block_tokens, &bb);
+  if (rc) return rc;
+  uint64_t rows = (uint64_t)num_blocks * d->cfg.n_layers * 2 * d->cfg.n_kv_heads * block_tokens;
+  CHECK_ARG(rows < (1ull << 31), "KV pool too large for 32-bit TMA row coordinates");
+  if (d->kv) cudaFree(d->kv);
+  d->kv = nullptr;
+  CU(cudaMalloc(&d->kv, bb * num_blocks));
+  CU(cudaMemset(d->kv, 0, bb * num_blocks));
+  d->bt = block_tokens;
+  d->nblocks = num_blocks;
+  d->kv_bytes = bb * num_blocks;
+  if (make_kv_tensor_map(d->kv_map, d->kv, rows) != 0)
+    return fail(PPD_ERR_CUDA, "cuTensorMapEncodeTiled failed for the KV pool");
+  return PPD_OK;
+}
+
+int ppd_kv_pool_ptr(ppd_dev* d, void** ptr, uint64_t* bytes) {
+  CHECK_ARG(d && ptr && bytes, "null arg");
+  *ptr = d->kv;
+  *bytes = d->kv_bytes;
+  return PPD_OK;
+}
+
+int ppd_step_submit(ppd_dev* d, const ppd_batch* b) {
+  CHECK_ARG(d, "null dev");
+  if (!d->weights_ready || !d->kv) return fail(PPD_ERR_STATE, "step before weights and KV pool");
+  if (d->pending) return fail(PPD_ERR_STATE, "step already in flight");
+  CU(cudaSetDevice(d->gpu));
+  StepLayout L{};
+  std::vector<AttnItem> items;
+  int rc = pack_batch(d, b, L, items);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(d->d_meta, d->h_meta, L.total, cudaMemcpyHostToDevice, d->compute));
+  CU(cudaEventRecord(d->ev0, d->compute));
+  rc = forward(d, L);
+  if (rc) return rc;
+  CU(cudaEventRecord(d->ev1, d->compute));
+  CU(cudaMemcpyAsync(d->h_tokens_out, d->d_tokens_out, L.n_out * 4, cudaMemcpyDeviceToHost,
+                     d->compute));
+  CU(cudaEventRecord(d->compute_done, d->compute));
+  d->pending = L.n_out > 0 ? L.n_out : -1;
+  d->last_logit_rows = L.n_out;
+  return PPD_OK;
+}
+
+int ppd_step_wait(ppd_dev* d, int32_t* out_tokens, float* out_ms) {
+  CHECK_ARG(d, "null dev");
+  if (!d->pending) return fail(PPD_ERR_STATE, "no step in flight");
+  CU(cudaSetDevice(d->gpu));
+  CU(cudaEventSynchronize(d->compute_done));
+  int n = d->pending > 0 ? d->pending : 0;
+  d->pending = 0;
+  if (out_tokens && n) std::memcpy(out_tokens, d->h_tokens_out, n * 4);
+  if (out_ms) CU(cudaEventElapsedTime(out_ms, d->ev0, d->ev1));
+  return PPD_OK;
+}
+
+int ppd_step(ppd_dev* d, const ppd_batch* b, int32_t* out_tokens, float* out_ms) {
+  int rc = ppd_step_submit(d, b);
+  if (rc) return rc;
+  return ppd_step_wait(d, out_tokens, out_ms);
+}
+
+int ppd_last_logits(ppd_dev* d, float* out, int64_t max_floats) {
+  CHECK_ARG(d && out, "null arg");
+  int64_t n = (int64_t)d->last_logit_rows * d->cfg.vocab;
+  CHECK_ARG(n <= max_floats, "output buffer too small");
+  CU(cudaSetDevice(d->gpu));
+  CU(cudaMemcpy(out, d->logits, n * 4, cudaMemcpyDeviceToHost));
+  return PPD_OK;
+}
+
+int ppd_prefill(ppd_dev* d, int32_t kind, const int32_t* tokens, int32_t n_new, int32_t n_ctx,
+                const int32_t* block_table, int32_t n_blocks, int32_t* out_token, float* out_ms) {
+  // mirrors the reference's argument checks (costmodel.cpp:319, :325-327)
+  if (kind == PPD_PREFILL_FULL) {
+    CHECK_ARG(n_new >= 1, "full_prefill_time: n must be >= 1");
+    CHECK_ARG(n_ctx == 0, "full prefill recomputes the whole history: n_ctx must be 0");
+  } else if (kind == PPD_PREFILL_APPEND) {
+    CHECK_ARG(n_new >= 1, "append_prefill_time: m must be >= 1");
+    CHECK_ARG(n_ctx >= 0, "append_prefill_time: n_ctx must be >= 0");
+  } else {
+    return fail(PPD_ERR_INVALID, "unknown prefill kind");
+  }
+  ppd_batch b{};
+  b.n_seqs = 1;
+  b.q_len = &n_new;
+  b.ctx = &n_ctx;
+  b.tokens = tokens;
+  b.block_tables = block_table;
+  b.max_blocks = n_blocks;
+  b.want_token = nullptr;
+  return ppd_step(d, &b, out_token, out_ms);
+}
+
+int ppd_kv_copy(ppd_dev* src, ppd_dev* dst, const int32_t* src_block_table,
+                const int32_t* dst_block_table, int32_t n_blocks, int32_t start, int32_t n_tokens,
+                float* out_ms) {
+  // reference: kv_transfer_time requires tokens >= 1 (costmodel.cpp:335)
+  CHECK_ARG(src && dst, "null dev");
+  CHECK_ARG(n_tokens >= 1, "kv_transfer_time: tokens >= 1");
+  CHECK_ARG(start >= 0 && (long)start + n_tokens <= (long)n_blocks * dst->bt, "token range outside block table");
+  CHECK_ARG(src->kv && dst->kv && src->bt == dst->bt, "pools not initialised / block size mismatch");
+  for (int j = start / dst->bt; j <= (start + n_tokens - 1) / dst->bt; ++j) {
+    CHECK_ARG(src_block_table[j] >= 0 && src_block_table[j] < src->nblocks, "src block id out of range");
+    CHECK_ARG(dst_block_table[j] >= 0 && dst_block_table[j] < dst->nblocks, "dst block id out of range");
+  }
+  CU(cudaSetDevice(dst->gpu));
+  if (src->gpu != dst->gpu) {
+    cudaError_t e = cudaDeviceEnablePeerAccess(src->gpu, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+      return fail(PPD_ERR_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+  }
+  // block tables travel in a small device buffer of the destination worker
+  int32_t* dbt = nullptr;
+  CU(cudaMallocAsync(&dbt, (size_t)n_blocks * 2 * 4, dst->xfer));
+  CU(cudaMemcpyAsync(dbt, src_block_table, (size_t)n_blocks * 4, cudaMemcpyHostToDevice, dst->xfer));
+  CU(cudaMemcpyAsync(dbt + n_blocks, dst_block_table, (size_t)n_blocks * 4, cudaMemcpyHostToDevice,
+                     dst->xfer));
+  // the producer's KV must be complete: fence after the source compute stream
+  CU(cudaStreamWaitEvent(dst->xfer, src->compute_done, 0));
+  CU(cudaEventRecord(dst->xev0, dst->xfer));
+  KvCopyParams p{};
+  p.src_pool = src->kv;
+  p.dst_pool = dst->kv;
+  p.src_blocks = dbt;
+  p.dst_blocks = dbt + n_blocks;
+  p.start = start;
+  p.n_tokens = n_tokens;
+  p.n_layers = dst->cfg.n_layers;
+  p.n_kv_heads = dst->cfg.n_kv_heads;
+  p.block_tokens = dst->bt;
+  p.head_dim = dst->cfg.head_dim;
+  CU(launch_kv_copy(p, dst->xfer));
+  CU(cudaEventRecord(dst->xev1, dst->xfer));
+  CU(cudaFreeAsync(dbt, dst->xfer));
+  // the decode node's next step starts after the KV has landed
+  CU(cudaStreamWaitEvent(dst->compute, dst->xev1, 0));
+  CU(cudaEventSynchronize(dst->xev1));
+  if (out_ms) CU(cudaEventElapsedTime(out_ms, dst->xev0, dst->xev1));
+  return PPD_OK;
+}
+
+// ------------------------------------------------------------ test entry points
+int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_pool,
+                     int32_t num_blocks, int32_t block_tokens, int32_t layer, int32_t n_seqs,
+                     const int32_t* q_start, const int32_t* ctx, const int32_t* block_tables,
+                     int32_t max_blocks, void* out, void* stream) {
+  int rc = validate_cfg(cfg);
+  if (rc) return rc;
+  CHECK_ARG(block_tokens == 16, "block_tokens must be 16");
+  CHECK_ARG(n_seqs >= 1 && layer >= 0 && layer < cfg->n_layers, "bad n_seqs/layer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int32_t> qlen(n_seqs);
+  for (int i = 0; i < n_seqs; ++i) qlen[i] = q_start[i + 1] - q_start[i];
+  const int G = cfg->n_q_heads / cfg->n_kv_heads;
+  std::vector<AttnItem> items;
+  int n_ws = 0;
+  build_items(n_seqs, qlen.data(), ctx, cfg->n_kv_heads, G, items, n_ws);
+  alignas(128) uint8_t map[128];
+  uint64_t rows = (uint64_t)num_blocks * cfg->n_layers * 2 * cfg->n_kv_heads * block_tokens;
+  if (make_kv_tensor_map(map, kv_pool, rows) != 0) return fail(PPD_ERR_CUDA, "tensor map encode failed");
+  size_t nb = (size_t)n_seqs * max_blocks;
+  size_t bytes = (n_seqs + 1 + n_seqs + nb) * 4 + items.size() * sizeof(AttnItem) + 64;
+  uint8_t* dm = nullptr;
+  float *ws_o = nullptr, *ws_ml = nullptr;
+  int* ctr = nullptr;
+  CU(cudaMalloc(&dm, bytes));
+  CU(cudaMalloc(&ws_o, (size_t)std::max(n_ws, 1) * cfg->n_kv_heads * G * 128 * 4));
+  CU(cudaMalloc(&ws_ml, (size_t)std::max(n_ws, 1) * cfg->n_kv_heads * G * 2 * 4));
+  CU(cudaMalloc(&ctr, (size_t)n_seqs * cfg->n_kv_heads * 4));
+  CU(cudaMemset(ctr, 0, (size_t)n_seqs * cfg->n_kv_heads * 4));
+  int* d_qs = reinterpret_cast<int*>(dm);
+  int* d_ctx = d_qs + n_seqs + 1;
+  int* d_bt = d_ctx + n_seqs;
+  AttnItem* d_items = reinterpret_cast<AttnItem*>(align_up(reinterpret_cast<uintptr_t>(d_bt + nb), 16));
+  CU(cudaMemcpy(d_qs, q_start, (n_seqs + 1) * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_ctx, ctx, n_seqs * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_bt, block_tables, nb * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(d_items, items.data(), items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice));
+  rc = run_attention(*cfg, map, static_cast<const bf16*>(q), static_cast<bf16*>(out), d_qs, d_ctx,
+                     d_bt, max_blocks, d_items, (int)items.size(), layer, ws_o, ws_ml, ctr, s);
+  cudaStreamSynchronize(s);
+  cudaFree(dm);
+  cudaFree(ws_o);
+  cudaFree(ws_ml);
+  cudaFree(ctr);
+  if (rc) return rc;
+  CU(cudaGetLastError());
+  return PPD_OK;
+}
+
+int ppd_op_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                int32_t out_f32, void* stream) {
+  CHECK_ARG(A && B && C && M > 0 && N > 0 && K > 0, "bad gemm args");
+  static thread_local GemmContext* ctx = nullptr;
+  if (!ctx) ctx = gemm_create();
+  if (!ctx) return fail(PPD_ERR_CUDA, "gemm context");
+  CU(gemm_run(ctx, static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0,
+              static_cast<cudaStream_t>(stream)));
+  CU(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return PPD_OK;
+}
+
+int ppd_op_fill_random(void* dst, uint64_t n, uint64_t seed, int32_t tensor, int32_t layer,
+                       void* stream) {
+  CHECK_ARG(dst, "null dst");
+  CU(launch_fill_random(static_cast<bf16*>(dst), n, seed, tensor, layer,
+                        static_cast<cudaStream_t>(stream)));
+  CU(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return PPD_OK;
+}
+
+}  // extern "C"

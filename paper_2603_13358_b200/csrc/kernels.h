@@ -1,0 +1,86 @@
+// kernels.h — host-visible declarations of the device kernels' launchers.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ppdk {
+
+typedef __nv_bfloat16 bf16;
+
+// One attention work item (a CTA per item per kv head).
+struct AttnItem {
+  int kind;       // 0 decode, 1 prefill tile
+  int seq;        // sequence index in the step
+  int q_tok0;     // first query token (within the sequence's new tokens)
+  int n_q;        // query tokens in this tile (decode: 1)
+  int key_begin;  // decode split: key range
+  int key_end;
+  int split;      // split index, n_splits total; ws_index = workspace slot
+  int n_splits;
+  int ws_index;
+  int pad[3];
+};
+
+struct AttnParams {
+  const AttnItem* items;
+  const bf16* q;             // [total_q][Hq][Dh]
+  bf16* out;                 // [total_q][Hq][Dh]
+  const int* q_start;        // [n_seqs+1]
+  const int* ctx;            // [n_seqs]
+  const int* block_tables;   // [n_seqs][max_blocks]
+  int max_blocks;
+  int n_layers, layer, n_q_heads, n_kv_heads, group;
+  float scale_log2;
+  float* ws_o;               // split partials [slot][Hkv][G][Dh]
+  float* ws_ml;              // [slot][Hkv][G][2]
+  int* counters;             // [n_seqs][Hkv], zero-initialised, self-resetting
+};
+
+int make_kv_tensor_map(void* map_out /* CUtensorMap, 128 B */, const void* pool, uint64_t total_rows);
+cudaError_t launch_paged_attention(const void* kv_map, const AttnParams& p, int n_items,
+                                   cudaStream_t stream);
+
+// ---- small fused ops (ops.cu) ----
+cudaError_t launch_fill_random(bf16* dst, uint64_t n, uint64_t seed, int tensor, int layer,
+                               cudaStream_t s);
+// fused QKV weight [Hq*Dh + 2*Hkv*Dh][d]: rows < qd from tensor WQ, then WK, then WV
+cudaError_t launch_fill_qkv(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer, cudaStream_t s);
+cudaError_t launch_fill_bias(float* dst, int qd, int kd, uint64_t seed, int layer, cudaStream_t s);
+// gate/up weight [2F][d], interleaved in groups of 64 rows: rows [128j, 128j+64) = gate
+// rows [64j, 64j+64), rows [128j+64, 128j+128) = up rows [64j, 64j+64)
+cudaError_t launch_fill_gate_up(bf16* dst, int F, int d, uint64_t seed, int layer, cudaStream_t s);
+cudaError_t launch_fill_const(bf16* dst, uint64_t n, float v, cudaStream_t s);
+
+cudaError_t launch_embed(const int* tokens, const bf16* embed, bf16* x, int T, int d, cudaStream_t s);
+// x = rbf(x + rbf(delta)) (if delta); h = rbf(rmsnorm(x) * w). delta may be fp32 split partials
+// (n_part slices of [T][d]) summed first, or bf16 when delta_bf16 != null.
+cudaError_t launch_add_rmsnorm(bf16* x, const float* delta_f32, int n_part, const bf16* delta_bf16,
+                               const bf16* w, bf16* h, int T, int d, float eps, cudaStream_t s);
+// final: for each selected row r = rows[i]: v = x[r] (+ delta[r]); out[i] = rbf(rmsnorm(v) * w)
+cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, int n_part,
+                              const bf16* delta_bf16, const int* rows, int n_rows, const bf16* w,
+                              bf16* out, int T, int d, float eps, cudaStream_t s);
+// qkv fp32 [T][qd+2kd] (+bias) -> q bf16 [T][Hq][Dh] roped; k roped, v -> paged pool
+cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias, const int* row_seq,
+                                 const int* row_pos, const int* block_tables, int max_blocks,
+                                 const float* rope_cos, const float* rope_sin, bf16* q_out,
+                                 bf16* kv_pool, int T, int Hq, int Hkv, int Dh, int n_layers,
+                                 int layer, int block_tokens, cudaStream_t s);
+// gate/up fp32 [T][2F] interleaved (see launch_fill_gate_up) -> m = rbf(silu(g) * u) [T][F]
+cudaError_t launch_silu_mul(const float* gu, bf16* m, int T, int F, cudaStream_t s);
+cudaError_t launch_argmax(const float* logits, int n, int V, int* out, cudaStream_t s);
+cudaError_t launch_f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t s);
+
+// ---- KV transfer (kv_copy.cu) ----
+struct KvCopyParams {
+  const bf16* src_pool;
+  bf16* dst_pool;
+  const int* src_blocks;  // block table rows (device)
+  const int* dst_blocks;
+  int start, n_tokens;
+  int n_layers, n_kv_heads, block_tokens, head_dim;
+};
+cudaError_t launch_kv_copy(const KvCopyParams& p, cudaStream_t s);
+
+}  // namespace ppdk

@@ -1,0 +1,54 @@
+// kv_copy.cu — K7: token-granular paged-KV transfer between two pools (the
+// P->D hop that replaces cost::kv_transfer_time, reference costmodel.cpp:333-345,
+// called at simulator.cpp:354 with need = ctx + new - have tokens).
+//
+// The sequence positions are identical on both sides, so for every 16-token
+// block b touched by [start, start+n) and every (layer, K|V, kv head) the bytes
+// to move are one contiguous run of (tokens in b) x head_dim x 2 B in both
+// pools. One warp moves one run with 16-byte vector accesses; when the pools
+// live on different GPUs the source is a peer (NVLink) pointer and the copy is a
+// pull by the destination GPU.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ppdk {
+
+__global__ void kv_copy_kernel(KvCopyParams p) {
+  const int lane = threadIdx.x & 31;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int n_warps = (gridDim.x * blockDim.x) >> 5;
+  const int BT = p.block_tokens;
+  const int first_b = p.start / BT;
+  const int last_b = (p.start + p.n_tokens - 1) / BT;
+  const int per_block = p.n_layers * 2 * p.n_kv_heads;
+  const long units = (long)(last_b - first_b + 1) * per_block;
+  const size_t row_bytes = (size_t)p.head_dim * 2;
+  for (long u = warp_global; u < units; u += n_warps) {
+    int bi = (int)(u / per_block);
+    int rest = (int)(u % per_block);  // (layer, kv, head) flattened = slice index inside a block
+    int b = first_b + bi;
+    int t0 = max(p.start, b * BT) - b * BT;
+    int t1 = min(p.start + p.n_tokens, (b + 1) * BT) - b * BT;
+    size_t slice = (size_t)rest * BT;  // rows of head_dim within the block
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(p.src_pool) +
+                         (((size_t)p.src_blocks[b] * per_block * BT) + slice + t0) * row_bytes;
+    uint8_t* dst = reinterpret_cast<uint8_t*>(p.dst_pool) +
+                   (((size_t)p.dst_blocks[b] * per_block * BT) + slice + t0) * row_bytes;
+    const int n16 = (int)((t1 - t0) * row_bytes / 16);
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int i = lane; i < n16; i += 32) d4[i] = __ldcs(s4 + i);
+  }
+}
+
+cudaError_t launch_kv_copy(const KvCopyParams& p, cudaStream_t s) {
+  if (p.n_tokens <= 0) return cudaSuccess;
+  const int BT = p.block_tokens;
+  long units = (long)((p.start + p.n_tokens - 1) / BT - p.start / BT + 1) * p.n_layers * 2 * p.n_kv_heads;
+  long warps = units < 148L * 64 ? units : 148L * 64;
+  int blocks = (int)((warps + 7) / 8);
+  kv_copy_kernel<<<blocks, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace ppdk

@@ -1,0 +1,323 @@
+// ops.cu — K6: small fused elementwise / reduction kernels of the forward step
+// (embedding gather, residual-add + RMSNorm, RoPE + paged KV write, SiLU-mul,
+// greedy argmax) and the deterministic random-init fills. All HBM-bound; one
+// CTA per token row with 16-byte vector accesses. Rounding points follow
+// oracle/model_oracle.c exactly (IEEE _rn intrinsics, no contraction).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ppdk {
+
+namespace {
+constexpr int kNormThreads = 256;
+constexpr int kMaxChunks = 4;  // d <= 256 * 8 * 4 = 8192
+
+template <int N>
+PPD_DEV float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float r = 0.f;
+  if (threadIdx.x < 32) {
+    r = threadIdx.x < N / 32 ? red[threadIdx.x] : 0.f;
+    r = warp_sum(r);
+    if (threadIdx.x == 0) red[32] = r;
+  }
+  __syncthreads();
+  r = red[32];
+  __syncthreads();
+  return r;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ fills
+__global__ void fill_random_kernel(bf16* dst, uint64_t n, uint64_t seed, int tensor, int layer) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = weight_value(seed, tensor, layer, i);
+}
+cudaError_t launch_fill_random(bf16* dst, uint64_t n, uint64_t seed, int tensor, int layer,
+                               cudaStream_t s) {
+  fill_random_kernel<<<148 * 8, 256, 0, s>>>(dst, n, seed, tensor, layer);
+  return cudaGetLastError();
+}
+
+__global__ void fill_qkv_kernel(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer) {
+  const uint64_t n = (uint64_t)(qd + 2 * kd) * d;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t r = i / d, c = i % d;
+    int tensor;
+    uint64_t lr;
+    if (r < (uint64_t)qd) { tensor = 1; lr = r; }
+    else if (r < (uint64_t)(qd + kd)) { tensor = 2; lr = r - qd; }
+    else { tensor = 3; lr = r - qd - kd; }
+    dst[i] = weight_value(seed, tensor, layer, lr * d + c);
+  }
+}
+cudaError_t launch_fill_qkv(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer, cudaStream_t s) {
+  fill_qkv_kernel<<<148 * 8, 256, 0, s>>>(dst, qd, kd, d, seed, layer);
+  return cudaGetLastError();
+}
+
+__global__ void fill_bias_kernel(float* dst, int qd, int kd, uint64_t seed, int layer) {
+  int n = qd + 2 * kd;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int tensor, lr;
+    if (i < qd) { tensor = 9; lr = i; }
+    else if (i < qd + kd) { tensor = 10; lr = i - qd; }
+    else { tensor = 11; lr = i - qd - kd; }
+    dst[i] = bf2f(weight_value(seed, tensor, layer, (uint64_t)lr));
+  }
+}
+cudaError_t launch_fill_bias(float* dst, int qd, int kd, uint64_t seed, int layer, cudaStream_t s) {
+  fill_bias_kernel<<<64, 256, 0, s>>>(dst, qd, kd, seed, layer);
+  return cudaGetLastError();
+}
+
+__global__ void fill_gate_up_kernel(bf16* dst, int F, int d, uint64_t seed, int layer) {
+  const uint64_t n = (uint64_t)2 * F * d;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t r = i / d, c = i % d;
+    uint64_t grp = r / 128, within = r % 128;
+    int tensor = within < 64 ? 5 : 6;  // gate | up
+    uint64_t lr = grp * 64 + (within & 63);
+    dst[i] = weight_value(seed, tensor, layer, lr * d + c);
+  }
+}
+cudaError_t launch_fill_gate_up(bf16* dst, int F, int d, uint64_t seed, int layer, cudaStream_t s) {
+  fill_gate_up_kernel<<<148 * 8, 256, 0, s>>>(dst, F, d, seed, layer);
+  return cudaGetLastError();
+}
+
+__global__ void fill_const_kernel(bf16* dst, uint64_t n, float v) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = f2bf(v);
+}
+cudaError_t launch_fill_const(bf16* dst, uint64_t n, float v, cudaStream_t s) {
+  fill_const_kernel<<<148, 256, 0, s>>>(dst, n, v);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ embed
+__global__ void embed_kernel(const int* tokens, const bf16* embed, bf16* x, int d) {
+  const int r = blockIdx.x;
+  const uint4* src = reinterpret_cast<const uint4*>(embed + (size_t)tokens[r] * d);
+  uint4* dst = reinterpret_cast<uint4*>(x + (size_t)r * d);
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) dst[c] = src[c];
+}
+cudaError_t launch_embed(const int* tokens, const bf16* embed, bf16* x, int T, int d, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  embed_kernel<<<T, 128, 0, s>>>(tokens, embed, x, d);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------- residual add + RMSNorm
+// v = x (+ rbf(sum of delta partials) | + delta_bf16); x <- v ; out = rbf(rbf(v) * inv_rms) * w
+template <bool kWriteX>
+__global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
+    bf16* x, const float* df, int n_part, size_t part_stride, const bf16* db, const bf16* w,
+    bf16* out, const int* rows, int d, float eps) {
+  __shared__ float red[33];
+  const size_t row = rows ? (size_t)rows[blockIdx.x] : (size_t)blockIdx.x;
+  const int nc = d / 8;
+  float v[kMaxChunks][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxChunks; ++k) {
+    int c = threadIdx.x + k * kNormThreads;
+    if (c < nc) {
+      unpack8(reinterpret_cast<const uint4*>(x + row * d)[c], v[k]);
+      if (df) {
+        float acc[8];
+        const float* base = df + row * d + (size_t)c * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        for (int pp = 0; pp < n_part; ++pp) {
+          float4 a = reinterpret_cast<const float4*>(base + pp * part_stride)[0];
+          float4 b = reinterpret_cast<const float4*>(base + pp * part_stride)[1];
+          acc[0] = __fadd_rn(acc[0], a.x); acc[1] = __fadd_rn(acc[1], a.y);
+          acc[2] = __fadd_rn(acc[2], a.z); acc[3] = __fadd_rn(acc[3], a.w);
+          acc[4] = __fadd_rn(acc[4], b.x); acc[5] = __fadd_rn(acc[5], b.y);
+          acc[6] = __fadd_rn(acc[6], b.z); acc[7] = __fadd_rn(acc[7], b.w);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[k][j] = rbf(__fadd_rn(v[k][j], rbf(acc[j])));
+      } else if (db) {
+        float dv[8];
+        unpack8(reinterpret_cast<const uint4*>(db + row * d)[c], dv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[k][j] = rbf(__fadd_rn(v[k][j], dv[j]));
+      }
+      if (kWriteX && (df || db)) reinterpret_cast<uint4*>(x + row * d)[c] = pack8(v[k]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += v[k][j] * v[k][j];
+    }
+  }
+  ss = block_sum<kNormThreads>(ss, red);
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), eps)));
+  const size_t orow = rows ? (size_t)blockIdx.x : row;
+#pragma unroll
+  for (int k = 0; k < kMaxChunks; ++k) {
+    int c = threadIdx.x + k * kNormThreads;
+    if (c < nc) {
+      float wv[8], o[8];
+      unpack8(reinterpret_cast<const uint4*>(w)[c], wv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = __fmul_rn(rbf(__fmul_rn(v[k][j], inv)), wv[j]);
+      reinterpret_cast<uint4*>(out + orow * d)[c] = pack8(o);
+    }
+  }
+}
+
+cudaError_t launch_add_rmsnorm(bf16* x, const float* delta_f32, int n_part, const bf16* delta_bf16,
+                               const bf16* w, bf16* h, int T, int d, float eps, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  add_rmsnorm_kernel<true><<<T, kNormThreads, 0, s>>>(x, delta_f32, n_part, (size_t)T * d,
+                                                      delta_bf16, w, h, nullptr, d, eps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, int n_part,
+                              const bf16* delta_bf16, const int* rows, int n_rows, const bf16* w,
+                              bf16* out, int T, int d, float eps, cudaStream_t s) {
+  if (n_rows == 0) return cudaSuccess;
+  add_rmsnorm_kernel<false><<<n_rows, kNormThreads, 0, s>>>(const_cast<bf16*>(x), delta_f32, n_part,
+                                                           (size_t)T * d, delta_bf16, w, out, rows,
+                                                           d, eps);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- RoPE + KV write
+__global__ void rope_kv_kernel(const float* qkv, int n_part, size_t part_stride, const float* bias,
+                               const int* row_seq, const int* row_pos, const int* block_tables,
+                               int max_blocks, const float* rope_cos, const float* rope_sin,
+                               bf16* q_out, bf16* kv, int Hq, int Hkv, int Dh, int n_layers,
+                               int layer, int BT) {
+  const int r = blockIdx.x;
+  const int half = Dh / 2;
+  const int qd = Hq * Dh, kd = Hkv * Dh, W = qd + 2 * kd;
+  const int pos = row_pos[r], seq = row_seq[r];
+  const int blk = block_tables[(size_t)seq * max_blocks + pos / BT];
+  const int tok = pos % BT;
+  const float* cs = rope_cos + (size_t)pos * half;
+  const float* sn = rope_sin + (size_t)pos * half;
+  auto val = [&](int col) {
+    float a = 0.f;
+    for (int pp = 0; pp < n_part; ++pp) a = __fadd_rn(a, qkv[pp * part_stride + (size_t)r * W + col]);
+    if (bias) a = __fadd_rn(a, bias[col]);
+    return rbf(a);
+  };
+  // rotary pairs of q heads and k heads
+  const int n_pairs = (Hq + Hkv) * half;
+  for (int i = threadIdx.x; i < n_pairs; i += blockDim.x) {
+    int head = i / half, j = i % half;
+    int col = head * Dh + j;  // k heads follow q heads contiguously in the fused layout
+    float x1 = val(col), x2 = val(col + half);
+    float c = cs[j], sv = sn[j];
+    float o1 = rbf(__fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, sv)));
+    float o2 = rbf(__fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, sv)));
+    if (head < Hq) {
+      bf16* q = q_out + ((size_t)r * Hq + head) * Dh;
+      q[j] = f2bf(o1);
+      q[j + half] = f2bf(o2);
+    } else {
+      int hk = head - Hq;
+      bf16* k = kv + ((((size_t)blk * n_layers + layer) * 2 + 0) * Hkv + hk) * BT * Dh + (size_t)tok * Dh;
+      k[j] = f2bf(o1);
+      k[j + half] = f2bf(o2);
+    }
+  }
+  for (int i = threadIdx.x; i < kd; i += blockDim.x) {
+    int hk = i / Dh, dd = i % Dh;
+    float v = val(qd + kd + i);
+    bf16* vp = kv + ((((size_t)blk * n_layers + layer) * 2 + 1) * Hkv + hk) * BT * Dh + (size_t)tok * Dh;
+    vp[dd] = f2bf(v);
+  }
+}
+
+cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias, const int* row_seq,
+                                 const int* row_pos, const int* block_tables, int max_blocks,
+                                 const float* rope_cos, const float* rope_sin, bf16* q_out,
+                                 bf16* kv_pool, int T, int Hq, int Hkv, int Dh, int n_layers,
+                                 int layer, int block_tokens, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const size_t W = (size_t)(Hq + 2 * Hkv) * Dh;
+  rope_kv_kernel<<<T, 256, 0, s>>>(qkv, n_part, (size_t)T * W, bias, row_seq, row_pos, block_tables,
+                                   max_blocks, rope_cos, rope_sin, q_out, kv_pool, Hq, Hkv, Dh,
+                                   n_layers, layer, block_tokens);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- SiLU * up
+__global__ void silu_mul_kernel(const float* gu, bf16* m, int F) {
+  const int r = blockIdx.y;
+  const float* row = gu + (size_t)r * 2 * F;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
+    int grp = j >> 6, within = j & 63;
+    float g = row[grp * 128 + within];
+    float u = row[grp * 128 + 64 + within];
+    float sv = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
+    m[(size_t)r * F + j] = f2bf(__fmul_rn(sv, u));
+  }
+}
+cudaError_t launch_silu_mul(const float* gu, bf16* m, int T, int F, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  dim3 grid((F + 255) / 256, T);
+  silu_mul_kernel<<<grid, 256, 0, s>>>(gu, m, F);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- argmax
+__global__ void argmax_kernel(const float* logits, int V, int* out) {
+  const float* row = logits + (size_t)blockIdx.x * V;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    float x = row[v];
+    if (x > best || (x == best && v < bi)) { best = x; bi = v; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { sb[w] = best; si[w] = bi; }
+  __syncthreads();
+  if (w == 0) {
+    int nw = blockDim.x >> 5;
+    best = l < nw ? sb[l] : -INFINITY;
+    bi = l < nw ? si[l] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (l == 0) out[blockIdx.x] = bi;
+  }
+}
+cudaError_t launch_argmax(const float* logits, int n, int V, int* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  argmax_kernel<<<n, 1024, 0, s>>>(logits, V, out);
+  return cudaGetLastError();
+}
+
+__global__ void f32_to_bf16_kernel(const float* in, bf16* out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = f2bf(in[i]);
+}
+cudaError_t launch_f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t s) {
+  f32_to_bf16_kernel<<<148 * 4, 256, 0, s>>>(in, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace ppdk
