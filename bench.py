@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py — PPD serving data path on B200 (see DESIGN.md §6 for definitions).
+
+Headline (N=1, BASELINE.json configs[1]): Llama-3-8B-shape random-init bf16 on
+one colocated B200; a "step" is one fused decode iteration of B=200 requests at
+context ~1024 through ppd_step (the C-ABI seam that replaces
+decode_step_time, reference costmodel.cpp:372-379). value = decode tokens/s
+(device time, CUDA events on the library's compute stream); e2e = the same
+through the C-ABI with host arrays and the H2D/D2H copies inside the timed
+region. The interference sweep of configs[1] (colocated full vs append
+prefill riding in the decode step) is reported beside it.
+
+--impl reference: the reference has no model (it prices this step with an
+analytic formula); its CPU arm here is the CPU port of the same decode step
+(oracle/model_oracle.c, kind "port") on all host cores, bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = json.load(open(os.path.join(REPO, "BASELINE.json")))["metric"]
+SEED = 20260313
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled (NVML, every 50 ms) during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self.stop = threading.Event()
+        self.err = None
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+        return self
+
+    def _run(self):
+        N = self.N
+        while not self.stop.is_set():
+            try:
+                self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception as e:  # noqa: BLE001
+                self.err = repr(e)
+            self.stop.wait(0.05)
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if hasattr(self, "t"):
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "error": self.err}
+        N = self.N
+        names = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                 "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                 "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap,
+                 "hw_power_brake": N.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+        reasons = sorted({n for _, r in self.samples for n, bit in names.items() if r & bit})
+        sm = [c for c, _ in self.samples]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU port
+def cpu_port_decode(batch: int, ctx: int, layers_full: int, n_rep: int = 1):
+    """Times the CPU port (oracle/model_oracle.c, all host threads) of one
+    Llama-3-8B-shape decode step: measures a 1-layer and a 2-layer model
+    step of `batch` rows at context `ctx` and extrapolates
+    t = t_head + layers_full * t_layer. Returns (tok/s, sample, seconds)."""
+    from oracle import oracle as O
+    t_sum = 0.0
+    times = {}
+    for nl in (1, 2):
+        cfg = O.MoCfg(nl, 4096, 32, 8, 128, 14336, 128256, 1e-5, 5e5, 0)
+        m = O.Model(cfg, SEED)
+        nbps = (ctx + 1 + 15) // 16
+        pool = O.KvPool(cfg, batch * nbps)
+        rng = np.random.default_rng(1)
+        pool.data[...] = O.f32_to_bf16((rng.standard_normal(pool.data.shape, dtype=np.float32) * 0.5))
+        bts = np.arange(batch * nbps, dtype=np.int32).reshape(batch, nbps)
+        toks = rng.integers(0, cfg.vocab, batch).astype(np.int32)
+        best = None
+        for _ in range(n_rep):
+            t0 = time.perf_counter()
+            m.step(pool, [1] * batch, [ctx] * batch, toks, bts, want_logits=False)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+            t_sum += dt
+        times[nl] = best
+        del m
+    t_layer = max(times[2] - times[1], 1e-9)
+    t_head = max(times[1] - t_layer, 0.0)
+    t_full = t_head + layers_full * t_layer
+    sample = (f"{batch} decode rows at ctx {ctx}, 1- and 2-layer Llama-3-8B-shape steps timed, "
+              f"extrapolated to {layers_full} layers (t_layer={t_layer*1e3:.1f} ms, t_head={t_head*1e3:.1f} ms)")
+    return batch / t_full, sample, t_sum
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2603_13358_b200 as ppd
+
+    torch.cuda.set_device(local_rank)
+    cfg = ppd.llama8b_cfg()
+    B, ctx0 = args.batch, args.ctx
+    K, W = args.steps, args.warmup
+    BT = 16
+    max_ctx = ctx0 + W + K + 16
+    bps = (max_ctx + BT - 1) // BT
+    n_inter_blocks = 4 * 64 + 4 * 64 + 8
+    dev = ppd.Device(local_rank, cfg, max_step_tokens=max(4096, B + 4 * 1024), max_step_seqs=max(B + 8, 256))
+    dev.load_random_weights(SEED)
+    dev.kv_pool_init(B * bps + n_inter_blocks)
+    bts = np.arange(B * bps, dtype=np.int32).reshape(B, bps)
+    rng = np.random.default_rng(SEED + rank)
+
+    # ---- prefill the B contexts (4 sequences of ctx0 tokens per step) ----
+    t0 = time.perf_counter()
+    last = np.zeros(B, dtype=np.int32)
+    if args.fill_kv == "random":
+        ptr, nbytes = dev.kv_pool_ptr()
+        ppd.check(ppd.lib().ppd_op_fill_random(ptr, nbytes // 2, SEED, 99, 0, None))
+        last[:] = rng.integers(0, cfg.vocab, B)
+    else:
+        per = max(1, 4096 // ctx0)
+        for s0 in range(0, B, per):
+            idx = list(range(s0, min(B, s0 + per)))
+            toks = rng.integers(0, cfg.vocab, ctx0 * len(idx)).astype(np.int32)
+            r = dev.step([ctx0] * len(idx), [0] * len(idx), toks, bts[idx])
+            last[idx] = r.tokens
+    prefill_s = time.perf_counter() - t0
+
+    ctx = np.full(B, ctx0, dtype=np.int32)
+    tok = last.copy()
+    for _ in range(W):
+        tok = dev.step([1] * B, ctx, tok, bts).tokens
+        ctx += 1
+
+    # ---- timed region: K decode steps ----
+    dist = world > 1
+    if dist:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    dev.reset_stats()
+    ncu = bool(os.environ.get("PPD_NCU"))
+    if ncu:
+        torch.cuda.profiler.start()
+    with ClockSampler(local_rank) as clk:
+        t0 = time.perf_counter()
+        step_ms = []
+        for _ in range(K):
+            r = dev.step([1] * B, ctx, tok, bts)
+            tok = r.tokens
+            step_ms.append(r.ms)
+            ctx += 1
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    if ncu:
+        torch.cuda.profiler.stop()
+        dev.close()
+        return
+    if dist:
+        torch.distributed.barrier()
+    st = dev.stats()
+    dev_ms = float(np.sum(step_ms))
+    h2d_bytes = 4 * (B + 1 + B + B + B * bps + B + B + B) + 48 * B * 2
+    times = torch.tensor([dev_ms, wall * 1e3], dtype=torch.float64, device="cuda")
+    if dist:
+        torch.distributed.all_reduce(times, op=torch.distributed.ReduceOp.MAX)
+    dev_ms_max, wall_ms_max = times.tolist()
+
+    # ---- profiled pass: per-kernel-class device time (roofline) ----
+    dev.set_profiling(True)
+    dev.reset_stats()
+    for _ in range(3):
+        tok = dev.step([1] * B, ctx, tok, bts).tokens
+        ctx += 1
+    prof = dev.stats()
+    dev.set_profiling(False)
+
+    # ---- interference sweep (configs[1]): prefills riding in the decode step ----
+    inter = {}
+    base_blk = B * bps
+    ib = lambda i: np.arange(base_blk + 64 * i, base_blk + 64 * (i + 1), dtype=np.int32)
+    # cached contexts for the append sequences: n = 1024 - m tokens each
+    m_app = args.append_new
+    for i in range(4):
+        dev.step([1024 - m_app], [0], rng.integers(0, cfg.vocab, 1024 - m_app), ib(4 + i))
+
+    def timed(extra_q, extra_ctx, extra_bt, n=3):
+        q = [1] * B + extra_q
+        c = list(ctx) + extra_ctx
+        bt = np.zeros((B + len(extra_q), bps + 64), dtype=np.int32)
+        bt[:B, :bps] = bts
+        for j, e in enumerate(extra_bt):
+            bt[B + j, :64] = e
+        want = [1] * B + [0] * len(extra_q)
+        ms = []
+        for _ in range(n):
+            toks = np.concatenate([tok, rng.integers(0, cfg.vocab, int(np.sum(extra_q)))]).astype(np.int32)
+            ms.append(dev.step(q, c, toks, bt, want).ms)
+        return float(np.median(ms))
+
+    alone = timed([], [], [])
+    for conc in (1, 4):
+        full = timed([1024] * conc, [0] * conc, [ib(i) for i in range(conc)])
+        app = timed([m_app] * conc, [1024 - m_app] * conc, [ib(4 + i) for i in range(conc)])
+        inter[f"conc{conc}"] = {"tpot_ms_full_1024": full, "tpot_ms_append_1024": app,
+                                "mult_full": full / alone, "mult_append": app / alone}
+    inter["tpot_ms_alone"] = alone
+    inter["append_new_tokens"] = m_app
+    inter["reference_anchor_mult"] = {"full_1024_b200": 1.48, "append_1024_b200": 1.02,
+                                      "full_1024_conc4": 1.57, "append_1024_conc4": 1.21}
+
+    if rank != 0:
+        dev.close()
+        return
+
+    pk, pk_kind = peaks()
+    attn_gbs = prof["attn_bytes"] / (prof["attn_ms"] * 1e-3) / 1e9 if prof["attn_ms"] > 0 else None
+    total_prof_ms = prof["step_ms"]
+    step_bytes_kv = float(np.sum(ctx)) * 131072
+    value = B * K * world / (dev_ms_max * 1e-3)
+    e2e_value = B * K * world / (wall_ms_max * 1e-3)
+
+    cpu = None
+    if not args.no_cpu:
+        nthr = cpu_threads()
+        tps, sample, secs = cpu_port_decode(args.cpu_batch, ctx0, cfg.n_layers)
+        cpu = {"value": tps, "unit": "tok/s", "cores": nthr, "kind": "port", "sample": sample,
+               "wall_s": secs}
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "tok/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": dev_ms_max / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic token ids, random-init bf16 weights (counter hash, std 0.02)",
+        "config": {
+            "workload": f"Llama-3-8B-shape decode step, B={B} requests at ctx {ctx0}+, 1 colocated node per GPU "
+                        "(BASELINE configs[1]); interference sweep beside it",
+            "model": "llama-3-8b-shape (random init)",
+            "global_batch": B * world,
+            "seq_len": ctx0,
+            "parallelism": "replicas (one node per GPU, no collective in the decode step)",
+            "l2_policy": f"inputs larger than L2: {step_bytes_kv/1e9:.1f} GB KV + 16.06 GB weights read per step",
+        },
+        "tpot_ms": dev_ms_max / K,
+        "interference": inter,
+        "roofline": {
+            "kernel": "paged_attention_kernel (K1/K2, decode rows)",
+            "bound": "hbm",
+            "achieved": attn_gbs,
+            "peak": pk["hbm_gbs"],
+            "peak_kind": pk_kind,
+            "unit": "GB/s",
+            "frac": (attn_gbs / pk["hbm_gbs"]) if attn_gbs else None,
+            "traffic": None,
+            "algorithmic_bytes_per_launch": prof["attn_bytes"] / max(prof["attn_launches"], 1),
+            "attn_share_of_step": prof["attn_ms"] / total_prof_ms if total_prof_ms else None,
+            "gemm_share_of_step": prof["gemm_ms"] / total_prof_ms if total_prof_ms else None,
+        },
+        "step_hbm": {
+            "bytes_per_step": step_bytes_kv + 16.06e9,
+            "achieved_gbs": (step_bytes_kv + 16.06e9) / (dev_ms_max / K * 1e-3) / 1e9,
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": h2d_bytes,
+                "d2h_bytes_per_step": 4 * B},
+        "gpu_launches": int(st["own_launches"]),
+        "lib_launches": int(st["lib_launches"]),
+        "clocks": clk.summary(),
+        "prefill_setup_s": prefill_s,
+    }
+    print(json.dumps(line), flush=True)
+    dev.close()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    nthr = cpu_threads()
+    vals = []
+    t_all = 0.0
+    sample = ""
+    for _ in range(args.warmup):
+        cpu_port_decode(args.cpu_batch, args.ctx, 32)
+    for _ in range(args.steps):
+        tps, sample, secs = cpu_port_decode(args.cpu_batch, args.ctx, 32)
+        vals.append(tps)
+        t_all += secs
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": "tok/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 (bf16 storage)",
+        "data": "synthetic",
+        "config": {"workload": f"Llama-3-8B-shape decode step at ctx {args.ctx} (CPU port, bounded sample)"},
+        "cpu_baseline": {"value": v, "unit": "tok/s", "cores": nthr, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (/root/reference/proj) prices this step analytically "
+                "(costmodel.cpp:372-379) and computes no tokens; its CPU arm is the oracle port",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=200)
+    ap.add_argument("--ctx", type=int, default=1024)
+    ap.add_argument("--append-new", type=int, default=128)
+    ap.add_argument("--cpu-batch", type=int, default=4)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fill-kv", default="prefill", choices=["prefill", "random"])
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        args.warmup = min(args.warmup, 1)
+        args.steps = min(args.steps, 3)
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -101,6 +101,23 @@ int ppd_kv_copy(ppd_dev* src, ppd_dev* dst, const int32_t* src_block_table,
                 const int32_t* dst_block_table, int32_t n_blocks, int32_t start,
                 int32_t n_tokens, float* out_ms);
 
+/* ---- instrumentation (CUDA events on the compute stream, per kernel class) ----
+ * With profiling on, every attention launch and every GEMM of a step is
+ * bracketed by CUDA events; ppd_step_wait accumulates the durations. The
+ * counters count launches of this library's own kernels vs library GEMMs. */
+typedef struct ppd_dev_stats {
+  int64_t steps;
+  int64_t own_launches;   /* kernels compiled in libppd_b200.so */
+  int64_t lib_launches;   /* vendor-library launches (cuBLAS GEMM calls) */
+  int64_t attn_launches;
+  double attn_ms, gemm_ms;   /* only with profiling on */
+  double attn_bytes;         /* algorithmic bytes of all attention launches */
+  double step_ms;            /* device time of all steps */
+} ppd_dev_stats;
+int ppd_dev_set_profiling(ppd_dev* dev, int32_t on);
+int ppd_dev_get_stats(ppd_dev* dev, ppd_dev_stats* out);
+int ppd_dev_reset_stats(ppd_dev* dev);
+
 /* ---- kernel-level entry points (device pointers; used by parity tests) ----
  * stream: cudaStream_t or NULL for the legacy default stream. */
 /* attention over a paged pool (num_blocks blocks) for one layer, through the

@@ -63,6 +63,17 @@ def qwen32b_cfg(n_layers: int = 64) -> ModelCfg:
     return ModelCfg(n_layers, 5120, 40, 8, 128, 27648, 152064, 1e-6, 1e6, 1)
 
 
+class DevStats(ctypes.Structure):
+    _fields_ = [
+        ("steps", ctypes.c_int64), ("own_launches", ctypes.c_int64), ("lib_launches", ctypes.c_int64),
+        ("attn_launches", ctypes.c_int64), ("attn_ms", ctypes.c_double), ("gemm_ms", ctypes.c_double),
+        ("attn_bytes", ctypes.c_double), ("step_ms", ctypes.c_double),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class Batch(ctypes.Structure):
     _fields_ = [
         ("n_seqs", ctypes.c_int32), ("q_len", ctypes.c_void_p), ("ctx", ctypes.c_void_p),
@@ -101,6 +112,9 @@ def lib():
             "ppd_op_attention": [P(ModelCfg), vp, vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp],
             "ppd_op_gemm": [vp, vp, vp, i32, i32, i32, i32, vp],
             "ppd_op_fill_random": [vp, u64, u64, i32, i32, vp],
+            "ppd_dev_set_profiling": [vp, i32],
+            "ppd_dev_get_stats": [vp, P(DevStats)],
+            "ppd_dev_reset_stats": [vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -187,6 +201,29 @@ class Device:
         check(lib().ppd_step(self.h, ctypes.byref(b), _ptr(out), ctypes.byref(ms)))
         del keep
         return StepResult(out[:n_out], ms.value)
+
+    def step_submit(self, q_len, ctx, tokens, block_tables, want_token=None):
+        b, keep = self._batch(q_len, ctx, tokens, block_tables, want_token)
+        self._keep = keep
+        check(lib().ppd_step_submit(self.h, ctypes.byref(b)))
+
+    def step_wait(self, n_out: int) -> StepResult:
+        out = np.zeros(max(n_out, 1), dtype=np.int32)
+        ms = ctypes.c_float()
+        check(lib().ppd_step_wait(self.h, _ptr(out), ctypes.byref(ms)))
+        self._keep = None
+        return StepResult(out[:n_out], ms.value)
+
+    def set_profiling(self, on: bool):
+        check(lib().ppd_dev_set_profiling(self.h, 1 if on else 0))
+
+    def stats(self) -> dict:
+        st = DevStats()
+        check(lib().ppd_dev_get_stats(self.h, ctypes.byref(st)))
+        return st.as_dict()
+
+    def reset_stats(self):
+        check(lib().ppd_dev_reset_stats(self.h))
 
     def last_logits(self, n_rows: int) -> np.ndarray:
         out = np.zeros((n_rows, self.cfg.vocab), dtype=np.float32)

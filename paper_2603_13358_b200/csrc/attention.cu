@@ -37,8 +37,7 @@ constexpr int kConsumerWarps = 4;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kBlockBytes = kBT * kDh * 2;                       // 4 KB
 constexpr int kStageBytes = kStageBlocks * 2 * kBlockBytes;      // 32 KB (K and V)
-constexpr int kQBytes = kRows * kDh * 2;                         // 16 KB
-constexpr int kSmemBytes = 1024 + kStages * kStageBytes + kQBytes + 256;
+constexpr int kSmemBytes = 1024 + kStages * kStageBytes + 256;   // 2 CTAs per SM
 
 PPD_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -65,11 +64,6 @@ PPD_DEV uint32_t kv_off(int row, int dim) {
   int chunk = (dim & 63) >> 3;
   return half * 2048 + row * 128 + ((chunk ^ (row & 7)) << 4) + ((dim & 7) << 1);
 }
-// Q tile: 64 rows x 256 B, 16-byte chunk index XOR (row & 7)
-PPD_DEV uint32_t q_off(int row, int dim) {
-  int chunk = dim >> 3;
-  return row * 256 + ((chunk ^ (row & 7)) << 4) + ((dim & 7) << 1);
-}
 
 PPD_DEV void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
@@ -81,13 +75,12 @@ PPD_DEV void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint6
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     paged_attention_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;                                  // kStages * 32 KB
-  uint8_t* q_smem = smem + kStages * kStageBytes;              // 16 KB
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(q_smem + kQBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty_bar = full_bar + kStages;
   int* flag = reinterpret_cast<int*>(empty_bar + kStages);
 
@@ -118,20 +111,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty_bar[i], kConsumerWarps);
     }
     fence_barrier_init();
-  }
-  // Q tile -> shared (swizzled). Rows r: token r / G, head r % G.
-  {
-    const int rows = is_decode ? G : (it.n_q * G);
-    for (int idx = threadIdx.x; idx < kRows * (kDh / 8); idx += kThreads) {
-      int r = idx >> 4, c = idx & 15;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < rows) {
-        int tok = r / G, h = r % G;
-        const bf16* src = p.q + ((size_t)(q_base + it.q_tok0 + tok) * p.n_q_heads + kvh * G + h) * kDh + c * 8;
-        v = *reinterpret_cast<const uint4*>(src);
-      }
-      *reinterpret_cast<uint4*>(q_smem + r * 256 + ((c ^ (r & 7)) << 4)) = v;
-    }
   }
   __syncthreads();
 
@@ -167,14 +146,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int row_base = is_decode ? 0 : warp * 16;
   const float sl2 = p.scale_log2;
 
-  // Q fragments for the 8 k-steps (dims 16kk..16kk+15)
+  // Q fragments for the 8 k-steps, loaded straight from global (row r of the
+  // tile = token r / G, head r % G; rows past the tile are zero)
   uint32_t qa[8][4];
   {
-    int r = row_base + (lane & 7) + ((lane >> 3) & 1) * 8;
+    const int rows = is_decode ? G : (it.n_q * G);
+    const uint32_t* qrow[2];
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+      int r = row_base + g + hr * 8;
+      qrow[hr] = r < rows ? reinterpret_cast<const uint32_t*>(
+                                p.q + ((size_t)(q_base + it.q_tok0 + r / G) * p.n_q_heads + kvh * G + r % G) * kDh)
+                          : nullptr;
+    }
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      int dim = kk * 16 + (lane >> 4) * 8;
-      ldsm_x4(smem_u32(q_smem) + q_off(r, dim), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+      int w0 = (kk * 16 + 2 * t) >> 1;  // 32-bit word index of dims (16kk+2t, +1)
+      qa[kk][0] = qrow[0] ? __ldg(qrow[0] + w0) : 0u;
+      qa[kk][1] = qrow[1] ? __ldg(qrow[1] + w0) : 0u;
+      qa[kk][2] = qrow[0] ? __ldg(qrow[0] + w0 + 4) : 0u;
+      qa[kk][3] = qrow[1] ? __ldg(qrow[1] + w0 + 4) : 0u;
     }
   }
   // causal limit (position) of this thread's two rows

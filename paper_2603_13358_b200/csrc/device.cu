@@ -103,6 +103,12 @@ struct ppd_dev {
   int* d_tokens_out = nullptr;
   int pending = 0;  // sequences of the in-flight step (0 = none)
   int last_logit_rows = 0;
+  // instrumentation
+  bool profiling = false;
+  ppd_dev_stats stats{};
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> prof_marks;  // (kind 0 attn / 1 gemm, first event index)
+  int ev_used = 0;
 };
 
 namespace {
@@ -110,6 +116,7 @@ namespace {
 // ------------------------------------------------------------ metadata
 struct StepLayout {
   int n, T, maxb, n_out, n_items, n_ws;
+  double attn_bytes;  // algorithmic bytes of one attention launch (one layer)
   size_t off_qstart, off_ctx, off_tokens, off_bt, off_rowseq, off_rowpos, off_outrows, off_items,
       total;
 };
@@ -227,6 +234,13 @@ int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnIt
     if (!b->want_token || b->want_token[s]) ++L.n_out;
   }
   CHECK_ARG(L.T <= d->max_T, "batch: sum(q_len) exceeds max_step_tokens");
+  {
+    // unique K/V bytes attended per layer + q in + o out
+    const double kv_tok = 2.0 * d->cfg.n_kv_heads * d->cfg.head_dim * 2;
+    double keys = 0;
+    for (int s = 0; s < L.n; ++s) keys += (double)b->ctx[s] + b->q_len[s];
+    L.attn_bytes = keys * kv_tok + 2.0 * L.T * d->cfg.n_q_heads * d->cfg.head_dim * 2;
+  }
   for (int i = 0; i < L.T; ++i)
     CHECK_ARG(b->tokens[i] >= 0 && b->tokens[i] < d->cfg.vocab, "batch: token id out of range");
   const int G = d->cfg.n_q_heads / d->cfg.n_kv_heads;
@@ -298,6 +312,24 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   return PPD_OK;
 }
 
+int prof_mark(ppd_dev* d, int kind, bool end) {
+  if (!d->profiling) return PPD_OK;
+  if (d->ev_used >= (int)d->ev_pool.size()) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    d->ev_pool.push_back(e);
+  }
+  if (!end) d->prof_marks.push_back({kind, d->ev_used});
+  CU(cudaEventRecord(d->ev_pool[d->ev_used++], d->compute));
+  return PPD_OK;
+}
+
+#define PROF(kind, end)                        \
+  do {                                         \
+    int _rc = prof_mark(d, kind, end);         \
+    if (_rc) return _rc;                       \
+  } while (0)
+
 // The forward pass of one step; metadata already staged in d->d_meta.
 int forward(ppd_dev* d, const StepLayout& L) {
   const ppd_model_cfg& c = d->cfg;
@@ -321,19 +353,34 @@ int forward(ppd_dev* d, const StepLayout& L) {
     // x += down(prev) ; h = norm(x)
     CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, 1, nullptr, d->ones, d->h, T, d_model,
                           c.rms_eps, s));
+    PROF(1, false);
     CU(gemm_run(d->gemm, d->h, w.wqkv, d->qkv32, T, W, d_model, true, s));
+    PROF(1, true);
     CU(launch_rope_kv_write(d->qkv32, 1, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
                             d->rope_sin, d->q, d->kv, T, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers,
                             l, d->bt, s));
+    PROF(0, false);
     int rc = run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_items, l,
                            d->ws_o, d->ws_ml, d->counters, s);
     if (rc) return rc;
+    PROF(0, true);
+    d->stats.attn_bytes += L.attn_bytes;
+    PROF(1, false);
     CU(gemm_run(d->gemm, d->attn, w.wo, d->proj32, T, d_model, qd, true, s));
+    PROF(1, true);
     CU(launch_add_rmsnorm(d->x, d->proj32, 1, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
+    PROF(1, false);
     CU(gemm_run(d->gemm, d->h, w.wgu, d->gu32, T, 2 * F, d_model, true, s));
+    PROF(1, true);
     CU(launch_silu_mul(d->gu32, d->m, T, F, s));
+    PROF(1, false);
     CU(gemm_run(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, true, s));
+    PROF(1, true);
   }
+  // own kernels per layer: add_rmsnorm x2, rope_kv, attention, silu_mul; + embed, final norm, argmax
+  d->stats.own_launches += 5L * c.n_layers + 3;
+  d->stats.lib_launches += 4L * c.n_layers + 1;
+  d->stats.attn_launches += c.n_layers;
   CU(launch_final_norm(d->x, d->down32, 1, nullptr, outrows, L.n_out, d->ones, d->hl, T, d_model,
                        c.rms_eps, s));
   CU(gemm_run(d->gemm, d->hl, d->lm_head, d->logits, L.n_out, c.vocab, d_model, true, s));
@@ -390,6 +437,7 @@ void free_all(ppd_dev* d) {
   cudaEvent_t evs[] = {d->ev0, d->ev1, d->xev0, d->xev1, d->compute_done};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
+  for (auto e : d->ev_pool) cudaEventDestroy(e);
   if (d->compute) cudaStreamDestroy(d->compute);
   if (d->xfer) cudaStreamDestroy(d->xfer);
 }
@@ -567,7 +615,37 @@ int ppd_step_wait(ppd_dev* d, int32_t* out_tokens, float* out_ms) {
   int n = d->pending > 0 ? d->pending : 0;
   d->pending = 0;
   if (out_tokens && n) std::memcpy(out_tokens, d->h_tokens_out, n * 4);
-  if (out_ms) CU(cudaEventElapsedTime(out_ms, d->ev0, d->ev1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
+  if (out_ms) *out_ms = ms;
+  d->stats.steps += 1;
+  d->stats.step_ms += ms;
+  for (auto& mk : d->prof_marks) {
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, d->ev_pool[mk.second], d->ev_pool[mk.second + 1]));
+    (mk.first == 0 ? d->stats.attn_ms : d->stats.gemm_ms) += t;
+  }
+  d->prof_marks.clear();
+  d->ev_used = 0;
+  return PPD_OK;
+}
+
+int ppd_dev_set_profiling(ppd_dev* d, int32_t on) {
+  CHECK_ARG(d, "null dev");
+  if (d->pending) return fail(PPD_ERR_STATE, "cannot toggle profiling with a step in flight");
+  d->profiling = on != 0;
+  return PPD_OK;
+}
+
+int ppd_dev_get_stats(ppd_dev* d, ppd_dev_stats* out) {
+  CHECK_ARG(d && out, "null arg");
+  *out = d->stats;
+  return PPD_OK;
+}
+
+int ppd_dev_reset_stats(ppd_dev* d) {
+  CHECK_ARG(d, "null dev");
+  d->stats = ppd_dev_stats{};
   return PPD_OK;
 }
 
