@@ -1,0 +1,178 @@
+// capi.cpp — JSON front door of the engine (include/ppd_engine.h).
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+
+#include <json.hpp>
+
+#include "../../include/ppd_engine.h"
+#include "ppd/costmodel.hpp"
+#include "ppd/engine.hpp"
+#include "ppd/md5.hpp"
+#include "ppd/metrics.hpp"
+#include "ppd/routing.hpp"
+#include "ppd/simulator.hpp"
+#include "ppd/workload.hpp"
+
+using nlohmann::json;
+using namespace ppd;
+
+namespace {
+
+thread_local std::string g_err;
+
+cost::CalibrationTable calib_from(const json& job) {
+  if (job.contains("calib_json")) return cost::CalibrationTable::from_json(job["calib_json"].get<std::string>());
+  cost::CalibrationTable c = cost::CalibrationTable::defaults();
+  if (job.contains("calib_overrides")) {
+    const json& o = job["calib_overrides"];
+    const std::pair<const char*, double*> fields[] = {
+        {"full_a_lin", &c.full_a_lin},         {"full_b_quad", &c.full_b_quad},
+        {"append_a_lin", &c.append_a_lin},     {"append_b_cross", &c.append_b_cross},
+        {"decode_c_base", &c.decode_c_base},   {"decode_d_batch", &c.decode_d_batch},
+        {"kv_bytes_per_token", &c.kv_bytes_per_token}, {"link_bandwidth", &c.link_bandwidth}};
+    for (const auto& [k, dst] : fields)
+      if (o.contains(k)) *dst = o[k].get<double>();
+    if (o.contains("prefill_service_distribution"))
+      c.prefill_service_distribution = o["prefill_service_distribution"].get<std::string>();
+    c.finalize();
+  }
+  return c;
+}
+
+std::vector<workload::Conversation> convs_from(const json& job) {
+  if (job.contains("workload")) {
+    const json& w = job["workload"];
+    workload::WorkloadSpec s;
+    s.id = w.value("id", std::string("workload"));
+    s.turn1 = {w.at("turn1")[0].get<long>(), w.at("turn1")[1].get<long>()};
+    s.turn2plus = {w.at("turn2plus")[0].get<long>(), w.at("turn2plus")[1].get<long>()};
+    s.num_turns = w.value("num_turns", 2);
+    s.qps = w.value("qps", 1.0);
+    s.duration_s = w.value("duration_s", 10.0);
+    s.think_time_s = w.value("think_time_s", 0.0);
+    s.jitter_pct = w.value("jitter_pct", 0.0);
+    s.category = workload::classify(s.turn2plus);
+    return workload::generate_conversations(s, job.value("seed", std::uint64_t{1}));
+  }
+  std::vector<workload::Conversation> out;
+  for (const json& c : job.at("conversations")) {
+    workload::Conversation cv;
+    cv.conv_id = c.at("conv_id").get<std::string>();
+    cv.first_message_digest = md5(cv.conv_id);
+    long ctx = 0;
+    const double arrival = c.value("arrival", -1.0);
+    for (const json& t : c.at("turns")) {
+      workload::TurnRequest r;
+      r.conv_id = cv.conv_id;
+      r.turn_index = int(cv.turns.size()) + 1;
+      r.new_input_tokens = t[0].get<long>();
+      r.target_output_tokens = t[1].get<long>();
+      r.cached_context_tokens = ctx;
+      r.arrival_time = r.turn_index == 1 ? arrival : -1.0;
+      ctx += r.new_input_tokens + r.target_output_tokens;
+      cv.turns.push_back(r);
+    }
+    out.push_back(std::move(cv));
+  }
+  return out;
+}
+
+routing::RoutingPolicy policy_from(const json& job) {
+  if (job.value("policy", std::string("static")) == "dynamic") {
+    auto t = std::make_shared<routing::DecisionTable>(
+        routing::DecisionTable::from_json(job.at("table_json").get<std::string>()));
+    return routing::RoutingPolicy::dynamic_policy(t);
+  }
+  return routing::RoutingPolicy::static_policy(job.value("x", 0.0));
+}
+
+json agg_json(const metrics::AggregateMetrics& a) {
+  auto o = [](const std::optional<double>& v) { return v ? json(*v) : json(nullptr); };
+  return {{"ttft_t1_mean", o(a.ttft_t1_mean)}, {"ttft_t1_p99", o(a.ttft_t1_p99)},
+          {"ttft_t2_mean", o(a.ttft_t2_mean)}, {"ttft_t2_p99", o(a.ttft_t2_p99)},
+          {"tpot_mean", o(a.tpot_mean)},       {"latency_mean", o(a.latency_mean)},
+          {"tps", a.tps},                      {"success_rate", a.success_rate},
+          {"degraded", a.degraded},            {"total_requests", a.total_requests},
+          {"completed_requests", a.completed_requests},
+          {"ttft_t1_p50", o(a.ttft_t1_p50)},   {"ttft_t2_p50", o(a.ttft_t2_p50)},
+          {"tpot_p50", o(a.tpot_p50)},         {"tpot_p99", o(a.tpot_p99)}};
+}
+
+json result_json(const sim::SimResult& r, const json& job, const std::string& calib_hash, double wall) {
+  std::ostringstream rec;
+  metrics::export_records(rec, job.value("manifest", std::string("{}")), r.records);
+  json ns = json::array();
+  for (const sim::NodeStats& n : r.node_stats)
+    ns.push_back({{"role", std::string(1, n.role)}, {"prefill_busy_s", n.prefill_busy_s},
+                  {"decode_busy_s", n.decode_busy_s}});
+  json kv = json::array();
+  for (const sim::KvTableSnapshot& t : r.kv_tables)
+    kv.push_back({{"node", t.node}, {"conv_id", t.conv_id}, {"tokens", t.tokens}, {"blocks", t.blocks}});
+  const double window = std::max(job.value("window", 0.0), r.makespan);
+  return {{"records_jsonl", rec.str()},
+          {"link_transfers", r.link_transfers},
+          {"link_bytes", r.link_bytes},
+          {"link_queue_delays", r.link_queue_delays},
+          {"node_stats", ns},
+          {"makespan", r.makespan},
+          {"prefill_wait_samples", r.prefill_wait_samples},
+          {"session_miss_fallbacks", r.session_miss_fallbacks},
+          {"aggregate", agg_json(metrics::aggregate(r.records, window))},
+          {"kv_tables", kv},
+          {"route_decisions", r.route_decisions},
+          {"calib_hash", calib_hash},
+          {"wall_s", wall}};
+}
+
+std::string run(const std::string& text) {
+  const json job = json::parse(text);
+  auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
+  sim::ClusterConfig cfg = sim::ClusterConfig::from_name(job.at("cluster").get<std::string>(), policy_from(job), calib);
+  if (job.contains("max_decode_batch")) cfg.max_decode_batch = job["max_decode_batch"].get<int>();
+  if (job.contains("request_timeout_s")) cfg.request_timeout_s = job["request_timeout_s"].get<double>();
+  if (job.contains("kv_blocks_per_node")) cfg.kv_blocks_per_node = job["kv_blocks_per_node"].get<int>();
+  const auto convs = convs_from(job);
+  const double qps_replay = job.value("qps_replay", -1.0);
+  const std::uint64_t seed = job.value("seed", std::uint64_t{1});
+  const double think = job.value("think_time_s", 0.0);
+  const auto t0 = std::chrono::steady_clock::now();
+  if (job.value("clock", std::string("virtual")) == "device") {
+    engine::DeviceOptions opt = engine::DeviceOptions::from_json(job.value("device", json::object()).dump());
+    engine::DeviceRun dr = engine::run_on_device(cfg, convs, qps_replay, seed, think, opt);
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    json out = result_json(dr.sim, job, calib->hash(), wall);
+    out["device"] = json::parse(dr.device_json);
+    return out.dump();
+  }
+  const sim::SimResult r = sim::run_simulation(cfg, convs, qps_replay, seed, think);
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return result_json(r, job, calib->hash(), wall).dump();
+}
+
+}  // namespace
+
+extern "C" {
+
+int ppd_engine_run_json(const char* job_json, char** out_json) {
+  try {
+    const std::string s = run(job_json ? job_json : "");
+    char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    *out_json = buf;
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return -1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -2;
+  }
+}
+
+void ppd_engine_free(char* p) { std::free(p); }
+const char* ppd_engine_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+"""Device clock: the host C++ engine drives real B200 execution (tiny model).
+
+* transfer accounting on the device equals the reference's rule (delta only,
+  simulator.cpp:349-353): x=1 ships only Turn-1 KV, x=0 ships every turn's
+  new tokens; byte counts use the device pool's real bytes/token;
+* every request emits exactly its target tokens; turn-2+ runs append locally
+  under x=1;
+* generated token ids are IDENTICAL to the CPU oracle replaying the engine's
+  own step log (teacher-forced per step; margin-filtered as in test_gpu_model),
+  including steps that read KV shipped P -> D by ppd_kv_copy."""
+import numpy as np
+import pytest
+
+import paper_2603_13358_b200 as ppd
+from paper_2603_13358_b200 import engine as E
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+MARGIN = 0.05
+
+
+def trace(n=3, turns=((40, 6), (24, 5), (17, 4))):
+    return [{"conv_id": f"c{i}", "arrival": 0.01 * i, "turns": [list(t) for t in turns]} for i in range(n)]
+
+
+def dev_job(cluster, x, record_steps=False, **kw):
+    return {"cluster": cluster, "x": x, "clock": "device", "conversations": trace(**kw),
+            "device": {"model": "tiny", "weight_seed": 5, "token_seed": 9, "gpus": [0],
+                       "prefill_chunk": 32, "record_steps": record_steps}}
+
+
+def test_device_replica_completes(gpu):
+    r = E.run(dev_job("1R", 0.0))
+    recs = E.records(r)
+    assert len(recs) == 9 and all(x["status"] == "completed" for x in recs)
+    want = {1: 6, 2: 5, 3: 4}
+    assert all(x["output_tokens_emitted"] == want[x["turn_index"]] for x in recs)
+    toks = r["device"]["tokens"]
+    assert all(len(toks[c][str(t)]) == want[t] for c in toks for t in (1, 2, 3))
+    assert all(x["route"] == "R_local" for x in recs)
+
+
+def test_device_transfer_accounting_matches_reference_rule(gpu):
+    kvb = ppd.kv_block_bytes(ppd.tiny_cfg()) / 16
+    x1 = E.run(dev_job("1P_1D", 1.0))
+    x0 = E.run(dev_job("1P_1D", 0.0))
+    assert x1["link_transfers"] == 3 and x1["link_bytes"] == 3 * 40 * kvb
+    assert x0["link_transfers"] == 9 and x0["link_bytes"] == 3 * (40 + 24 + 17) * kvb
+    # identical to the reference's accounting on the same trace (virtual clock, same bytes/token)
+    from paper_2603_13358_b200 import engine
+    v0 = engine.run({"cluster": "1P_1D", "x": 0.0, "conversations": trace(),
+                     "calib_overrides": {"kv_bytes_per_token": kvb}})
+    assert v0["link_transfers"] == x0["link_transfers"] and v0["link_bytes"] == x0["link_bytes"]
+    r1 = E.records(x1)
+    assert [x["route"] for x in r1 if x["turn_index"] > 1] == ["D_local"] * 6
+    assert x1["device"]["kv_transfer"]["gbs"] > 0
+
+
+def test_device_tokens_match_oracle_replay(gpu):
+    r = E.run(dev_job("1P_1D", 0.5, record_steps=True))
+    log = r["device"]["step_log"]
+    cfg = O.cfg_from(ppd.tiny_cfg())
+    model = O.Model(cfg, 5)
+    nblocks = max(max(e.get("block_tables", [0]) + e.get("src_blocks", [0]) + e.get("dst_blocks", [0]))
+                  for e in log) + 1
+    pools = {}
+    checked = 0
+    for e in log:
+        if e.get("copy"):
+            src = pools.setdefault(e["src"], O.KvPool(cfg, nblocks)).data
+            dst = pools.setdefault(e["dst"], O.KvPool(cfg, nblocks)).data
+            for p in range(e["start"], e["start"] + e["n"]):
+                dst[e["dst_blocks"][p // 16], :, :, :, p % 16] = src[e["src_blocks"][p // 16], :, :, :, p % 16]
+            continue
+        pool = pools.setdefault(e["node"], O.KvPool(cfg, nblocks))
+        n = len(e["q_len"])
+        bt = np.array(e["block_tables"], dtype=np.int32).reshape(n, e["max_blocks"])
+        t_o, _, margin = model.step(pool, e["q_len"], e["ctx"], e["tokens"], bt, want_logits=False)
+        for i in range(n):
+            if e["want"][i] and margin[i] > MARGIN:
+                assert e["out"][i] == t_o[i], (e["node"], i, e["out"][i], t_o[i], margin[i])
+                checked += 1
+    assert checked > 20
