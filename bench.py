@@ -127,6 +127,37 @@ def cpu_port_decode(batch: int, ctx: int, layers_full: int, n_rep: int = 1):
     return batch / t_full, sample, t_sum
 
 
+def engine_ttft(gpu: int, quick: bool = False):
+    """Turn-2+ TTFT / TPOT, PD (x=0) vs PPD (x=1), through the host C++ engine
+    on the DEVICE clock (BASELINE configs[2] shape: 1P:1D, 4 turns, Llama-3-8B
+    shape). Both nodes live on the one visible GPU; each node's clock advances
+    by the CUDA-event time of its own steps and KV hops (the nodes would be
+    separate GPUs of the box). Returns a dict for the JSON line."""
+    from paper_2603_13358_b200 import engine as E
+    wl = {"id": "cfg3", "turn1": [1536, 128], "turn2plus": [1536, 128], "num_turns": 4,
+          "qps": 1.0, "duration_s": 4.0 if quick else 8.0}
+    out = {"cluster": "1P_1D", "workload": wl, "model": "llama-3-8b-shape",
+           "placement": "both nodes on GPU %d; device-clock replay (per-node CUDA-event durations)" % gpu}
+    for x in (0.0, 1.0):
+        job = {"cluster": "1P_1D", "x": x, "clock": "device", "seed": 3, "workload": wl,
+               "device": {"model": "llama8b", "weight_seed": SEED, "token_seed": 3, "gpus": [gpu],
+                          "kv_blocks_per_node": 4096, "prefill_chunk": 2048, "record_tokens": False}}
+        t0 = time.perf_counter()
+        r = E.run(job)
+        agg = r["aggregate"]
+        ms = lambda v: None if v is None else v * 1e3
+        out[f"x{int(x)}"] = {"ttft_t2_p50_ms": ms(agg["ttft_t2_p50"]), "ttft_t2_p99_ms": ms(agg["ttft_t2_p99"]),
+                             "ttft_t2_mean_ms": ms(agg["ttft_t2_mean"]), "tpot_mean_ms": ms(agg["tpot_mean"]),
+                             "tpot_p50_ms": ms(agg["tpot_p50"]), "success_rate": agg["success_rate"],
+                             "link_transfers": r["link_transfers"], "link_gb": r["link_bytes"] / 1e9,
+                             "kv_transfer_gbs": r["device"]["kv_transfer"]["gbs"],
+                             "wall_s": time.perf_counter() - t0}
+    p0, p1 = out["x0"]["ttft_t2_p50_ms"], out["x1"]["ttft_t2_p50_ms"]
+    if p0 and p1:
+        out["ttft_t2_p50_reduction"] = 1.0 - p1 / p0
+    return out
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -254,6 +285,8 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         dev.close()
         return
+    dev.close()
+    ttft = None if args.no_engine else engine_ttft(local_rank, quick=args.quick)
 
     pk, pk_kind = peaks()
     attn_gbs = prof["attn_bytes"] / (prof["attn_ms"] * 1e-3) / 1e9 if prof["attn_ms"] > 0 else None
@@ -293,6 +326,7 @@ def run_ours(args, rank, world, local_rank):
         },
         "tpot_ms": dev_ms_max / K,
         "interference": inter,
+        "ttft_pd_vs_ppd": ttft,
         "roofline": {
             "kernel": "paged_attention_kernel (K1/K2, decode rows)",
             "bound": "hbm",
@@ -319,7 +353,6 @@ def run_ours(args, rank, world, local_rank):
         "prefill_setup_s": prefill_s,
     }
     print(json.dumps(line), flush=True)
-    dev.close()
 
 
 def run_reference(args, rank, world):
@@ -370,6 +403,8 @@ def main():
     ap.add_argument("--cpu-batch", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--fill-kv", default="prefill", choices=["prefill", "random"])
+    ap.add_argument("--no-engine", action="store_true")
+    ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -128,9 +128,14 @@ int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_poo
                      int32_t num_blocks, int32_t block_tokens, int32_t layer, int32_t n_seqs,
                      const int32_t* q_start, const int32_t* ctx, const int32_t* block_tables,
                      int32_t max_blocks, void* out, void* stream);
-/* C[M][N] = A[M][K] . B[N][K]^T ; bf16 in, out_f32 ? fp32 : bf16 out. */
+/* C[M][N] = A[M][K] . B[N][K]^T ; bf16 in, out_f32 ? fp32 : bf16 out.
+ * ppd_op_gemm: the cuBLAS library GEMM (the reference the kernel is tested against);
+ * ppd_op_gemm_tc: the tcgen05/TMEM kernel used by ppd_step; with splits > 1 it
+ * writes `splits` fp32 K-partial slices of M*N floats (their sum is C). */
 int ppd_op_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                 int32_t out_f32, void* stream);
+int ppd_op_gemm_tc(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                   int32_t out_f32, int32_t splits, void* stream);
 /* deterministic random-init fill, identical to the oracle's mo_weight_bf16 */
 int ppd_op_fill_random(void* dst, uint64_t n, uint64_t seed, int32_t tensor, int32_t layer,
                        void* stream);

@@ -111,6 +111,7 @@ def lib():
             "ppd_kv_copy": [vp, vp, vp, vp, i32, i32, i32, P(ctypes.c_float)],
             "ppd_op_attention": [P(ModelCfg), vp, vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp],
             "ppd_op_gemm": [vp, vp, vp, i32, i32, i32, i32, vp],
+            "ppd_op_gemm_tc": [vp, vp, vp, i32, i32, i32, i32, i32, vp],
             "ppd_op_fill_random": [vp, u64, u64, i32, i32, vp],
             "ppd_dev_set_profiling": [vp, i32],
             "ppd_dev_get_stats": [vp, P(DevStats)],

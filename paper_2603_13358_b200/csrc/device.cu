@@ -19,6 +19,7 @@
 
 #include "../../include/ppd_b200.h"
 #include "gemm.h"
+#include "gemm_tc.h"
 #include "kernels.h"
 
 using namespace ppdk;
@@ -346,17 +347,19 @@ int forward(ppd_dev* d, const StepLayout& L) {
   const int* outrows = at<int>(m, L.off_outrows);
   const AttnItem* items = at<AttnItem>(m, L.off_items);
   const int T = L.T;
+  int np_down = 1;
 
   CU(launch_embed(tokens, d->embed, d->x, T, d_model, s));
   for (int l = 0; l < c.n_layers; ++l) {
+    int np_qkv = 1, np_o = 1;
     const Layer& w = d->layers[l];
     // x += down(prev) ; h = norm(x)
-    CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, 1, nullptr, d->ones, d->h, T, d_model,
+    CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, np_down, nullptr, d->ones, d->h, T, d_model,
                           c.rms_eps, s));
     PROF(1, false);
-    CU(gemm_run(d->gemm, d->h, w.wqkv, d->qkv32, T, W, d_model, true, s));
+    CU(gemm_run_split(d->gemm, d->h, w.wqkv, d->qkv32, T, W, d_model, &np_qkv, s));
     PROF(1, true);
-    CU(launch_rope_kv_write(d->qkv32, 1, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
+    CU(launch_rope_kv_write(d->qkv32, np_qkv, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
                             d->rope_sin, d->q, d->kv, T, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers,
                             l, d->bt, s));
     PROF(0, false);
@@ -366,22 +369,25 @@ int forward(ppd_dev* d, const StepLayout& L) {
     PROF(0, true);
     d->stats.attn_bytes += L.attn_bytes;
     PROF(1, false);
-    CU(gemm_run(d->gemm, d->attn, w.wo, d->proj32, T, d_model, qd, true, s));
+    CU(gemm_run_split(d->gemm, d->attn, w.wo, d->proj32, T, d_model, qd, &np_o, s));
     PROF(1, true);
-    CU(launch_add_rmsnorm(d->x, d->proj32, 1, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
+    CU(launch_add_rmsnorm(d->x, d->proj32, np_o, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
     PROF(1, false);
     CU(gemm_run(d->gemm, d->h, w.wgu, d->gu32, T, 2 * F, d_model, true, s));
     PROF(1, true);
     CU(launch_silu_mul(d->gu32, d->m, T, F, s));
     PROF(1, false);
-    CU(gemm_run(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, true, s));
+    CU(gemm_run_split(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, &np_down, s));
     PROF(1, true);
   }
   // own kernels per layer: add_rmsnorm x2, rope_kv, attention, silu_mul; + embed, final norm, argmax
   d->stats.own_launches += 5L * c.n_layers + 3;
-  d->stats.lib_launches += 4L * c.n_layers + 1;
+  if (gemm_uses_tcgen05(d->gemm))
+    d->stats.own_launches += 4L * c.n_layers + 1;
+  else
+    d->stats.lib_launches += 4L * c.n_layers + 1;
   d->stats.attn_launches += c.n_layers;
-  CU(launch_final_norm(d->x, d->down32, 1, nullptr, outrows, L.n_out, d->ones, d->hl, T, d_model,
+  CU(launch_final_norm(d->x, d->down32, np_down, nullptr, outrows, L.n_out, d->ones, d->hl, T, d_model,
                        c.rms_eps, s));
   CU(gemm_run(d->gemm, d->hl, d->lm_head, d->logits, L.n_out, c.vocab, d_model, true, s));
   CU(launch_argmax(d->logits, L.n_out, c.vocab, d->d_tokens_out, s));
@@ -398,10 +404,12 @@ int alloc_workspaces(ppd_dev* d) {
   CU(cudaMalloc(&d->attn, T * qd * 2));
   CU(cudaMalloc(&d->m, T * c.d_ff * 2));
   CU(cudaMalloc(&d->hl, S * c.d_model * 2));
-  CU(cudaMalloc(&d->qkv32, T * (qd + 2 * kd) * 4));
-  CU(cudaMalloc(&d->proj32, T * c.d_model * 4));
+  // fp32 GEMM outputs also hold up to 8 K-split partial slices of a <=256-token step
+  const size_t Tp = std::max<size_t>(T, 8 * 256);
+  CU(cudaMalloc(&d->qkv32, Tp * (qd + 2 * kd) * 4));
+  CU(cudaMalloc(&d->proj32, Tp * c.d_model * 4));
   CU(cudaMalloc(&d->gu32, T * 2 * c.d_ff * 4));
-  CU(cudaMalloc(&d->down32, T * c.d_model * 4));
+  CU(cudaMalloc(&d->down32, Tp * c.d_model * 4));
   CU(cudaMalloc(&d->logits, S * c.vocab * 4));
   CU(cudaMalloc(&d->counters, S * c.n_kv_heads * 4));
   CU(cudaMemset(d->counters, 0, S * c.n_kv_heads * 4));
@@ -791,8 +799,19 @@ int ppd_op_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int
   static thread_local GemmContext* ctx = nullptr;
   if (!ctx) ctx = gemm_create();
   if (!ctx) return fail(PPD_ERR_CUDA, "gemm context");
-  CU(gemm_run(ctx, static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0,
-              static_cast<cudaStream_t>(stream)));
+  CU(gemm_run_cublas(ctx, static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0,
+                     static_cast<cudaStream_t>(stream)));
+  CU(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  return PPD_OK;
+}
+
+int ppd_op_gemm_tc(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t out_f32,
+                   int32_t splits, void* stream) {
+  CHECK_ARG(A && B && C && M > 0 && N > 0 && K > 0 && splits >= 1, "bad gemm args");
+  CHECK_ARG(K % 8 == 0, "K must be a multiple of 8");
+  CHECK_ARG(splits == 1 || out_f32, "K-split partials need fp32 output");
+  CU(gemm_tc_run(static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0, splits,
+                 (size_t)M * N, static_cast<cudaStream_t>(stream)));
   CU(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return PPD_OK;
 }

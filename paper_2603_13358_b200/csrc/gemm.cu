@@ -1,14 +1,18 @@
-// gemm.cu — K5 GEMM dispatch. Stage 1: cuBLAS (library GEMM) so the whole
-// forward step is correct end to end; the hand-written tcgen05/TMEM kernel
-// (gemm_tc.cu) replaces it shape by shape once it is parity-green against this.
+// gemm.cu — K5 GEMM dispatch: tcgen05 kernel (gemm_tc.cu) by default, cuBLAS
+// as the library reference the tcgen05 path is parity-tested against.
 #include <cublas_v2.h>
 
+#include <cstdlib>
+#include <cstring>
+
 #include "gemm.h"
+#include "gemm_tc.h"
 
 namespace ppdk {
 
 struct GemmContext {
   cublasHandle_t handle = nullptr;
+  bool tc = true;
 };
 
 GemmContext* gemm_create() {
@@ -17,7 +21,8 @@ GemmContext* gemm_create() {
     delete c;
     return nullptr;
   }
-  cublasSetMathMode(c->handle, CUBLAS_DEFAULT_MATH);
+  const char* e = std::getenv("PPD_GEMM");
+  c->tc = !(e && std::strcmp(e, "cublas") == 0);
   return c;
 }
 
@@ -27,17 +32,35 @@ void gemm_destroy(GemmContext* c) {
   delete c;
 }
 
-cudaError_t gemm_run(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M,
-                     int N, int K, bool out_f32, cudaStream_t s) {
+bool gemm_uses_tcgen05(const GemmContext* c) { return c && c->tc; }
+
+cudaError_t gemm_run_cublas(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N,
+                            int K, bool out_f32, cudaStream_t s) {
   if (M == 0) return cudaSuccess;
   cublasSetStream(c->handle, s);
   const float alpha = 1.f, beta = 0.f;
   // row-major C[M][N] = A B^T  <=>  column-major C^T[N][M] = B^T(op T of [K][N]) . A
-  cublasStatus_t st = cublasGemmEx(c->handle, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, B,
-                                   CUDA_R_16BF, K, A, CUDA_R_16BF, K, &beta, C,
-                                   out_f32 ? CUDA_R_32F : CUDA_R_16BF, N, CUBLAS_COMPUTE_32F,
-                                   CUBLAS_GEMM_DEFAULT);
+  cublasStatus_t st = cublasGemmEx(c->handle, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, B, CUDA_R_16BF, K, A,
+                                   CUDA_R_16BF, K, &beta, C, out_f32 ? CUDA_R_32F : CUDA_R_16BF, N,
+                                   CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
   return st == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown;
+}
+
+cudaError_t gemm_run(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N, int K,
+                     bool out_f32, cudaStream_t s) {
+  if (!c->tc) return gemm_run_cublas(c, A, B, C, M, N, K, out_f32, s);
+  return gemm_tc_run(A, B, C, M, N, K, out_f32, 1, 0, s);
+}
+
+cudaError_t gemm_run_split(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, float* C, int M, int N,
+                           int K, int* n_part, cudaStream_t s) {
+  if (!c->tc) {
+    *n_part = 1;
+    return gemm_run_cublas(c, A, B, C, M, N, K, true, s);
+  }
+  const int splits = gemm_tc_plan_splits(M, N, K);
+  *n_part = splits;
+  return gemm_tc_run(A, B, C, M, N, K, true, splits, (size_t)M * N, s);
 }
 
 }  // namespace ppdk

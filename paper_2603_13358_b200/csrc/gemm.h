@@ -1,13 +1,23 @@
 // gemm.h — K5 projection / MLP / lm_head GEMMs: C[M][N] = A[M][K] . B[N][K]^T,
-// bf16 operands, fp32 accumulate, fp32 or bf16 output.
+// bf16 operands, fp32 accumulate. Default path: the hand-written tcgen05 kernel
+// (gemm_tc.cu); PPD_GEMM=cublas selects the cuBLAS reference path (tests).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <stddef.h>
 
 namespace ppdk {
 struct GemmContext;
 GemmContext* gemm_create();
 void gemm_destroy(GemmContext* ctx);
-cudaError_t gemm_run(GemmContext* ctx, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C,
-                     int M, int N, int K, bool out_f32, cudaStream_t s);
+bool gemm_uses_tcgen05(const GemmContext* ctx);
+// single-slice product (no K split)
+cudaError_t gemm_run(GemmContext* ctx, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N,
+                     int K, bool out_f32, cudaStream_t s);
+// fp32 product written as *n_part K-split partial slices of M*N floats each
+// (the consumer sums them); the split count fills the SMs for small M.
+cudaError_t gemm_run_split(GemmContext* ctx, const __nv_bfloat16* A, const __nv_bfloat16* B, float* C, int M, int N,
+                           int K, int* n_part, cudaStream_t s);
+cudaError_t gemm_run_cublas(GemmContext* ctx, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M,
+                            int N, int K, bool out_f32, cudaStream_t s);
 }  // namespace ppdk
