@@ -119,7 +119,8 @@ int ppd_dev_get_stats(ppd_dev* dev, ppd_dev_stats* out);
 int ppd_dev_reset_stats(ppd_dev* dev);
 
 /* ---- kernel-level entry points (device pointers; used by parity tests) ----
- * stream: cudaStream_t or NULL for the legacy default stream. */
+ * stream: cudaStream_t or NULL for the legacy default stream. The GEMM ops are
+ * asynchronous on that stream; the others synchronise before returning. */
 /* attention over a paged pool (num_blocks blocks) for one layer, through the
  * same work-item builder and kernel as ppd_step. q [total_q][Hq][Dh] bf16
  * (roped, device), out same shape bf16 (device). q_start [n_seqs+1], ctx

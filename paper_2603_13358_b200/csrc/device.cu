@@ -13,8 +13,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <map>
+#include <tuple>
 #include <vector>
 
 #include "../../include/ppd_b200.h"
@@ -104,6 +107,11 @@ struct ppd_dev {
   int* d_tokens_out = nullptr;
   int pending = 0;  // sequences of the in-flight step (0 = none)
   int last_logit_rows = 0;
+  // CUDA graphs of the forward pass, keyed by the step's shape (the metadata
+  // contents change per step; the pointers and launch parameters do not)
+  std::map<std::tuple<int, int, int, int, int, int>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<int, int, int, int, int, int>, int> shape_seen;
+  bool use_graphs = true;
   // instrumentation
   bool profiling = false;
   ppd_dev_stats stats{};
@@ -179,6 +187,11 @@ void build_items(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads
   }
 }
 
+void clear_graphs(ppd_dev* d) {
+  for (auto& kv : d->graphs) cudaGraphExecDestroy(kv.second);
+  d->graphs.clear();
+}
+
 int ensure_meta(ppd_dev* d, size_t bytes) {
   if (bytes <= d->meta_cap) return PPD_OK;
   size_t cap = align_up(bytes * 2, 1 << 20);
@@ -189,6 +202,7 @@ int ensure_meta(ppd_dev* d, size_t bytes) {
   CU(cudaMallocHost(&d->h_meta, cap));
   CU(cudaMalloc(&d->d_meta, cap));
   d->meta_cap = cap;
+  clear_graphs(d);
   return PPD_OK;
 }
 
@@ -203,6 +217,7 @@ int ensure_ws(ppd_dev* d, int slots) {
   CU(cudaMalloc(&d->ws_o, (size_t)cap * d->cfg.n_kv_heads * G * 128 * sizeof(float)));
   CU(cudaMalloc(&d->ws_ml, (size_t)cap * d->cfg.n_kv_heads * G * 2 * sizeof(float)));
   d->ws_slots = cap;
+  clear_graphs(d);
   return PPD_OK;
 }
 
@@ -313,6 +328,18 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   return PPD_OK;
 }
 
+void count_launches(ppd_dev* d, const StepLayout& L) {
+  const long nl = d->cfg.n_layers;
+  // own kernels per layer: add_rmsnorm x2, rope_kv, attention, silu_mul; + embed, final norm, argmax
+  d->stats.own_launches += 5 * nl + 3;
+  if (gemm_uses_tcgen05(d->gemm))
+    d->stats.own_launches += 4 * nl + 1;
+  else
+    d->stats.lib_launches += 4 * nl + 1;
+  d->stats.attn_launches += nl;
+  d->stats.attn_bytes += L.attn_bytes * nl;
+}
+
 int prof_mark(ppd_dev* d, int kind, bool end) {
   if (!d->profiling) return PPD_OK;
   if (d->ev_used >= (int)d->ev_pool.size()) {
@@ -367,7 +394,6 @@ int forward(ppd_dev* d, const StepLayout& L) {
                            d->ws_o, d->ws_ml, d->counters, s);
     if (rc) return rc;
     PROF(0, true);
-    d->stats.attn_bytes += L.attn_bytes;
     PROF(1, false);
     CU(gemm_run_split(d->gemm, d->attn, w.wo, d->proj32, T, d_model, qd, &np_o, s));
     PROF(1, true);
@@ -380,13 +406,7 @@ int forward(ppd_dev* d, const StepLayout& L) {
     CU(gemm_run_split(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, &np_down, s));
     PROF(1, true);
   }
-  // own kernels per layer: add_rmsnorm x2, rope_kv, attention, silu_mul; + embed, final norm, argmax
-  d->stats.own_launches += 5L * c.n_layers + 3;
-  if (gemm_uses_tcgen05(d->gemm))
-    d->stats.own_launches += 4L * c.n_layers + 1;
-  else
-    d->stats.lib_launches += 4L * c.n_layers + 1;
-  d->stats.attn_launches += c.n_layers;
+  count_launches(d, L);
   CU(launch_final_norm(d->x, d->down32, np_down, nullptr, outrows, L.n_out, d->ones, d->hl, T, d_model,
                        c.rms_eps, s));
   CU(gemm_run(d->gemm, d->hl, d->lm_head, d->logits, L.n_out, c.vocab, d_model, true, s));
@@ -446,6 +466,7 @@ void free_all(ppd_dev* d) {
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
   for (auto e : d->ev_pool) cudaEventDestroy(e);
+  clear_graphs(d);
   if (d->compute) cudaStreamDestroy(d->compute);
   if (d->xfer) cudaStreamDestroy(d->xfer);
 }
@@ -489,6 +510,7 @@ int ppd_dev_open(int32_t gpu, const ppd_model_cfg* cfg, int32_t max_step_tokens,
   d->cfg = *cfg;
   d->max_T = max_step_tokens;
   d->max_S = max_step_seqs;
+  if (const char* g = std::getenv("PPD_GRAPHS")) d->use_graphs = std::strcmp(g, "0") != 0;
   auto bail = [&](int code) {
     free_all(d);
     delete d;
@@ -604,8 +626,32 @@ int ppd_step_submit(ppd_dev* d, const ppd_batch* b) {
   if (rc) return rc;
   CU(cudaMemcpyAsync(d->d_meta, d->h_meta, L.total, cudaMemcpyHostToDevice, d->compute));
   CU(cudaEventRecord(d->ev0, d->compute));
-  rc = forward(d, L);
-  if (rc) return rc;
+  // repeated shapes replay a captured graph (decode steps: ~300 launches -> 1)
+  const auto key = std::make_tuple(L.n, L.T, L.maxb, L.n_out, L.n_items, L.n_ws);
+  const bool graph_ok = d->use_graphs && !d->profiling && d->shape_seen[key]++ > 0;
+  if (graph_ok) {
+    auto it = d->graphs.find(key);
+    if (it == d->graphs.end()) {
+      if (d->graphs.size() >= 64) clear_graphs(d);
+      cudaGraph_t g = nullptr;
+      CU(cudaStreamBeginCapture(d->compute, cudaStreamCaptureModeThreadLocal));
+      const ppd_dev_stats saved = d->stats;
+      rc = forward(d, L);
+      d->stats = saved;  // launches are counted when the graph runs
+      cudaError_t ce = cudaStreamEndCapture(d->compute, &g);
+      if (rc) return rc;
+      CU(ce);
+      cudaGraphExec_t ge = nullptr;
+      CU(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      it = d->graphs.emplace(key, ge).first;
+    }
+    CU(cudaGraphLaunch(it->second, d->compute));
+    count_launches(d, L);
+  } else {
+    rc = forward(d, L);
+    if (rc) return rc;
+  }
   CU(cudaEventRecord(d->ev1, d->compute));
   CU(cudaMemcpyAsync(d->h_tokens_out, d->d_tokens_out, L.n_out * 4, cudaMemcpyDeviceToHost,
                      d->compute));
@@ -801,7 +847,6 @@ int ppd_op_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int
   if (!ctx) return fail(PPD_ERR_CUDA, "gemm context");
   CU(gemm_run_cublas(ctx, static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0,
                      static_cast<cudaStream_t>(stream)));
-  CU(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return PPD_OK;
 }
 
@@ -812,7 +857,6 @@ int ppd_op_gemm_tc(const void* A, const void* B, void* C, int32_t M, int32_t N, 
   CHECK_ARG(splits == 1 || out_f32, "K-split partials need fp32 output");
   CU(gemm_tc_run(static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0, splits,
                  (size_t)M * N, static_cast<cudaStream_t>(stream)));
-  CU(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return PPD_OK;
 }
 

@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -86,6 +87,12 @@ PPD_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
 
 }  // namespace
 
+// Persistent: grid = min(units, 148); CTA c processes units c, c + grid, ...
+// where a unit is (weight tile, token tile, K split), weight-tile-major so the
+// CTAs running concurrently share weight tiles and token tiles through L2. The
+// producer streams stages across unit boundaries without draining; the MMA
+// warp alternates between two TMEM accumulators (when 2*BN <= 512 columns) so
+// the epilogue of unit i overlaps the MMAs of unit i+1.
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                    GemmTcParams p) {
@@ -96,25 +103,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int stage_bytes = kWBytes + x_bytes;  // both multiples of 1 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
-  uint64_t* tmem_full = empty + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + S;   // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * kBM;        // weight rows
-  const int t0 = blockIdx.y * p.bn;       // tokens
-  const int split = blockIdx.z;
+  const int n_tiles_w = (p.N + kBM - 1) / kBM;
+  const int n_tiles_t = (p.T + p.bn - 1) / p.bn;
+  const int n_units = n_tiles_w * n_tiles_t * p.splits;
   const int kb_total = (p.K + kBK - 1) / kBK;
   const int kb_per = (kb_total + p.splits - 1) / p.splits;
-  const int kb0 = split * kb_per;
-  const int kb1 = min(kb_total, kb0 + kb_per);
-  const int nkb = max(0, kb1 - kb0);
+  const int n_acc = p.tmem_cols >= 2 * p.bn_cols ? 2 : 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4);  // one arrive per epilogue warp
+    }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -127,66 +136,97 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // unit -> (weight tile, token tile, split); token tile fastest
+  auto decode_unit = [&](int u, int& tw, int& tt, int& sp) {
+    sp = u % p.splits;
+    const int rest = u / p.splits;
+    tt = rest % n_tiles_t;
+    tw = rest / n_tiles_t;
+  };
+
   if (warp == 0) {
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % S;
-        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
-        uint8_t* sw = smem + s * stage_bytes;
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
-        const int k = (kb0 + i) * kBK;
-        tma_load_2d(sw, &map_w, k, n0, &full[s]);
-        tma_load_2d(sw + kWBytes, &map_x, k, t0, &full[s]);
+      int it = 0;  // global stage counter across units
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int tw, tt, sp;
+        decode_unit(u, tw, tt, sp);
+        const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % S;
+          if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+          uint8_t* sw = smem + s * stage_bytes;
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          tma_load_2d(sw, &map_w, kb * kBK, tw * kBM, &full[s]);
+          tma_load_2d(sw + kWBytes, &map_x, kb * kBK, tt * p.bn, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.bn >> 3) << 17) |
                              ((uint32_t)(kBM >> 4) << 24);
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % S;
-        mbar_wait(&full[s], (i / S) & 1);
+      int it = 0, j = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
+        int tw, tt, sp;
+        decode_unit(u, tw, tt, sp);
+        const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+        const int acc = j % n_acc;
+        const int use = j / n_acc;  // how many times this accumulator was used before
+        if (use > 0) mbar_wait(&acc_empty[acc], (use - 1) & 1);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * stage_bytes);
-        const uint64_t da = sw128_kmajor_desc(sa);
-        const uint64_t db = sw128_kmajor_desc(sa + kWBytes);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn_cols);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % S;
+          mbar_wait(&full[s], (it / S) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * stage_bytes);
+          const uint64_t da = sw128_kmajor_desc(sa);
+          const uint64_t db = sw128_kmajor_desc(sa + kWBytes);
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k)  // 32 B per UMMA_K step inside the swizzle atom
-          mma_bf16(tmem_base, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (i | k) != 0);
-        mma_commit(&empty[s]);  // smem slot free once these MMAs retire
+          for (int k = 0; k < kBK / 16; ++k)  // 32 B per UMMA_K step inside the swizzle atom
+            mma_bf16(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (kb != kb0) || (k != 0));
+          mma_commit(&empty[s]);  // smem slot free once these MMAs retire
+        }
+        mma_commit(&acc_full[acc]);
       }
-      mma_commit(tmem_full);
     }
   } else if (warp >= 4) {
     const int q = warp & 3;  // TMEM lane quarter owned by this warp
-    const int row = n0 + q * 32 + lane;
-    if (nkb > 0) {
-      mbar_wait(tmem_full, 0);
+    int j = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
+      int tw, tt, sp;
+      decode_unit(u, tw, tt, sp);
+      const int acc = j % n_acc;
+      const int use = j / n_acc;
+      const int row = tw * kBM + q * 32 + lane;
+      const int t0 = tt * p.bn;
+      mbar_wait(&acc_full[acc], use & 1);
       tc_fence_after();
-    }
-    float* out32 = reinterpret_cast<float*>(p.out) + (size_t)split * p.split_stride;
-    __nv_bfloat16* out16 = reinterpret_cast<__nv_bfloat16*>(p.out);
-    for (int c0 = 0; c0 < p.bn; c0 += 32) {
-      uint32_t r[32];
-      if (nkb > 0) {
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
-      } else {
+      float* out32 = reinterpret_cast<float*>(p.out) + (size_t)sp * p.split_stride;
+      __nv_bfloat16* out16 = reinterpret_cast<__nv_bfloat16*>(p.out);
+      const uint32_t t_acc = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * p.bn_cols);
+      const int ncols = min(p.bn, p.T - t0);
+      for (int c0 = 0; c0 < ncols; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(t_acc + (uint32_t)c0, r);
+        if (row < p.N) {
+          const int nj = min(32, ncols - c0);
+          if (p.out_f32) {
+            float* dst = out32 + (size_t)(t0 + c0) * p.ldo + row;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = 0u;
-      }
-      if (row < p.N) {
+            for (int jj = 0; jj < 32; ++jj)
+              if (jj < nj) dst[(size_t)jj * p.ldo] = __uint_as_float(r[jj]);
+          } else {
+            __nv_bfloat16* dst = out16 + (size_t)(t0 + c0) * p.ldo + row;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int tok = t0 + c0 + j;
-          if (c0 + j < p.bn && tok < p.T) {
-            const float v = __uint_as_float(r[j]);
-            if (p.out_f32)
-              out32[(size_t)tok * p.ldo + row] = v;
-            else
-              out16[(size_t)tok * p.ldo + row] = __float2bfloat16_rn(v);
+            for (int jj = 0; jj < 32; ++jj)
+              if (jj < nj) dst[(size_t)jj * p.ldo] = __float2bfloat16_rn(__uint_as_float(r[jj]));
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
     }
   }
   tc_fence_before();
@@ -281,10 +321,17 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
   p.out_f32 = out_f32 ? 1 : 0;
   p.splits = splits;
   p.split_stride = split_stride ? split_stride : (size_t)T * N;
-  p.tmem_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+  // accumulator columns per unit (power of two >= bn); two accumulators when they fit
+  p.bn_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+  p.tmem_cols = 2 * p.bn_cols <= 512 ? 2 * p.bn_cols : p.bn_cols;
   const int stage_bytes = kWBytes + bn * kBK * 2;
   int stages = kSmemBudget / stage_bytes;
   stages = stages > kMaxStages ? kMaxStages : stages;
+  static const int stage_cap = [] {
+    const char* e = std::getenv("PPD_GEMM_STAGES");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (stage_cap > 0 && stage_cap < stages) stages = stage_cap;
   p.stages = stages;
   const int smem = 1024 + stages * stage_bytes + 256;
   CUtensorMap mw, mx;
@@ -294,7 +341,8 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 + kSmemBudget + 256);
     attr = true;
   }
-  dim3 grid((N + kBM - 1) / kBM, (T + bn - 1) / bn, splits);
+  const int units = ((N + kBM - 1) / kBM) * ((T + bn - 1) / bn) * splits;
+  const int grid = units < 148 ? units : 148;
   gemm_tc_kernel<<<grid, kThreads, smem, s>>>(mw, mx, p);
   return cudaGetLastError();
 }

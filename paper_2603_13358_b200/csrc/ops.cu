@@ -192,6 +192,32 @@ cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, int n_part,
 }
 
 // ------------------------------------------------------- RoPE + KV write
+// One CTA per token row. Each thread owns 4 consecutive rotary pairs (i..i+3,
+// i+64..i+67) of one q/k head, or 4 consecutive dims of one v head, and reads
+// the fp32 GEMM output (all K-split partial slices) with 16-byte loads.
+PPD_DEV float4 ld_sum4(const float* base, int n_part, size_t part_stride, const float* bias, int col) {
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int pp = 0; pp < n_part; ++pp) {
+    const float4 v = *reinterpret_cast<const float4*>(base + pp * part_stride + col);
+    a.x = __fadd_rn(a.x, v.x);
+    a.y = __fadd_rn(a.y, v.y);
+    a.z = __fadd_rn(a.z, v.z);
+    a.w = __fadd_rn(a.w, v.w);
+  }
+  if (bias) {
+    const float4 b = *reinterpret_cast<const float4*>(bias + col);
+    a.x = __fadd_rn(a.x, b.x);
+    a.y = __fadd_rn(a.y, b.y);
+    a.z = __fadd_rn(a.z, b.z);
+    a.w = __fadd_rn(a.w, b.w);
+  }
+  return make_float4(rbf(a.x), rbf(a.y), rbf(a.z), rbf(a.w));
+}
+
+PPD_DEV void st_bf16x4(bf16* dst, float a, float b, float c, float d) {
+  *reinterpret_cast<uint2*>(dst) = make_uint2(pack2(a, b), pack2(c, d));
+}
+
 __global__ void rope_kv_kernel(const float* qkv, int n_part, size_t part_stride, const float* bias,
                                const int* row_seq, const int* row_pos, const int* block_tables,
                                int max_blocks, const float* rope_cos, const float* rope_sin,
@@ -205,37 +231,41 @@ __global__ void rope_kv_kernel(const float* qkv, int n_part, size_t part_stride,
   const int tok = pos % BT;
   const float* cs = rope_cos + (size_t)pos * half;
   const float* sn = rope_sin + (size_t)pos * half;
-  auto val = [&](int col) {
-    float a = 0.f;
-    for (int pp = 0; pp < n_part; ++pp) a = __fadd_rn(a, qkv[pp * part_stride + (size_t)r * W + col]);
-    if (bias) a = __fadd_rn(a, bias[col]);
-    return rbf(a);
-  };
-  // rotary pairs of q heads and k heads
-  const int n_pairs = (Hq + Hkv) * half;
-  for (int i = threadIdx.x; i < n_pairs; i += blockDim.x) {
-    int head = i / half, j = i % half;
-    int col = head * Dh + j;  // k heads follow q heads contiguously in the fused layout
-    float x1 = val(col), x2 = val(col + half);
-    float c = cs[j], sv = sn[j];
-    float o1 = rbf(__fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, sv)));
-    float o2 = rbf(__fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, sv)));
-    if (head < Hq) {
-      bf16* q = q_out + ((size_t)r * Hq + head) * Dh;
-      q[j] = f2bf(o1);
-      q[j + half] = f2bf(o2);
+  const float* row = qkv + (size_t)r * W;
+  const int per_head = half / 4;                 // rotary units per head
+  const int n_rot = (Hq + Hkv) * per_head;
+  const int n_v = kd / 4;
+  for (int u = threadIdx.x; u < n_rot + n_v; u += blockDim.x) {
+    if (u < n_rot) {
+      const int head = u / per_head, i = (u % per_head) * 4;
+      const int col = head * Dh + i;  // k heads follow q heads in the fused layout
+      const float4 x1 = ld_sum4(row, n_part, part_stride, bias, col);
+      const float4 x2 = ld_sum4(row, n_part, part_stride, bias, col + half);
+      const float4 c = *reinterpret_cast<const float4*>(cs + i);
+      const float4 sv = *reinterpret_cast<const float4*>(sn + i);
+      const float a0 = rbf(__fsub_rn(__fmul_rn(x1.x, c.x), __fmul_rn(x2.x, sv.x)));
+      const float a1 = rbf(__fsub_rn(__fmul_rn(x1.y, c.y), __fmul_rn(x2.y, sv.y)));
+      const float a2 = rbf(__fsub_rn(__fmul_rn(x1.z, c.z), __fmul_rn(x2.z, sv.z)));
+      const float a3 = rbf(__fsub_rn(__fmul_rn(x1.w, c.w), __fmul_rn(x2.w, sv.w)));
+      const float b0 = rbf(__fadd_rn(__fmul_rn(x2.x, c.x), __fmul_rn(x1.x, sv.x)));
+      const float b1 = rbf(__fadd_rn(__fmul_rn(x2.y, c.y), __fmul_rn(x1.y, sv.y)));
+      const float b2 = rbf(__fadd_rn(__fmul_rn(x2.z, c.z), __fmul_rn(x1.z, sv.z)));
+      const float b3 = rbf(__fadd_rn(__fmul_rn(x2.w, c.w), __fmul_rn(x1.w, sv.w)));
+      bf16* dst;
+      if (head < Hq) {
+        dst = q_out + ((size_t)r * Hq + head) * Dh;
+      } else {
+        dst = kv + ((((size_t)blk * n_layers + layer) * 2 + 0) * Hkv + (head - Hq)) * BT * Dh + (size_t)tok * Dh;
+      }
+      st_bf16x4(dst + i, a0, a1, a2, a3);
+      st_bf16x4(dst + i + half, b0, b1, b2, b3);
     } else {
-      int hk = head - Hq;
-      bf16* k = kv + ((((size_t)blk * n_layers + layer) * 2 + 0) * Hkv + hk) * BT * Dh + (size_t)tok * Dh;
-      k[j] = f2bf(o1);
-      k[j + half] = f2bf(o2);
+      const int v = (u - n_rot) * 4;
+      const int hk = v / Dh, dd = v % Dh;
+      const float4 x = ld_sum4(row, n_part, part_stride, bias, qd + kd + v);
+      bf16* dst = kv + ((((size_t)blk * n_layers + layer) * 2 + 1) * Hkv + hk) * BT * Dh + (size_t)tok * Dh + dd;
+      st_bf16x4(dst, x.x, x.y, x.z, x.w);
     }
-  }
-  for (int i = threadIdx.x; i < kd; i += blockDim.x) {
-    int hk = i / Dh, dd = i % Dh;
-    float v = val(qd + kd + i);
-    bf16* vp = kv + ((((size_t)blk * n_layers + layer) * 2 + 1) * Hkv + hk) * BT * Dh + (size_t)tok * Dh;
-    vp[dd] = f2bf(v);
   }
 }
 
@@ -253,20 +283,25 @@ cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias
 }
 
 // ------------------------------------------------------------- SiLU * up
+// gate/up come interleaved in 64-column groups (launch_fill_gate_up layout);
+// each thread produces 4 outputs from one float4 of gate and one of up.
 __global__ void silu_mul_kernel(const float* gu, bf16* m, int F) {
   const int r = blockIdx.y;
   const float* row = gu + (size_t)r * 2 * F;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
-    int grp = j >> 6, within = j & 63;
-    float g = row[grp * 128 + within];
-    float u = row[grp * 128 + 64 + within];
-    float sv = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-    m[(size_t)r * F + j] = f2bf(__fmul_rn(sv, u));
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4) {
+    const int grp = j >> 6, within = j & 63;
+    const float4 g = *reinterpret_cast<const float4*>(row + grp * 128 + within);
+    const float4 u = *reinterpret_cast<const float4*>(row + grp * 128 + 64 + within);
+    const float gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
+    float o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = __fmul_rn(__fdiv_rn(gv[e], __fadd_rn(1.0f, expf(-gv[e]))), uv[e]);
+    st_bf16x4(m + (size_t)r * F + j, o[0], o[1], o[2], o[3]);
   }
 }
 cudaError_t launch_silu_mul(const float* gu, bf16* m, int T, int F, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  dim3 grid((F + 255) / 256, T);
+  dim3 grid((F / 4 + 255) / 256, T);
   silu_mul_kernel<<<grid, 256, 0, s>>>(gu, m, F);
   return cudaGetLastError();
 }
