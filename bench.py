@@ -101,15 +101,16 @@ def cpu_port_decode(batch: int, ctx: int, layers_full: int, n_rep: int = 1):
     from oracle import oracle as O
     t_sum = 0.0
     times = {}
+    cfg = O.MoCfg(2, 4096, 32, 8, 128, 14336, 128256, 1e-5, 5e5, 0)
+    m = O.Model(cfg, SEED)
+    nbps = (ctx + 1 + 15) // 16
+    pool = O.KvPool(cfg, batch * nbps)
+    rng = np.random.default_rng(1)
+    pool.data[...] = O.f32_to_bf16((rng.standard_normal(pool.data.shape, dtype=np.float32) * 0.5))
+    bts = np.arange(batch * nbps, dtype=np.int32).reshape(batch, nbps)
+    toks = rng.integers(0, cfg.vocab, batch).astype(np.int32)
     for nl in (1, 2):
-        cfg = O.MoCfg(nl, 4096, 32, 8, 128, 14336, 128256, 1e-5, 5e5, 0)
-        m = O.Model(cfg, SEED)
-        nbps = (ctx + 1 + 15) // 16
-        pool = O.KvPool(cfg, batch * nbps)
-        rng = np.random.default_rng(1)
-        pool.data[...] = O.f32_to_bf16((rng.standard_normal(pool.data.shape, dtype=np.float32) * 0.5))
-        bts = np.arange(batch * nbps, dtype=np.int32).reshape(batch, nbps)
-        toks = rng.integers(0, cfg.vocab, batch).astype(np.int32)
+        m.set_active_layers(nl)
         best = None
         for _ in range(n_rep):
             t0 = time.perf_counter()
@@ -118,7 +119,7 @@ def cpu_port_decode(batch: int, ctx: int, layers_full: int, n_rep: int = 1):
             best = dt if best is None else min(best, dt)
             t_sum += dt
         times[nl] = best
-        del m
+    del m
     t_layer = max(times[2] - times[1], 1e-9)
     t_head = max(times[1] - t_layer, 0.0)
     t_full = t_head + layers_full * t_layer
@@ -400,7 +401,7 @@ def main():
     ap.add_argument("--batch", type=int, default=200)
     ap.add_argument("--ctx", type=int, default=1024)
     ap.add_argument("--append-new", type=int, default=128)
-    ap.add_argument("--cpu-batch", type=int, default=4)
+    ap.add_argument("--cpu-batch", type=int, default=200)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--fill-kv", default="prefill", choices=["prefill", "random"])
     ap.add_argument("--no-engine", action="store_true")

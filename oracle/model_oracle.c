@@ -76,6 +76,7 @@ typedef struct {
 
 struct mo_model {
   mo_cfg cfg;
+  int n_alloc_layers;
   uint64_t seed;
   mo_layer* layers;
   uint16_t* lm_head;
@@ -99,6 +100,7 @@ static float* gen_bias(uint64_t seed, int tensor, int layer, size_t n) {
 mo_model* mo_model_create(const mo_cfg* cfg, uint64_t seed) {
   mo_model* m = (mo_model*)calloc(1, sizeof(mo_model));
   m->cfg = *cfg;
+  m->n_alloc_layers = cfg->n_layers;
   m->seed = seed;
   int L = cfg->n_layers, d = cfg->d_model, Dh = cfg->head_dim;
   size_t qd = (size_t)cfg->n_q_heads * Dh, kd = (size_t)cfg->n_kv_heads * Dh;
@@ -123,9 +125,14 @@ mo_model* mo_model_create(const mo_cfg* cfg, uint64_t seed) {
   return m;
 }
 
+/* Runs only the first n layers in mo_step (timing extrapolation in bench.py). */
+void mo_set_active_layers(mo_model* m, int n) {
+  if (n >= 1 && n <= m->n_alloc_layers) m->cfg.n_layers = n;
+}
+
 void mo_model_free(mo_model* m) {
   if (!m) return;
-  for (int l = 0; l < m->cfg.n_layers; ++l) {
+  for (int l = 0; l < m->n_alloc_layers; ++l) {
     mo_layer* w = &m->layers[l];
     free(w->wq); free(w->wk); free(w->wv); free(w->wo);
     free(w->wgate); free(w->wup); free(w->wdown);

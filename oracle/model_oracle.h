@@ -46,6 +46,7 @@ void mo_rope_table(float theta, int head_dim, int max_pos, float* cos_out, float
 typedef struct mo_model mo_model;
 mo_model* mo_model_create(const mo_cfg* cfg, uint64_t seed);
 void mo_model_free(mo_model* m);
+void mo_set_active_layers(mo_model* m, int n);
 
 /* Paged KV pool, bf16, layout above. Caller owns the memory:
  * num_blocks * n_layers * 2 * n_kv_heads * block_tokens * head_dim uint16. */

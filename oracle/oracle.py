@@ -54,6 +54,7 @@ def lib():
         L.mo_model_create.restype = vp
         L.mo_model_create.argtypes = [ctypes.POINTER(MoCfg), u64]
         L.mo_model_free.argtypes = [vp]
+        L.mo_set_active_layers.argtypes = [vp, i32]
         L.mo_step.restype = i32
         L.mo_step.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, i32, vp, vp, vp]
         L.mo_attention_paged.argtypes = [ctypes.POINTER(MoCfg), vp, vp, i32, i32, i32, vp, vp, vp, i32, vp]
@@ -100,6 +101,9 @@ class Model:
     def __init__(self, cfg: MoCfg, seed: int):
         self.cfg = cfg
         self.h = lib().mo_model_create(ctypes.byref(cfg), seed)
+
+    def set_active_layers(self, n: int):
+        lib().mo_set_active_layers(self.h, n)
 
     def __del__(self):
         try:
