@@ -378,7 +378,7 @@ int forward(ppd_dev* d, const StepLayout& L) {
 
   CU(launch_embed(tokens, d->embed, d->x, T, d_model, s));
   for (int l = 0; l < c.n_layers; ++l) {
-    int np_qkv = 1, np_o = 1;
+    int np_qkv = 1, np_o = 1, np_gu = 1;
     const Layer& w = d->layers[l];
     // x += down(prev) ; h = norm(x)
     CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, np_down, nullptr, d->ones, d->h, T, d_model,
@@ -399,9 +399,9 @@ int forward(ppd_dev* d, const StepLayout& L) {
     PROF(1, true);
     CU(launch_add_rmsnorm(d->x, d->proj32, np_o, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
     PROF(1, false);
-    CU(gemm_run(d->gemm, d->h, w.wgu, d->gu32, T, 2 * F, d_model, true, s));
+    CU(gemm_run_split(d->gemm, d->h, w.wgu, d->gu32, T, 2 * F, d_model, &np_gu, s));
     PROF(1, true);
-    CU(launch_silu_mul(d->gu32, d->m, T, F, s));
+    CU(launch_silu_mul(d->gu32, np_gu, d->m, T, F, s));
     PROF(1, false);
     CU(gemm_run_split(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, &np_down, s));
     PROF(1, true);
@@ -428,7 +428,7 @@ int alloc_workspaces(ppd_dev* d) {
   const size_t Tp = std::max<size_t>(T, 8 * 256);
   CU(cudaMalloc(&d->qkv32, Tp * (qd + 2 * kd) * 4));
   CU(cudaMalloc(&d->proj32, Tp * c.d_model * 4));
-  CU(cudaMalloc(&d->gu32, T * 2 * c.d_ff * 4));
+  CU(cudaMalloc(&d->gu32, Tp * 2 * c.d_ff * 4));
   CU(cudaMalloc(&d->down32, Tp * c.d_model * 4));
   CU(cudaMalloc(&d->logits, S * c.vocab * 4));
   CU(cudaMalloc(&d->counters, S * c.n_kv_heads * 4));

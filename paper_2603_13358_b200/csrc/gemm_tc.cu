@@ -297,11 +297,23 @@ int gemm_tc_plan_splits(int T, int N, int K) {
   const int bn = T >= kMaxBN ? kMaxBN : ((T + 15) / 16) * 16;
   const int tiles = ((N + kBM - 1) / kBM) * ((T + bn - 1) / bn);
   const int kb = (K + kBK - 1) / kBK;
-  if (tiles >= 120) return 1;
-  int splits = 148 / tiles;
-  splits = splits < 1 ? 1 : splits;
-  splits = splits > kb / 4 ? (kb / 4 > 0 ? kb / 4 : 1) : splits;
-  return splits > 8 ? 8 : splits;
+  // Persistent CTAs take units round-robin, so the step costs
+  //   rounds(s) x (bytes of one unit) = ceil(tiles*s/148) x (W slab / s + fp32 partial write + read).
+  // Pick the split count minimising it (s <= 8, >= 4 K-blocks per split).
+  const double w_unit = double(kBM) * K * 2.0;
+  const double out_unit = double(bn) * kBM * 4.0 * 2.0;
+  int best = 1;
+  double best_cost = 1e300;
+  // the callers' fp32 workspaces hold 8 x 256 token rows of partial slices
+  for (int s = 1; s <= 8 && kb / s >= 4 && s * T <= 8 * 256; ++s) {
+    const int rounds = (tiles * s + 147) / 148;
+    const double cost = rounds * (w_unit / s + (s > 1 ? out_unit : out_unit * 0.5));
+    if (cost < best_cost * 0.97) {  // prefer fewer partial slices unless clearly better
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
 }
 
 cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, int K, bool out_f32, int splits,

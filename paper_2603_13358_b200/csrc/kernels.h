@@ -68,7 +68,7 @@ cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias
                                  bf16* kv_pool, int T, int Hq, int Hkv, int Dh, int n_layers,
                                  int layer, int block_tokens, cudaStream_t s);
 // gate/up fp32 [T][2F] interleaved (see launch_fill_gate_up) -> m = rbf(silu(g) * u) [T][F]
-cudaError_t launch_silu_mul(const float* gu, bf16* m, int T, int F, cudaStream_t s);
+cudaError_t launch_silu_mul(const float* gu, int n_part, bf16* m, int T, int F, cudaStream_t s);
 cudaError_t launch_argmax(const float* logits, int n, int V, int* out, cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t s);
 

@@ -195,6 +195,7 @@ cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, int n_part,
 // One CTA per token row. Each thread owns 4 consecutive rotary pairs (i..i+3,
 // i+64..i+67) of one q/k head, or 4 consecutive dims of one v head, and reads
 // the fp32 GEMM output (all K-split partial slices) with 16-byte loads.
+template <bool kRound = true>
 PPD_DEV float4 ld_sum4(const float* base, int n_part, size_t part_stride, const float* bias, int col) {
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int pp = 0; pp < n_part; ++pp) {
@@ -211,6 +212,7 @@ PPD_DEV float4 ld_sum4(const float* base, int n_part, size_t part_stride, const 
     a.z = __fadd_rn(a.z, b.z);
     a.w = __fadd_rn(a.w, b.w);
   }
+  if (!kRound) return a;
   return make_float4(rbf(a.x), rbf(a.y), rbf(a.z), rbf(a.w));
 }
 
@@ -285,13 +287,13 @@ cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias
 // ------------------------------------------------------------- SiLU * up
 // gate/up come interleaved in 64-column groups (launch_fill_gate_up layout);
 // each thread produces 4 outputs from one float4 of gate and one of up.
-__global__ void silu_mul_kernel(const float* gu, bf16* m, int F) {
+__global__ void silu_mul_kernel(const float* gu, int n_part, size_t part_stride, bf16* m, int F) {
   const int r = blockIdx.y;
   const float* row = gu + (size_t)r * 2 * F;
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4) {
     const int grp = j >> 6, within = j & 63;
-    const float4 g = *reinterpret_cast<const float4*>(row + grp * 128 + within);
-    const float4 u = *reinterpret_cast<const float4*>(row + grp * 128 + 64 + within);
+    const float4 g = ld_sum4<false>(row, n_part, part_stride, nullptr, grp * 128 + within);
+    const float4 u = ld_sum4<false>(row, n_part, part_stride, nullptr, grp * 128 + 64 + within);
     const float gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
     float o[4];
 #pragma unroll
@@ -299,10 +301,10 @@ __global__ void silu_mul_kernel(const float* gu, bf16* m, int F) {
     st_bf16x4(m + (size_t)r * F + j, o[0], o[1], o[2], o[3]);
   }
 }
-cudaError_t launch_silu_mul(const float* gu, bf16* m, int T, int F, cudaStream_t s) {
+cudaError_t launch_silu_mul(const float* gu, int n_part, bf16* m, int T, int F, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   dim3 grid((F / 4 + 255) / 256, T);
-  silu_mul_kernel<<<grid, 256, 0, s>>>(gu, m, F);
+  silu_mul_kernel<<<grid, 256, 0, s>>>(gu, n_part, (size_t)T * 2 * F, m, F);
   return cudaGetLastError();
 }
 

@@ -127,8 +127,60 @@ json result_json(const sim::SimResult& r, const json& job, const std::string& ca
           {"wall_s", wall}};
 }
 
+// op=fit_calibration: device samples -> CalibrationTable (costmodel.hpp fit_from_measurements)
+std::string fit(const json& job) {
+  cost::DeviceSamples s;
+  const json& j = job.at("samples");
+  for (const json& r : j.value("full", json::array())) s.full.emplace_back(r[0].get<long>(), r[1].get<double>());
+  for (const json& r : j.value("append", json::array()))
+    s.append.emplace_back(r[0].get<long>(), r[1].get<long>(), r[2].get<double>());
+  for (const json& r : j.value("decode", json::array())) s.decode.emplace_back(r[0].get<int>(), r[1].get<double>());
+  for (const json& r : j.value("interference", json::array()))
+    s.interference.push_back({cost::prefill_kind_from_string(r.at("kind").get<std::string>()),
+                              r.at("prefill_tokens").get<long>(), r.at("concurrent_prefills").get<int>(),
+                              r.at("decode_batch").get<int>(), r.at("tpot_multiplier").get<double>()});
+  s.kv_bytes_per_token = j.value("kv_bytes_per_token", 0.0);
+  s.link_bandwidth = j.value("link_bandwidth", 0.0);
+  const cost::CalibrationTable c = cost::fit_from_measurements(s);
+  return json{{"calib_json", c.to_json()}, {"hash", c.hash()}}.dump();
+}
+
+// op=build_table: Phase 1 of Algorithm 1 (routing.cpp:220-244) over the default
+// 90-key grid with a virtual-clock runner on the given (e.g. device-fitted)
+// calibration -> the decision table the dynamic router consumes.
+std::string build_table(const json& job) {
+  auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
+  const std::string cluster = job.value("cluster", std::string("1P_3D"));
+  std::vector<std::uint64_t> seeds = job.value("seeds", std::vector<std::uint64_t>{1});
+  const double duration = job.value("duration_s", 10.0);
+  routing::BenchmarkRunner runner = [&](const routing::GridSpec& g, int x) -> std::optional<std::pair<double, double>> {
+    double ttft = 0, tpot = 0;
+    int n = 0;
+    for (std::uint64_t seed : seeds) {
+      workload::WorkloadSpec spec = g.spec;
+      spec.duration_s = duration;
+      const auto convs = workload::generate_conversations(spec, seed);
+      auto cfg = sim::ClusterConfig::from_name(cluster, routing::RoutingPolicy::static_policy(double(x)), calib);
+      const sim::SimResult r = sim::run_simulation(cfg, convs, -1, seed);
+      const auto a = metrics::aggregate(r.records, std::max(spec.duration_s, r.makespan));
+      if (!a.ttft_t2_mean || !a.tpot_mean) return std::nullopt;
+      ttft += *a.ttft_t2_mean;
+      tpot += *a.tpot_mean;
+      ++n;
+    }
+    if (n == 0) return std::nullopt;
+    return std::make_pair(ttft / n, tpot / n);
+  };
+  routing::SLOWeights w{job.value("w_ttft", 1.0), job.value("w_tpot", 1.0)};
+  const routing::DecisionTable t = routing::build_decision_table(routing::default_grid(), w, runner, calib->hash());
+  return json{{"table_json", t.to_json()}, {"calib_hash", calib->hash()}}.dump();
+}
+
 std::string run(const std::string& text) {
   const json job = json::parse(text);
+  const std::string op = job.value("op", std::string("simulate"));
+  if (op == "fit_calibration") return fit(job);
+  if (op == "build_table") return build_table(job);
   auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
   sim::ClusterConfig cfg = sim::ClusterConfig::from_name(job.at("cluster").get<std::string>(), policy_from(job), calib);
   if (job.contains("max_decode_batch")) cfg.max_decode_batch = job["max_decode_batch"].get<int>();
