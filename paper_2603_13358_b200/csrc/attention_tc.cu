@@ -1,0 +1,271 @@
+// attention_tc.cu — K3/K4: full- and append-prefill attention over the paged
+// KV pool on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// Replaces append_prefill_time / full_prefill_time (reference
+// costmodel.cpp:318-331, called simulator.cpp:327-329) for the attention part
+// of a prefill chunk. One CTA = 128 query rows (128/G tokens x the G query
+// heads of one kv head) of one sequence, causal over the paged history.
+//
+//   warp 0  TMA producer: per 128-key block, 8 paged 16-token blocks of K and V
+//           (2-D tensor map over the pool, 128 B swizzle) -> 2-stage ring
+//   warp 1  MMA issuer (one thread): S_j = Q K_j^T into TMEM (double-buffered),
+//           then O += P_{j-1} V_{j-1} (A = P from smem, B = V MN-major)
+//   warp 2  TMEM allocator (512 columns: S0 | S1 | O)
+//   warps 4-7  one thread per query row: online softmax on the S row read with
+//           tcgen05.ld, lazy O rescaling (only when the running max grows by
+//           more than 2^8), P (bf16) to smem, epilogue O / l -> bf16.
+#include <cuda.h>
+
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace ppdk {
+
+namespace {
+constexpr int kThreads = 256;
+constexpr int kBT = 16;
+constexpr int kDh = 128;
+constexpr int kKeys = 128;                  // keys per block
+constexpr int kTile = 32768;                // 128 x 128 bf16
+constexpr int kStages = 2;
+constexpr int kSmem = 1024 + kTile /*Q*/ + kStages * 2 * kTile /*K,V*/ + kTile /*P*/ + 256;
+constexpr uint32_t kTmemCols = 512;
+constexpr float kRescaleThreshold = 8.0f;   // log2 domain
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 1)
+    prefill_attention_tc_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* q_s = smem;
+  uint8_t* kv_s = smem + kTile;                        // [stage][K|V]
+  uint8_t* p_s = kv_s + kStages * 2 * kTile;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + kTile);
+  uint64_t* k_full = bars;            // [2]
+  uint64_t* v_full = bars + 2;        // [2]
+  uint64_t* kv_empty = bars + 4;      // [2]
+  uint64_t* s_full = bars + 6;        // [2]
+  uint64_t* p_ready = bars + 8;
+  uint64_t* o_done = bars + 9;
+  uint64_t* q_ready = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+
+  const AttnItem it = p.items[blockIdx.x];
+  if (it.kind != 1) return;  // decode rows are served by paged_attention_kernel
+  const int kvh = blockIdx.y;
+  const int G = p.group;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = it.seq;
+  const int ctx = p.ctx[s];
+  const int q_base = p.q_start[s];
+  const int rows = it.n_q * G;
+  const int key_end = ctx + it.q_tok0 + it.n_q;
+  const int nblk = (key_end + kKeys - 1) / kKeys;
+  const int* btab = p.block_tables + (size_t)s * p.max_blocks;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+    }
+    mbar_init(p_ready, 4);
+    mbar_init(o_done, 1);
+    mbar_init(q_ready, 4);
+    fence_barrier_init();
+  }
+  if (warp == 2) tc::alloc(tmem_slot, kTmemCols);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_o = tmem + 2 * kKeys;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int last_blk = (key_end - 1) / kBT;
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % kStages;
+        if (j >= kStages) mbar_wait(&kv_empty[st], ((j / kStages) - 1) & 1);
+        uint8_t* k_dst = kv_s + (st * 2 + 0) * kTile;
+        uint8_t* v_dst = kv_s + (st * 2 + 1) * kTile;
+        mbar_arrive_expect_tx(&k_full[st], kTile);
+        mbar_arrive_expect_tx(&v_full[st], kTile);
+        for (int b = 0; b < kKeys / kBT; ++b) {
+          // slots past the sequence re-load its last block: finite data, masked to p = 0
+          const int pb = min(j * (kKeys / kBT) + b, last_blk);
+          const int blk = btab[pb];
+          const int rowK = (((blk * p.n_layers + p.layer) * 2 + 0) * p.n_kv_heads + kvh) * kBT;
+          const int rowV = rowK + p.n_kv_heads * kBT;
+          for (int h = 0; h < 2; ++h) {
+            tc::tma_load_2d(k_dst + h * (kTile / 2) + b * 2048, &kv_map, h * 64, rowK, &k_full[st]);
+            tc::tma_load_2d(v_dst + h * (kTile / 2) + b * 2048, &kv_map, h * 64, rowV, &v_full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = tc::idesc_bf16(128, kKeys, false);
+      const uint32_t id_o = tc::idesc_bf16(128, kDh, true);
+      mbar_wait(q_ready, 0);
+      tc::fence_after();
+      const uint32_t qa = smem_u32(q_s), pa = smem_u32(p_s);
+      for (int j = 0; j <= nblk; ++j) {
+        if (j < nblk) {
+          const int st = j % kStages;
+          mbar_wait(&k_full[st], (j / kStages) & 1);
+          tc::fence_after();
+          const uint32_t ka = smem_u32(kv_s + (st * 2 + 0) * kTile);
+#pragma unroll
+          for (int kk = 0; kk < kDh / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+            tc::mma_bf16_ss(tmem + (j & 1) * kKeys, tc::desc_kmajor_sw128(qa + off), tc::desc_kmajor_sw128(ka + off),
+                            id_s, kk > 0);
+          }
+          tc::commit(&s_full[j & 1]);
+        }
+        if (j >= 1) {
+          const int jj = j - 1, st = jj % kStages;
+          mbar_wait(p_ready, jj & 1);
+          mbar_wait(&v_full[st], (jj / kStages) & 1);
+          tc::fence_after();
+          const uint32_t va = smem_u32(kv_s + (st * 2 + 1) * kTile);
+#pragma unroll
+          for (int kk = 0; kk < kKeys / 16; ++kk) {
+            const uint32_t poff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+            tc::mma_bf16_ss(t_o, tc::desc_kmajor_sw128(pa + poff), tc::desc_mnmajor_sw128(va + kk * 2048, kTile / 2),
+                            id_o, (jj > 0) || (kk > 0));
+          }
+          tc::commit(o_done);
+          tc::commit(&kv_empty[st]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int r = threadIdx.x - 128;  // query row == TMEM lane
+    const int q4 = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    // ---- Q row -> shared (K-major, 128 B swizzle, two 64-dim atoms)
+    {
+      const uint4* src = nullptr;
+      if (r < rows)
+        src = reinterpret_cast<const uint4*>(p.q + ((size_t)(q_base + it.q_tok0 + r / G) * p.n_q_heads + kvh * G + r % G) * kDh);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const uint4 v = src ? src[c] : make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(q_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_ready);
+    }
+    const int pos = r < rows ? ctx + it.q_tok0 + r / G : -1;
+    const float sl2 = p.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc::fence_after();
+      float sv[kKeys];
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys; c0 += 32) {
+        uint32_t raw[32];
+        tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + c0, raw);
+        tc::wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) sv[c0 + c] = __uint_as_float(raw[c]);
+      }
+      const int key0 = j * kKeys;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kKeys; ++c) {
+        sv[c] = (key0 + c <= pos) ? sv[c] * sl2 : -INFINITY;
+        mx = fmaxf(mx, sv[c]);
+      }
+      float alpha = 1.f;
+      bool rescale = false;
+      if (m == -INFINITY) {
+        m = mx;  // first keys this row sees (O holds zeros for it so far)
+      } else if (mx > m + kRescaleThreshold) {
+        alpha = exp2f(m - mx);
+        m = mx;
+        rescale = true;
+      }
+      const float base = m == -INFINITY ? 0.f : m;
+      float rs = 0.f;
+      uint32_t pk[kKeys / 2];
+#pragma unroll
+      for (int c = 0; c < kKeys; c += 2) {
+        const float p0 = exp2f(sv[c] - base), p1 = exp2f(sv[c + 1] - base);
+        rs += p0 + p1;
+        pk[c >> 1] = pack2(p0, p1);
+      }
+      // P_{j-1} and O must have been consumed by PV_{j-1} before we overwrite / rescale
+      if (j >= 1) {
+        mbar_wait(o_done, (j - 1) & 1);
+        tc::fence_after();
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const uint4 v = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+        *reinterpret_cast<uint4*>(p_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+      }
+      if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c0 = 0; c0 < kDh; c0 += 32) {
+          uint32_t o[32];
+          tc::ld32x32(t_o + lane_base + c0, o);
+          tc::wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+          tc::st32x32(t_o + lane_base + c0, o);
+        }
+        tc::wait_st();
+      }
+      l = l * alpha + rs;
+      fence_proxy_async();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_ready);
+    }
+    // ---- epilogue: O / l -> bf16
+    mbar_wait(o_done, (nblk - 1) & 1);
+    tc::fence_after();
+    const float inv = 1.f / l;
+    bf16* dst = r < rows ? p.out + ((size_t)(q_base + it.q_tok0 + r / G) * p.n_q_heads + kvh * G + r % G) * kDh
+                         : nullptr;
+#pragma unroll
+    for (int c0 = 0; c0 < kDh; c0 += 32) {
+      uint32_t o[32];
+      tc::ld32x32(t_o + lane_base + c0, o);
+      tc::wait_ld();
+      if (dst) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 8) {
+          float f[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(o[c + e]) * inv;
+          *reinterpret_cast<uint4*>(dst + c0 + c) = pack8(f);
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 2) tc::dealloc(tmem, kTmemCols);
+}
+
+cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p, int n_items, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(prefill_attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  if (n_items == 0) return cudaSuccess;
+  dim3 grid(n_items, p.n_kv_heads);
+  prefill_attention_tc_kernel<<<grid, kThreads, kSmem, stream>>>(*reinterpret_cast<const CUtensorMap*>(kv_map), p);
+  return cudaGetLastError();
+}
+
+}  // namespace ppdk

@@ -124,7 +124,7 @@ namespace {
 
 // ------------------------------------------------------------ metadata
 struct StepLayout {
-  int n, T, maxb, n_out, n_items, n_ws;
+  int n, T, maxb, n_out, n_items, n_ws, n_dec;
   double attn_bytes;  // algorithmic bytes of one attention launch (one layer)
   size_t off_qstart, off_ctx, off_tokens, off_bt, off_rowseq, off_rowpos, off_outrows, off_items,
       total;
@@ -132,11 +132,23 @@ struct StepLayout {
 
 // Builds the attention work list for the batch. Decode rows (q_len == 1) get
 // KV splits when the grid would otherwise under-fill the 148 SMs.
+bool attention_tc_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PPD_ATTN_TC");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
+
+// Decode items come first, then prefill tiles (n_dec = number of decode items):
+// decode rows run on paged_attention_kernel, prefill tiles of 128/G tokens on
+// the tcgen05 kernel (or 64/G-token tiles on paged_attention_kernel when the
+// tensor-core path is disabled).
 void build_items(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads, int group,
-                 std::vector<AttnItem>& items, int& n_ws) {
+                 std::vector<AttnItem>& items, int& n_ws, int& n_dec) {
   items.clear();
   n_ws = 0;
-  const int tq = std::max(1, 64 / group);
+  const int tq = std::max(1, (attention_tc_enabled() ? 128 : 64) / group);
   long base_ctas = 0;
   int n_decode = 0;
   for (int s = 0; s < n; ++s) {
@@ -185,6 +197,9 @@ void build_items(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads
       }
     }
   }
+  std::stable_partition(items.begin(), items.end(), [](const AttnItem& it) { return it.kind == 0; });
+  n_dec = 0;
+  for (const AttnItem& it : items) n_dec += it.kind == 0;
 }
 
 void clear_graphs(ppd_dev* d) {
@@ -260,7 +275,7 @@ int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnIt
   for (int i = 0; i < L.T; ++i)
     CHECK_ARG(b->tokens[i] >= 0 && b->tokens[i] < d->cfg.vocab, "batch: token id out of range");
   const int G = d->cfg.n_q_heads / d->cfg.n_kv_heads;
-  build_items(L.n, b->q_len, b->ctx, d->cfg.n_kv_heads, G, items, L.n_ws);
+  build_items(L.n, b->q_len, b->ctx, d->cfg.n_kv_heads, G, items, L.n_ws, L.n_dec);
   L.n_items = (int)items.size();
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -305,7 +320,7 @@ int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnIt
 
 int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf16* out,
                   const int* d_qstart, const int* d_ctx, const int* d_bt, int maxb,
-                  const AttnItem* d_items, int n_items, int layer, float* ws_o, float* ws_ml,
+                  const AttnItem* d_items, int n_dec, int n_items, int layer, float* ws_o, float* ws_ml,
                   int* counters, cudaStream_t s) {
   AttnParams p{};
   p.items = d_items;
@@ -324,7 +339,13 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   p.ws_o = ws_o;
   p.ws_ml = ws_ml;
   p.counters = counters;
-  CU(launch_paged_attention(kv_map, p, n_items, s));
+  if (attention_tc_enabled() && n_items > n_dec) {
+    CU(launch_paged_attention(kv_map, p, n_dec, s));
+    p.items = d_items + n_dec;
+    CU(launch_prefill_attention_tc(kv_map, p, n_items - n_dec, s));
+  } else {
+    CU(launch_paged_attention(kv_map, p, n_items, s));
+  }
   return PPD_OK;
 }
 
@@ -390,7 +411,7 @@ int forward(ppd_dev* d, const StepLayout& L) {
                             d->rope_sin, d->q, d->kv, T, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers,
                             l, d->bt, s));
     PROF(0, false);
-    int rc = run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_items, l,
+    int rc = run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items, l,
                            d->ws_o, d->ws_ml, d->counters, s);
     if (rc) return rc;
     PROF(0, true);
@@ -627,7 +648,7 @@ int ppd_step_submit(ppd_dev* d, const ppd_batch* b) {
   CU(cudaMemcpyAsync(d->d_meta, d->h_meta, L.total, cudaMemcpyHostToDevice, d->compute));
   CU(cudaEventRecord(d->ev0, d->compute));
   // repeated shapes replay a captured graph (decode steps: ~300 launches -> 1)
-  const auto key = std::make_tuple(L.n, L.T, L.maxb, L.n_out, L.n_items, L.n_ws);
+  const auto key = std::make_tuple(L.n, L.T, L.maxb, L.n_out, L.n_items * 4096 + L.n_dec, L.n_ws);
   const bool graph_ok = d->use_graphs && !d->profiling && d->shape_seen[key]++ > 0;
   if (graph_ok) {
     auto it = d->graphs.find(key);
@@ -805,7 +826,8 @@ int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_poo
   const int G = cfg->n_q_heads / cfg->n_kv_heads;
   std::vector<AttnItem> items;
   int n_ws = 0;
-  build_items(n_seqs, qlen.data(), ctx, cfg->n_kv_heads, G, items, n_ws);
+  int n_dec = 0;
+  build_items(n_seqs, qlen.data(), ctx, cfg->n_kv_heads, G, items, n_ws, n_dec);
   alignas(128) uint8_t map[128];
   uint64_t rows = (uint64_t)num_blocks * cfg->n_layers * 2 * cfg->n_kv_heads * block_tokens;
   if (make_kv_tensor_map(map, kv_pool, rows) != 0) return fail(PPD_ERR_CUDA, "tensor map encode failed");
@@ -828,7 +850,7 @@ int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_poo
   CU(cudaMemcpy(d_bt, block_tables, nb * 4, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_items, items.data(), items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice));
   rc = run_attention(*cfg, map, static_cast<const bf16*>(q), static_cast<bf16*>(out), d_qs, d_ctx,
-                     d_bt, max_blocks, d_items, (int)items.size(), layer, ws_o, ws_ml, ctr, s);
+                     d_bt, max_blocks, d_items, n_dec, (int)items.size(), layer, ws_o, ws_ml, ctr, s);
   cudaStreamSynchronize(s);
   cudaFree(dm);
   cudaFree(ws_o);

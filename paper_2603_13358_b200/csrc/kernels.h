@@ -40,6 +40,8 @@ struct AttnParams {
 int make_kv_tensor_map(void* map_out /* CUtensorMap, 128 B */, const void* pool, uint64_t total_rows);
 cudaError_t launch_paged_attention(const void* kv_map, const AttnParams& p, int n_items,
                                    cudaStream_t stream);
+// tcgen05/TMEM prefill tiles (kind 1 items of 128/G tokens)
+cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p, int n_items, cudaStream_t stream);
 
 // ---- small fused ops (ops.cu) ----
 cudaError_t launch_fill_random(bf16* dst, uint64_t n, uint64_t seed, int tensor, int layer,
