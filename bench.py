@@ -128,20 +128,27 @@ def cpu_port_decode(batch: int, ctx: int, layers_full: int, n_rep: int = 1):
     return batch / t_full, sample, t_sum
 
 
-def engine_ttft(gpu: int, quick: bool = False):
+def engine_ttft(gpus, layout: str, quick: bool = False):
     """Turn-2+ TTFT / TPOT, PD (x=0) vs PPD (x=1), through the host C++ engine
-    on the DEVICE clock (BASELINE configs[2] shape: 1P:1D, 4 turns, Llama-3-8B
-    shape). Both nodes live on the one visible GPU; each node's clock advances
-    by the CUDA-event time of its own steps and KV hops (the nodes would be
-    separate GPUs of the box). Returns a dict for the JSON line."""
+    on the DEVICE clock: every prefill chunk, decode iteration and P->D KV hop
+    runs on the GPUs listed (node i -> gpus[i]); each node's clock advances by
+    the CUDA-event time of its own work. 1P_1D uses the BASELINE configs[2]
+    trace (4 turns of 1536 in / 128 out); the 8-node layouts use configs[3]
+    (2048 then 2x1024 in, 128 out, high load)."""
     from paper_2603_13358_b200 import engine as E
-    wl = {"id": "cfg3", "turn1": [1536, 128], "turn2plus": [1536, 128], "num_turns": 4,
-          "qps": 1.0, "duration_s": 4.0 if quick else 8.0}
-    out = {"cluster": "1P_1D", "workload": wl, "model": "llama-3-8b-shape",
-           "placement": "both nodes on GPU %d; device-clock replay (per-node CUDA-event durations)" % gpu}
+    if layout in ("1P_1D", "1R"):
+        wl = {"id": "cfg3", "turn1": [1536, 128], "turn2plus": [1536, 128], "num_turns": 4,
+              "qps": 1.0, "duration_s": 4.0 if quick else 8.0}
+    else:
+        wl = {"id": "cfg4", "turn1": [2048, 128], "turn2plus": [1024, 128], "num_turns": 3,
+              "qps": 8.0, "duration_s": 4.0 if quick else 8.0}
+    distinct = len(set(gpus)) == len(gpus)
+    out = {"cluster": layout, "workload": wl, "model": "llama-3-8b-shape", "gpus": gpus,
+           "placement": ("one node per GPU" if distinct else "nodes share GPU %s" % sorted(set(gpus)))
+           + "; device clock = per-node CUDA-event durations"}
     for x in (0.0, 1.0):
-        job = {"cluster": "1P_1D", "x": x, "clock": "device", "seed": 3, "workload": wl,
-               "device": {"model": "llama8b", "weight_seed": SEED, "token_seed": 3, "gpus": [gpu],
+        job = {"cluster": layout, "x": x, "clock": "device", "seed": 3, "workload": wl,
+               "device": {"model": "llama8b", "weight_seed": SEED, "token_seed": 3, "gpus": gpus,
                           "kv_blocks_per_node": 4096, "prefill_chunk": 2048, "record_tokens": False}}
         t0 = time.perf_counter()
         r = E.run(job)
@@ -150,6 +157,7 @@ def engine_ttft(gpu: int, quick: bool = False):
         out[f"x{int(x)}"] = {"ttft_t2_p50_ms": ms(agg["ttft_t2_p50"]), "ttft_t2_p99_ms": ms(agg["ttft_t2_p99"]),
                              "ttft_t2_mean_ms": ms(agg["ttft_t2_mean"]), "tpot_mean_ms": ms(agg["tpot_mean"]),
                              "tpot_p50_ms": ms(agg["tpot_p50"]), "success_rate": agg["success_rate"],
+                             "decode_tok_s": agg["tps"],
                              "link_transfers": r["link_transfers"], "link_gb": r["link_bytes"] / 1e9,
                              "kv_transfer_gbs": r["device"]["kv_transfer"]["gbs"],
                              "wall_s": time.perf_counter() - t0}
@@ -283,11 +291,18 @@ def run_ours(args, rank, world, local_rank):
     inter["reference_anchor_mult"] = {"full_1024_b200": 1.48, "append_1024_b200": 1.02,
                                       "full_1024_conc4": 1.57, "append_1024_conc4": 1.21}
 
-    if rank != 0:
-        dev.close()
-        return
     dev.close()
-    ttft = None if args.no_engine else engine_ttft(local_rank, quick=args.quick)
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()  # rank 0 drives all GPUs for the engine runs
+        return
+    ttft = None
+    if not args.no_engine:
+        from paper_2603_13358_b200 import dist as D
+        if world == 1:
+            ttft = [engine_ttft([local_rank, local_rank], "1P_1D", quick=args.quick)]
+        else:
+            ttft = [engine_ttft(D.layout_gpus(lay, world), lay, quick=args.quick) for lay in D.node_layouts(world)]
 
     pk, pk_kind = peaks()
     attn_gbs = prof["attn_bytes"] / (prof["attn_ms"] * 1e-3) / 1e9 if prof["attn_ms"] > 0 else None
@@ -354,6 +369,8 @@ def run_ours(args, rank, world, local_rank):
         "prefill_setup_s": prefill_s,
     }
     print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
 
 
 def run_reference(args, rank, world):
