@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* empty_bar = full_bar + kStages;
   int* flag = reinterpret_cast<int*>(empty_bar + kStages);
 
+  pdl_wait();
   const AttnItem it = p.items[blockIdx.x];
   const int kvh = blockIdx.y;
   const int G = p.group;
@@ -293,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[slot]);
   }
+  pdl_trigger();
 
   if (!is_decode) {
     // prefill rows: normalise and store bf16
@@ -430,9 +432,8 @@ cudaError_t launch_paged_attention(const void* kv_map, const AttnParams& p, int 
   }
   if (n_items == 0) return cudaSuccess;
   dim3 grid(n_items, p.n_kv_heads);
-  paged_attention_kernel<<<grid, kThreads, kSmemBytes, stream>>>(
-      *reinterpret_cast<const CUtensorMap*>(kv_map), p);
-  return cudaGetLastError();
+  return launch_pdl(paged_attention_kernel, grid, dim3(kThreads), kSmemBytes, stream,
+                    *reinterpret_cast<const CUtensorMap*>(kv_map), p);
 }
 
 }  // namespace ppdk

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_ready = bars + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
+  pdl_wait();
   const AttnItem it = p.items[blockIdx.x];
   if (it.kind != 1) return;  // decode rows are served by paged_attention_kernel
   const int kvh = blockIdx.y;
@@ -230,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(p_ready);
     }
     // ---- epilogue: O / l -> bf16
+    pdl_trigger();
     mbar_wait(o_done, (nblk - 1) & 1);
     tc::fence_after();
     const float inv = 1.f / l;
@@ -264,8 +266,8 @@ cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p,
   }
   if (n_items == 0) return cudaSuccess;
   dim3 grid(n_items, p.n_kv_heads);
-  prefill_attention_tc_kernel<<<grid, kThreads, kSmem, stream>>>(*reinterpret_cast<const CUtensorMap*>(kv_map), p);
-  return cudaGetLastError();
+  return launch_pdl(prefill_attention_tc_kernel, grid, dim3(kThreads), kSmem, stream,
+                    *reinterpret_cast<const CUtensorMap*>(kv_map), p);
 }
 
 }  // namespace ppdk

@@ -118,3 +118,13 @@ PPD_DEV void cp_async_wait() {
 }
 
 }  // namespace ppdk
+
+namespace ppdk {
+// ---- programmatic dependent launch (PDL) ----------------------------------
+// pdl_wait: block until the preceding kernel in the stream has completed and
+// its memory is visible (no-op when launched without the PDL attribute).
+// pdl_trigger: allow the next kernel to start launching (its prologue and any
+// weight prefetch overlap this kernel's tail).
+PPD_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+PPD_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+}  // namespace ppdk

@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "gemm_tc.h"
+#include "kernels.h"
 
 namespace ppdk {
 
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();  // the next kernel may launch; it waits for our completion itself
 
   // unit -> (weight tile, token tile, split); token tile fastest
   auto decode_unit = [&](int u, int& tw, int& tt, int& sp) {
@@ -146,6 +148,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      // Weights do not depend on the previous kernel: stream the first stages of
+      // W before waiting on it (PDL), then the activations.
+      int npre = 0;
+      if ((int)blockIdx.x < n_units) {
+        int tw, tt, sp;
+        decode_unit(blockIdx.x, tw, tt, sp);
+        const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+        npre = min(S, max(0, kb1 - kb0));
+        for (int i = 0; i < npre; ++i) {
+          mbar_arrive_expect_tx(&full[i], stage_bytes);
+          tma_load_2d(smem + i * stage_bytes, &map_w, (kb0 + i) * kBK, tw * kBM, &full[i]);
+        }
+      }
+      pdl_wait();
       int it = 0;  // global stage counter across units
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         int tw, tt, sp;
@@ -153,10 +169,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % S;
-          if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
           uint8_t* sw = smem + s * stage_bytes;
-          mbar_arrive_expect_tx(&full[s], stage_bytes);
-          tma_load_2d(sw, &map_w, kb * kBK, tw * kBM, &full[s]);
+          if (it >= npre) {
+            if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
+            mbar_arrive_expect_tx(&full[s], stage_bytes);
+            tma_load_2d(sw, &map_w, kb * kBK, tw * kBM, &full[s]);
+          }
           tma_load_2d(sw + kWBytes, &map_x, kb * kBK, tt * p.bn, &full[s]);
         }
       }
@@ -191,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
+    pdl_wait();  // outputs are written only after the predecessor retired
     const int q = warp & 3;  // TMEM lane quarter owned by this warp
     int j = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
@@ -355,8 +374,7 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
   }
   const int units = ((N + kBM - 1) / kBM) * ((T + bn - 1) / bn) * splits;
   const int grid = units < 148 ? units : 148;
-  gemm_tc_kernel<<<grid, kThreads, smem, s>>>(mw, mx, p);
-  return cudaGetLastError();
+  return launch_pdl(gemm_tc_kernel, dim3(grid), dim3(kThreads), (size_t)smem, s, mw, mx, p);
 }
 
 }  // namespace ppdk

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace ppdk {
 
 typedef __nv_bfloat16 bf16;
@@ -85,4 +87,26 @@ struct KvCopyParams {
 };
 cudaError_t launch_kv_copy(const KvCopyParams& p, cudaStream_t s);
 
+}  // namespace ppdk
+
+namespace ppdk {
+// Launch with the programmatic-stream-serialization attribute (PDL) so the
+// kernel may begin while its predecessor drains; kernels call pdl_wait()
+// before consuming predecessor outputs.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 }  // namespace ppdk

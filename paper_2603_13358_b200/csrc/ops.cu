@@ -6,6 +6,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace ppdk {
 
 namespace {
@@ -104,6 +106,8 @@ cudaError_t launch_fill_const(bf16* dst, uint64_t n, float v, cudaStream_t s) {
 
 // ------------------------------------------------------------------ embed
 __global__ void embed_kernel(const int* tokens, const bf16* embed, bf16* x, int d) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(embed + (size_t)tokens[r] * d);
   uint4* dst = reinterpret_cast<uint4*>(x + (size_t)r * d);
@@ -111,7 +115,7 @@ __global__ void embed_kernel(const int* tokens, const bf16* embed, bf16* x, int 
 }
 cudaError_t launch_embed(const int* tokens, const bf16* embed, bf16* x, int T, int d, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  embed_kernel<<<T, 128, 0, s>>>(tokens, embed, x, d);
+  return launch_pdl(embed_kernel, dim3(T), dim3(128), 0, s, tokens, embed, x, d);
   return cudaGetLastError();
 }
 
@@ -122,6 +126,8 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
     bf16* x, const float* df, int n_part, size_t part_stride, const bf16* db, const bf16* w,
     bf16* out, const int* rows, int d, float eps) {
   __shared__ float red[33];
+  pdl_wait();
+  pdl_trigger();
   const size_t row = rows ? (size_t)rows[blockIdx.x] : (size_t)blockIdx.x;
   const int nc = d / 8;
   float v[kMaxChunks][8];
@@ -176,19 +182,16 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
 cudaError_t launch_add_rmsnorm(bf16* x, const float* delta_f32, int n_part, const bf16* delta_bf16,
                                const bf16* w, bf16* h, int T, int d, float eps, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  add_rmsnorm_kernel<true><<<T, kNormThreads, 0, s>>>(x, delta_f32, n_part, (size_t)T * d,
-                                                      delta_bf16, w, h, nullptr, d, eps);
-  return cudaGetLastError();
+  return launch_pdl(add_rmsnorm_kernel<true>, dim3(T), dim3(kNormThreads), 0, s, x, delta_f32, n_part,
+                    (size_t)T * d, delta_bf16, w, h, (const int*)nullptr, d, eps);
 }
 
 cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, int n_part,
                               const bf16* delta_bf16, const int* rows, int n_rows, const bf16* w,
                               bf16* out, int T, int d, float eps, cudaStream_t s) {
   if (n_rows == 0) return cudaSuccess;
-  add_rmsnorm_kernel<false><<<n_rows, kNormThreads, 0, s>>>(const_cast<bf16*>(x), delta_f32, n_part,
-                                                           (size_t)T * d, delta_bf16, w, out, rows,
-                                                           d, eps);
-  return cudaGetLastError();
+  return launch_pdl(add_rmsnorm_kernel<false>, dim3(n_rows), dim3(kNormThreads), 0, s, const_cast<bf16*>(x),
+                    delta_f32, n_part, (size_t)T * d, delta_bf16, w, out, rows, d, eps);
 }
 
 // ------------------------------------------------------- RoPE + KV write
@@ -225,6 +228,8 @@ __global__ void rope_kv_kernel(const float* qkv, int n_part, size_t part_stride,
                                int max_blocks, const float* rope_cos, const float* rope_sin,
                                bf16* q_out, bf16* kv, int Hq, int Hkv, int Dh, int n_layers,
                                int layer, int BT) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const int half = Dh / 2;
   const int qd = Hq * Dh, kd = Hkv * Dh, W = qd + 2 * kd;
@@ -278,16 +283,17 @@ cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias
                                  int layer, int block_tokens, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const size_t W = (size_t)(Hq + 2 * Hkv) * Dh;
-  rope_kv_kernel<<<T, 256, 0, s>>>(qkv, n_part, (size_t)T * W, bias, row_seq, row_pos, block_tables,
-                                   max_blocks, rope_cos, rope_sin, q_out, kv_pool, Hq, Hkv, Dh,
-                                   n_layers, layer, block_tokens);
-  return cudaGetLastError();
+  return launch_pdl(rope_kv_kernel, dim3(T), dim3(256), 0, s, qkv, n_part, (size_t)T * W, bias, row_seq, row_pos,
+                    block_tables, max_blocks, rope_cos, rope_sin, q_out, kv_pool, Hq, Hkv, Dh, n_layers, layer,
+                    block_tokens);
 }
 
 // ------------------------------------------------------------- SiLU * up
 // gate/up come interleaved in 64-column groups (launch_fill_gate_up layout);
 // each thread produces 4 outputs from one float4 of gate and one of up.
 __global__ void silu_mul_kernel(const float* gu, int n_part, size_t part_stride, bf16* m, int F) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.y;
   const float* row = gu + (size_t)r * 2 * F;
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4) {
@@ -304,12 +310,13 @@ __global__ void silu_mul_kernel(const float* gu, int n_part, size_t part_stride,
 cudaError_t launch_silu_mul(const float* gu, int n_part, bf16* m, int T, int F, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   dim3 grid((F / 4 + 255) / 256, T);
-  silu_mul_kernel<<<grid, 256, 0, s>>>(gu, n_part, (size_t)T * 2 * F, m, F);
-  return cudaGetLastError();
+  return launch_pdl(silu_mul_kernel, grid, dim3(256), 0, s, gu, n_part, (size_t)T * 2 * F, m, F);
 }
 
 // ---------------------------------------------------------------- argmax
 __global__ void argmax_kernel(const float* logits, int V, int* out) {
+  pdl_wait();
+  pdl_trigger();
   const float* row = logits + (size_t)blockIdx.x * V;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -343,8 +350,7 @@ __global__ void argmax_kernel(const float* logits, int V, int* out) {
 }
 cudaError_t launch_argmax(const float* logits, int n, int V, int* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  argmax_kernel<<<n, 1024, 0, s>>>(logits, V, out);
-  return cudaGetLastError();
+  return launch_pdl(argmax_kernel, dim3(n), dim3(1024), 0, s, logits, V, out);
 }
 
 __global__ void f32_to_bf16_kernel(const float* in, bf16* out, uint64_t n) {
@@ -357,4 +363,14 @@ cudaError_t launch_f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStrea
   return cudaGetLastError();
 }
 
+}  // namespace ppdk
+
+namespace ppdk {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PPD_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 }  // namespace ppdk
