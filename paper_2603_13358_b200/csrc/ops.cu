@@ -242,7 +242,7 @@ __global__ void rope_kv_kernel(const float* qkv, int n_part, size_t part_stride,
   const int per_head = half / 4;                 // rotary units per head
   const int n_rot = (Hq + Hkv) * per_head;
   const int n_v = kd / 4;
-  for (int u = threadIdx.x; u < n_rot + n_v; u += blockDim.x) {
+  for (int u = blockIdx.y * blockDim.x + threadIdx.x; u < n_rot + n_v; u += gridDim.y * blockDim.x) {
     if (u < n_rot) {
       const int head = u / per_head, i = (u % per_head) * 4;
       const int col = head * Dh + i;  // k heads follow q heads in the fused layout
@@ -283,7 +283,8 @@ cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias
                                  int layer, int block_tokens, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const size_t W = (size_t)(Hq + 2 * Hkv) * Dh;
-  return launch_pdl(rope_kv_kernel, dim3(T), dim3(256), 0, s, qkv, n_part, (size_t)T * W, bias, row_seq, row_pos,
+  // (row, quarter of the row's rotary/v units): 4 CTAs per token row for memory parallelism
+  return launch_pdl(rope_kv_kernel, dim3(T, 4), dim3(128), 0, s, qkv, n_part, (size_t)T * W, bias, row_seq, row_pos,
                     block_tables, max_blocks, rope_cos, rope_sin, q_out, kv_pool, Hq, Hkv, Dh, n_layers, layer,
                     block_tokens);
 }
@@ -303,7 +304,8 @@ __global__ void silu_mul_kernel(const float* gu, int n_part, size_t part_stride,
     const float gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
     float o[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) o[e] = __fmul_rn(__fdiv_rn(gv[e], __fadd_rn(1.0f, expf(-gv[e]))), uv[e]);
+    for (int e = 0; e < 4; ++e)  // fast exp/div: within 2 ulp of the oracle's fp32, rounded to bf16 next
+      o[e] = __fmul_rn(__fdividef(gv[e], __fadd_rn(1.0f, __expf(-gv[e]))), uv[e]);
     st_bf16x4(m + (size_t)r * F + j, o[0], o[1], o[2], o[3]);
   }
 }

@@ -81,3 +81,23 @@ def test_device_tokens_match_oracle_replay(gpu):
                 assert e["out"][i] == t_o[i], (e["node"], i, e["out"][i], t_o[i], margin[i])
                 checked += 1
     assert checked > 20
+
+
+def test_device_timeouts_and_hybrid(gpu):
+    """Timeouts free the batch slot on the device clock too (simulator.cpp:436-445),
+    and hybrid R/P/D clusters keep replica-pinned conversations local."""
+    job = dev_job("1P_1D", 0.0)
+    job["request_timeout_s"] = 1e-4  # every request expires before its first token
+    r = E.run(job)
+    recs = E.records(r)
+    assert len(recs) == 3 and all(x["status"] == "timed_out" for x in recs)
+    h = E.run(dev_job("1R_1P_1D", 1.0, n=4))
+    routes = {}
+    for x in E.records(h):
+        routes.setdefault(x["conv_id"], []).append(x["route"])
+    for rs in routes.values():
+        if rs[0] == "R_local":
+            assert all(v == "R_local" for v in rs)
+        else:
+            assert "R_local" not in rs
+    assert all(x["status"] == "completed" for x in E.records(h))

@@ -127,3 +127,24 @@ def test_kv_copy_delta_then_decode(pair):
     if m1[0] > MARGIN and m2[0] > MARGIN:
         assert r_d.tokens[0] == t2[0]
     dev_p.close()
+
+
+def test_qwen_shape_bias_group5_parity(gpu):
+    """Qwen2.5-style numerics (QKV bias, GQA group 5, theta 1e6, eps 1e-6) on a
+    tiny shape: prefill + decode + append through ppd_step vs the oracle."""
+    cfg = ppd.ModelCfg(2, 640, 5, 1, 128, 1280, 2048, 1e-6, 1e6, 1)
+    dev = ppd.Device(0, cfg, max_step_tokens=512, max_step_seqs=8)
+    dev.load_random_weights(77)
+    dev.kv_pool_init(32)
+    model = O.Model(O.cfg_from(cfg), 77)
+    pool = O.KvPool(O.cfg_from(cfg), 32)
+    rng = np.random.default_rng(21)
+    bts = np.array([np.arange(0, 8), np.arange(8, 16)], dtype=np.int32)
+    tok, _ = compare(dev, model, pool, [45, 13], [0, 0], rng.integers(0, cfg.vocab, 58), bts)
+    ctx = np.array([45, 13])
+    for _ in range(3):
+        tok, _ = compare(dev, model, pool, [1, 1], ctx, tok, bts)
+        ctx += 1
+    new = rng.integers(0, cfg.vocab, 30)
+    compare(dev, model, pool, [1, 30], ctx, np.concatenate([tok[:1], new]), bts)
+    dev.close()
