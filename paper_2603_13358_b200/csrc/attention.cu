@@ -396,6 +396,266 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// ===========================================================================
+// K1 persistent decode attention with a balanced schedule.
+//
+// The host cuts the decode work (every (sequence, kv head) pair's 64-key
+// stages) into one contiguous range of equal length per CTA (stream-K style);
+// a range may start or end inside a sequence, which then has several key
+// segments merged through the split workspace by the last one to finish. The
+// producer warp streams the paged K/V of all of a CTA's segments back to back
+// (TMA, 3-stage ring), so the memory pipe never drains between sequences; the
+// 4 consumer warps take interleaved 16-key blocks and merge per segment in a
+// small dedicated shared buffer.
+// ===========================================================================
+namespace {
+constexpr int kDecMaxG = 5;  // Llama-3 (4) and Qwen2.5 (5) groups; larger groups use paged_attention_kernel
+constexpr int kDecSmem = 1024 + kStages * kStageBytes + kConsumerWarps * kDecMaxG * (kDh + 2) * 4 + 256;
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 2)
+    decode_attention_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;
+  float* mo = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [warp][G][Dh]
+  float* mml = mo + kConsumerWarps * kDecMaxG * kDh;                    // [warp][G][2]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(mml + kConsumerWarps * kDecMaxG * 2);
+  uint64_t* empty_bar = full_bar + kStages;
+  int* flag = reinterpret_cast<int*>(empty_bar + kStages);
+
+  pdl_wait();
+  const int G = p.group;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seg0 = p.seg_start[blockIdx.x], seg1 = p.seg_start[blockIdx.x + 1];
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      int g = 0;  // global stage counter across this CTA's segments
+      for (int sg = seg0; sg < seg1; ++sg) {
+        const AttnItem it = p.items[sg];
+        const int kvh = it.pad[0];
+        const int* btab = p.block_tables + (size_t)it.seq * p.max_blocks;
+        const int first_blk = it.key_begin / kBT, last_blk = (it.key_end - 1) / kBT;
+        const int nst = (last_blk - first_blk) / kStageBlocks + 1;
+        for (int st = 0; st < nst; ++st, ++g) {
+          const int slot = g % kStages;
+          if (g >= kStages) mbar_wait(&empty_bar[slot], ((g / kStages) - 1) & 1);
+          const int b0 = first_blk + st * kStageBlocks;
+          const int nb = min(kStageBlocks, last_blk - b0 + 1);
+          mbar_arrive_expect_tx(&full_bar[slot], nb * 2 * kBlockBytes);
+          uint8_t* dst = stage_base + slot * kStageBytes;
+          for (int b = 0; b < nb; ++b) {
+            const int blk = btab[b0 + b];
+            const int rowK = (((blk * p.n_layers + p.layer) * 2 + 0) * p.n_kv_heads + kvh) * kBT;
+            const int rowV = rowK + p.n_kv_heads * kBT;
+            tma_load_2d(dst + (b * 2 + 0) * kBlockBytes, &kv_map, 0, rowK, &full_bar[slot]);
+            tma_load_2d(dst + (b * 2 + 0) * kBlockBytes + 2048, &kv_map, 64, rowK, &full_bar[slot]);
+            tma_load_2d(dst + (b * 2 + 1) * kBlockBytes, &kv_map, 0, rowV, &full_bar[slot]);
+            tma_load_2d(dst + (b * 2 + 1) * kBlockBytes + 2048, &kv_map, 64, rowV, &full_bar[slot]);
+          }
+        }
+      }
+    }
+    pdl_trigger();
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int g8 = lane >> 2, t = lane & 3;
+  const float sl2 = p.scale_log2;
+  const int tid = threadIdx.x;  // 0..127
+  int g = 0;
+  for (int sg = seg0; sg < seg1; ++sg) {
+    const AttnItem it = p.items[sg];
+    const int kvh = it.pad[0];
+    const int s = it.seq;
+    const int pos = p.ctx[s];
+    const int q_base = p.q_start[s];
+    const int key_begin = it.key_begin, key_end = it.key_end;
+    const int first_blk = key_begin / kBT, last_blk = (key_end - 1) / kBT;
+    const int nst = (last_blk - first_blk) / kStageBlocks + 1;
+    // Q fragments: rows 0..G-1 are the G heads of this kv head (rows >= G zero)
+    uint32_t qa[8][4];
+    {
+      const uint32_t* q0 = g8 < G ? reinterpret_cast<const uint32_t*>(p.q + ((size_t)q_base * p.n_q_heads + kvh * G + g8) * kDh)
+                                  : nullptr;
+      const uint32_t* q1 = (g8 + 8) < G ? reinterpret_cast<const uint32_t*>(
+                                              p.q + ((size_t)q_base * p.n_q_heads + kvh * G + g8 + 8) * kDh)
+                                        : nullptr;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int w0 = (kk * 16 + 2 * t) >> 1;
+        qa[kk][0] = q0 ? __ldg(q0 + w0) : 0u;
+        qa[kk][1] = q1 ? __ldg(q1 + w0) : 0u;
+        qa[kk][2] = q0 ? __ldg(q0 + w0 + 4) : 0u;
+        qa[kk][3] = q1 ? __ldg(q1 + w0 + 4) : 0u;
+      }
+    }
+    float o[16][4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    for (int st = 0; st < nst; ++st, ++g) {
+      const int slot = g % kStages;
+      mbar_wait(&full_bar[slot], (g / kStages) & 1);
+      const int stage_blocks_valid = min(kStageBlocks, last_blk - (first_blk + st * kStageBlocks) + 1);
+      if (warp < stage_blocks_valid) {
+        const uint32_t kb = smem_u32(stage_base + slot * kStageBytes) + (warp * 2 + 0) * kBlockBytes;
+        const uint32_t vb = kb + kBlockBytes;
+        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kb + kv_off((lane & 7) + (lane >> 4) * 8, kk * 16 + ((lane >> 3) & 1) * 8), b0, b1, b2, b3);
+          mma16816(sc[0], qa[kk], b0, b1);
+          mma16816(sc[1], qa[kk], b2, b3);
+        }
+        const int key = (first_blk + st * kStageBlocks + warp) * kBT;
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int k = key + nt * 8 + 2 * t + e;
+            const bool ok = k >= key_begin && k < key_end && k <= pos;
+            sc[nt][e] = ok ? sc[nt][e] * sl2 : -INFINITY;
+            sc[nt][2 + e] = ok ? sc[nt][2 + e] * sl2 : -INFINITY;
+            mx0 = fmaxf(mx0, sc[nt][e]);
+            mx1 = fmaxf(mx1, sc[nt][2 + e]);
+          }
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float base0 = mn0 == -INFINITY ? 0.f : mn0, base1 = mn1 == -INFINITY ? 0.f : mn1;
+        const float corr0 = exp2f(m0 - base0), corr1 = exp2f(m1 - base1);
+        m0 = mn0;
+        m1 = mn1;
+        const float p00 = exp2f(sc[0][0] - base0), p01 = exp2f(sc[0][1] - base0);
+        const float p02 = exp2f(sc[0][2] - base1), p03 = exp2f(sc[0][3] - base1);
+        const float p10 = exp2f(sc[1][0] - base0), p11 = exp2f(sc[1][1] - base0);
+        const float p12 = exp2f(sc[1][2] - base1), p13 = exp2f(sc[1][3] - base1);
+        float rs0 = p00 + p01 + p10 + p11, rs1 = p02 + p03 + p12 + p13;
+        rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
+        rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
+        rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
+        rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
+        l0 = l0 * corr0 + rs0;
+        l1 = l1 * corr1 + rs1;
+        const uint32_t a[4] = {pack2(p00, p01), pack2(p02, p03), pack2(p10, p11), pack2(p12, p13)};
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          o[i][0] *= corr0;
+          o[i][1] *= corr0;
+          o[i][2] *= corr1;
+          o[i][3] *= corr1;
+        }
+#pragma unroll
+        for (int nt = 0; nt < 16; nt += 2) {
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vb + kv_off((lane & 7) + ((lane >> 3) & 1) * 8, nt * 8 + (lane >> 4) * 8), b0, b1, b2, b3);
+          mma16816(o[nt], a, b0, b1);
+          mma16816(o[nt + 1], a, b2, b3);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[slot]);
+    }
+    // ---- merge the 4 warps (rows < G) through the dedicated buffer
+    if (g8 < G) {
+      float* ow = mo + (warp * kDecMaxG + g8) * kDh;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+        ow[nt * 8 + 2 * t] = o[nt][0];
+        ow[nt * 8 + 2 * t + 1] = o[nt][1];
+      }
+      if (t == 0) {
+        mml[(warp * kDecMaxG + g8) * 2 + 0] = m0;
+        mml[(warp * kDecMaxG + g8) * 2 + 1] = l0;
+      }
+    }
+    named_barrier_sync(1, kConsumerWarps * 32);
+    const bool split = it.n_splits > 1;
+    for (int r = 0; r < G; ++r) {
+      float mm = -INFINITY;
+      for (int w = 0; w < kConsumerWarps; ++w) mm = fmaxf(mm, mml[(w * kDecMaxG + r) * 2]);
+      const float base = mm == -INFINITY ? 0.f : mm;
+      float ll = 0.f, acc = 0.f;
+      for (int w = 0; w < kConsumerWarps; ++w) {
+        const float f = exp2f(mml[(w * kDecMaxG + r) * 2] - base);
+        ll += mml[(w * kDecMaxG + r) * 2 + 1] * f;
+        acc += mo[(w * kDecMaxG + r) * kDh + tid] * f;
+      }
+      if (!split) {
+        p.out[((size_t)q_base * p.n_q_heads + kvh * G + r) * kDh + tid] = f2bf(acc / ll);
+      } else {
+        const size_t wi = ((size_t)it.ws_index * p.n_kv_heads + kvh) * G + r;
+        p.ws_o[wi * kDh + tid] = acc;
+        if (tid == 0) {
+          p.ws_ml[wi * 2 + 0] = mm;
+          p.ws_ml[wi * 2 + 1] = ll;
+        }
+      }
+    }
+    if (split) {
+      __threadfence();
+      named_barrier_sync(1, kConsumerWarps * 32);
+      if (tid == 0) {
+        int* ctr = p.counters + (size_t)s * p.n_kv_heads + kvh;
+        const int prev = atomicAdd(ctr, 1);
+        const int last = prev == it.n_splits - 1;
+        if (last) *ctr = 0;
+        *flag = last;
+      }
+      named_barrier_sync(1, kConsumerWarps * 32);
+      if (*flag) {
+        __threadfence();
+        const int ws0 = it.ws_index - it.split;
+        for (int r = 0; r < G; ++r) {
+          float mm = -INFINITY;
+          for (int sp = 0; sp < it.n_splits; ++sp)
+            mm = fmaxf(mm, __ldcg(&p.ws_ml[(((size_t)(ws0 + sp) * p.n_kv_heads + kvh) * G + r) * 2]));
+          const float base = mm == -INFINITY ? 0.f : mm;
+          float ll = 0.f, acc = 0.f;
+          for (int sp = 0; sp < it.n_splits; ++sp) {
+            const size_t wi = ((size_t)(ws0 + sp) * p.n_kv_heads + kvh) * G + r;
+            const float f = exp2f(__ldcg(&p.ws_ml[wi * 2]) - base);
+            ll += __ldcg(&p.ws_ml[wi * 2 + 1]) * f;
+            acc += __ldcg(&p.ws_o[wi * kDh + tid]) * f;
+          }
+          p.out[((size_t)q_base * p.n_q_heads + kvh * G + r) * kDh + tid] = f2bf(acc / ll);
+        }
+      }
+    }
+    named_barrier_sync(1, kConsumerWarps * 32);  // merge buffer / flag reused by the next segment
+  }
+  pdl_trigger();
+}
+
+cudaError_t launch_decode_attention(const void* kv_map, const AttnParams& p, int n_cta, int group,
+                                    cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
+    attr = true;
+  }
+  if (n_cta == 0) return cudaSuccess;
+  if (group > kDecMaxG) return cudaErrorInvalidValue;
+  return launch_pdl(decode_attention_kernel, dim3(n_cta), dim3(kThreads), kDecSmem, stream,
+                    *reinterpret_cast<const CUtensorMap*>(kv_map), p);
+}
+
 // ---------------------------------------------------------------------------
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {

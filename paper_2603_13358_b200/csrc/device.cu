@@ -124,7 +124,8 @@ namespace {
 
 // ------------------------------------------------------------ metadata
 struct StepLayout {
-  int n, T, maxb, n_out, n_items, n_ws, n_dec;
+  int n, T, maxb, n_out, n_items, n_ws, n_dec, n_cta;
+  size_t off_seg;
   double attn_bytes;  // algorithmic bytes of one attention launch (one layer)
   size_t off_qstart, off_ctx, off_tokens, off_bt, off_rowseq, off_rowpos, off_outrows, off_items,
       total;
@@ -202,6 +203,79 @@ void build_items(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads
   for (const AttnItem& it : items) n_dec += it.kind == 0;
 }
 
+bool decode_persistent_enabled(int group) {
+  static const bool on = [] {
+    const char* e = std::getenv("PPD_DEC_PERSIST");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on && group <= 5;
+}
+
+// Balanced decode schedule (decode_attention_kernel): the 64-key stages of all
+// (decode sequence, kv head) pairs are cut into n_cta equal contiguous ranges;
+// a pair cut by a range boundary becomes several key segments merged through
+// the split workspace. Replaces the decode items of `items` (kept first) and
+// fills seg_start[n_cta + 1].
+void balance_decode(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads, std::vector<AttnItem>& items,
+                    int& n_ws, int& n_dec, std::vector<int>& seg_start) {
+  constexpr int kStageKeys = 64, kMaxCtas = 148 * 2;
+  long U = 0;
+  for (int s = 0; s < n; ++s)
+    if (q_len[s] == 1) U += (long)((ctx[s] + 1 + kStageKeys - 1) / kStageKeys) * n_kv_heads;
+  std::vector<AttnItem> rest(items.begin() + n_dec, items.end());
+  items.clear();
+  seg_start.clear();
+  n_ws = 0;
+  if (U > 0) {
+    long n_cta = std::min<long>(kMaxCtas, U);
+    const long quota = (U + n_cta - 1) / n_cta;
+    n_cta = (U + quota - 1) / quota;
+    long u = 0;
+    for (int s = 0; s < n; ++s) {
+      if (q_len[s] != 1) continue;
+      const int keys = ctx[s] + 1;
+      const int nst = (keys + kStageKeys - 1) / kStageKeys;
+      for (int h = 0; h < n_kv_heads; ++h) {
+        std::vector<std::pair<int, int>> segs;
+        for (int st = 0; st < nst;) {
+          const long cta = u / quota;
+          const int take = (int)std::min<long>(nst - st, (cta + 1) * quota - u);
+          segs.push_back({st, st + take});
+          st += take;
+          u += take;
+        }
+        const int nseg = (int)segs.size();
+        for (int k = 0; k < nseg; ++k) {
+          AttnItem it{};
+          it.kind = 0;
+          it.seq = s;
+          it.n_q = 1;
+          it.key_begin = segs[k].first * kStageKeys;
+          it.key_end = std::min(keys, segs[k].second * kStageKeys);
+          it.split = k;
+          it.n_splits = nseg;
+          it.ws_index = nseg > 1 ? n_ws + k : -1;
+          it.pad[0] = h;
+          items.push_back(it);
+        }
+        if (nseg > 1) n_ws += nseg;
+      }
+    }
+    // CTA c owns the segments whose first unit falls in [c*quota, (c+1)*quota)
+    seg_start.assign(n_cta + 1, (int)items.size());
+    long unit = 0;
+    int c_next = 0;
+    for (int i = 0; i < (int)items.size(); ++i) {
+      const long cta = unit / quota;
+      while (c_next <= cta) seg_start[c_next++] = i;
+      unit += (items[i].key_end - items[i].key_begin + kStageKeys - 1) / kStageKeys;
+    }
+    while (c_next <= n_cta) seg_start[c_next++] = (int)items.size();
+  }
+  n_dec = (int)items.size();
+  items.insert(items.end(), rest.begin(), rest.end());
+}
+
 void clear_graphs(ppd_dev* d) {
   for (auto& kv : d->graphs) cudaGraphExecDestroy(kv.second);
   d->graphs.clear();
@@ -276,6 +350,10 @@ int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnIt
     CHECK_ARG(b->tokens[i] >= 0 && b->tokens[i] < d->cfg.vocab, "batch: token id out of range");
   const int G = d->cfg.n_q_heads / d->cfg.n_kv_heads;
   build_items(L.n, b->q_len, b->ctx, d->cfg.n_kv_heads, G, items, L.n_ws, L.n_dec);
+  std::vector<int> seg_start;
+  if (decode_persistent_enabled(G))
+    balance_decode(L.n, b->q_len, b->ctx, d->cfg.n_kv_heads, items, L.n_ws, L.n_dec, seg_start);
+  L.n_cta = seg_start.empty() ? 0 : (int)seg_start.size() - 1;
   L.n_items = (int)items.size();
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -291,6 +369,7 @@ int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnIt
   L.off_rowpos = take(L.T * 4);
   L.off_outrows = take(std::max(L.n_out, 1) * 4);
   L.off_items = take(items.size() * sizeof(AttnItem));
+  L.off_seg = take(seg_start.size() * 4 + 4);
   L.total = o;
   int rc = ensure_meta(d, L.total);
   if (rc) return rc;
@@ -315,14 +394,16 @@ int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnIt
   std::memcpy(h + L.off_tokens, b->tokens, L.T * 4);
   std::memcpy(h + L.off_bt, b->block_tables, (size_t)L.n * L.maxb * 4);
   std::memcpy(h + L.off_items, items.data(), items.size() * sizeof(AttnItem));
+  if (!seg_start.empty()) std::memcpy(h + L.off_seg, seg_start.data(), seg_start.size() * 4);
   return PPD_OK;
 }
 
 int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf16* out,
                   const int* d_qstart, const int* d_ctx, const int* d_bt, int maxb,
-                  const AttnItem* d_items, int n_dec, int n_items, int layer, float* ws_o, float* ws_ml,
-                  int* counters, cudaStream_t s) {
+                  const AttnItem* d_items, int n_dec, int n_items, const int* d_seg, int n_cta, int layer,
+                  float* ws_o, float* ws_ml, int* counters, cudaStream_t s) {
   AttnParams p{};
+  p.seg_start = d_seg;
   p.items = d_items;
   p.q = q;
   p.out = out;
@@ -339,12 +420,22 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   p.ws_o = ws_o;
   p.ws_ml = ws_ml;
   p.counters = counters;
-  if (attention_tc_enabled() && n_items > n_dec) {
+  // decode rows: the balanced persistent kernel (n_cta > 0) or one CTA per item
+  if (n_cta > 0) {
+    CU(launch_decode_attention(kv_map, p, n_cta, p.group, s));
+  } else if (n_dec > 0 && (attention_tc_enabled() || n_items == n_dec)) {
     CU(launch_paged_attention(kv_map, p, n_dec, s));
-    p.items = d_items + n_dec;
-    CU(launch_prefill_attention_tc(kv_map, p, n_items - n_dec, s));
-  } else {
-    CU(launch_paged_attention(kv_map, p, n_items, s));
+  }
+  if (n_items > n_dec) {
+    if (attention_tc_enabled()) {
+      p.items = d_items + n_dec;
+      CU(launch_prefill_attention_tc(kv_map, p, n_items - n_dec, s));
+    } else if (n_cta > 0) {
+      p.items = d_items + n_dec;
+      CU(launch_paged_attention(kv_map, p, n_items - n_dec, s));
+    } else {
+      CU(launch_paged_attention(kv_map, p, n_items, s));  // decode + prefill items, one launch
+    }
   }
   return PPD_OK;
 }
@@ -411,8 +502,8 @@ int forward(ppd_dev* d, const StepLayout& L) {
                             d->rope_sin, d->q, d->kv, T, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers,
                             l, d->bt, s));
     PROF(0, false);
-    int rc = run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items, l,
-                           d->ws_o, d->ws_ml, d->counters, s);
+    int rc = run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items,
+                           at<int>(m, L.off_seg), L.n_cta, l, d->ws_o, d->ws_ml, d->counters, s);
     if (rc) return rc;
     PROF(0, true);
     PROF(1, false);
@@ -648,7 +739,8 @@ int ppd_step_submit(ppd_dev* d, const ppd_batch* b) {
   CU(cudaMemcpyAsync(d->d_meta, d->h_meta, L.total, cudaMemcpyHostToDevice, d->compute));
   CU(cudaEventRecord(d->ev0, d->compute));
   // repeated shapes replay a captured graph (decode steps: ~300 launches -> 1)
-  const auto key = std::make_tuple(L.n, L.T, L.maxb, L.n_out, L.n_items * 4096 + L.n_dec, L.n_ws);
+  // every launch parameter of forward() is a function of these (grids: items, n_dec, n_cta)
+  const auto key = std::make_tuple(L.n, L.T, L.maxb, L.n_out, L.n_items * 4096 + L.n_dec, L.n_ws * 8192 + L.n_cta);
   const bool graph_ok = d->use_graphs && !d->profiling && d->shape_seen[key]++ > 0;
   if (graph_ok) {
     auto it = d->graphs.find(key);
@@ -828,11 +920,14 @@ int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_poo
   int n_ws = 0;
   int n_dec = 0;
   build_items(n_seqs, qlen.data(), ctx, cfg->n_kv_heads, G, items, n_ws, n_dec);
+  std::vector<int> seg_start;
+  if (decode_persistent_enabled(G)) balance_decode(n_seqs, qlen.data(), ctx, cfg->n_kv_heads, items, n_ws, n_dec, seg_start);
+  const int n_cta = seg_start.empty() ? 0 : (int)seg_start.size() - 1;
   alignas(128) uint8_t map[128];
   uint64_t rows = (uint64_t)num_blocks * cfg->n_layers * 2 * cfg->n_kv_heads * block_tokens;
   if (make_kv_tensor_map(map, kv_pool, rows) != 0) return fail(PPD_ERR_CUDA, "tensor map encode failed");
   size_t nb = (size_t)n_seqs * max_blocks;
-  size_t bytes = (n_seqs + 1 + n_seqs + nb) * 4 + items.size() * sizeof(AttnItem) + 64;
+  size_t bytes = (n_seqs + 1 + n_seqs + nb) * 4 + items.size() * sizeof(AttnItem) + seg_start.size() * 4 + 64;
   uint8_t* dm = nullptr;
   float *ws_o = nullptr, *ws_ml = nullptr;
   int* ctr = nullptr;
@@ -849,8 +944,10 @@ int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_poo
   CU(cudaMemcpy(d_ctx, ctx, n_seqs * 4, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_bt, block_tables, nb * 4, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(d_items, items.data(), items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice));
+  int* d_seg = reinterpret_cast<int*>(d_items + items.size());
+  if (!seg_start.empty()) CU(cudaMemcpy(d_seg, seg_start.data(), seg_start.size() * 4, cudaMemcpyHostToDevice));
   rc = run_attention(*cfg, map, static_cast<const bf16*>(q), static_cast<bf16*>(out), d_qs, d_ctx,
-                     d_bt, max_blocks, d_items, n_dec, (int)items.size(), layer, ws_o, ws_ml, ctr, s);
+                     d_bt, max_blocks, d_items, n_dec, (int)items.size(), d_seg, n_cta, layer, ws_o, ws_ml, ctr, s);
   cudaStreamSynchronize(s);
   cudaFree(dm);
   cudaFree(ws_o);

@@ -37,7 +37,13 @@ struct AttnParams {
   float* ws_o;               // split partials [slot][Hkv][G][Dh]
   float* ws_ml;              // [slot][Hkv][G][2]
   int* counters;             // [n_seqs][Hkv], zero-initialised, self-resetting
+  // balanced decode schedule: CTA c owns decode segments [seg_start[c], seg_start[c+1])
+  const int* seg_start;
 };
+
+// Persistent decode attention over balanced key segments (kv head in item.pad[0]).
+cudaError_t launch_decode_attention(const void* kv_map, const AttnParams& p, int n_cta, int group,
+                                    cudaStream_t stream);
 
 int make_kv_tensor_map(void* map_out /* CUtensorMap, 128 B */, const void* pool, uint64_t total_rows);
 cudaError_t launch_paged_attention(const void* kv_map, const AttnParams& p, int n_items,
