@@ -439,30 +439,27 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    if (lane == 0) {
-      int g = 0;  // global stage counter across this CTA's segments
-      for (int sg = seg0; sg < seg1; ++sg) {
-        const AttnItem it = p.items[sg];
-        const int kvh = it.pad[0];
-        const int* btab = p.block_tables + (size_t)it.seq * p.max_blocks;
-        const int first_blk = it.key_begin / kBT, last_blk = (it.key_end - 1) / kBT;
-        const int nst = (last_blk - first_blk) / kStageBlocks + 1;
-        for (int st = 0; st < nst; ++st, ++g) {
-          const int slot = g % kStages;
-          if (g >= kStages) mbar_wait(&empty_bar[slot], ((g / kStages) - 1) & 1);
-          const int b0 = first_blk + st * kStageBlocks;
-          const int nb = min(kStageBlocks, last_blk - b0 + 1);
-          mbar_arrive_expect_tx(&full_bar[slot], nb * 2 * kBlockBytes);
-          uint8_t* dst = stage_base + slot * kStageBytes;
-          for (int b = 0; b < nb; ++b) {
-            const int blk = btab[b0 + b];
-            const int rowK = (((blk * p.n_layers + p.layer) * 2 + 0) * p.n_kv_heads + kvh) * kBT;
-            const int rowV = rowK + p.n_kv_heads * kBT;
-            tma_load_2d(dst + (b * 2 + 0) * kBlockBytes, &kv_map, 0, rowK, &full_bar[slot]);
-            tma_load_2d(dst + (b * 2 + 0) * kBlockBytes + 2048, &kv_map, 64, rowK, &full_bar[slot]);
-            tma_load_2d(dst + (b * 2 + 1) * kBlockBytes, &kv_map, 0, rowV, &full_bar[slot]);
-            tma_load_2d(dst + (b * 2 + 1) * kBlockBytes + 2048, &kv_map, 64, rowV, &full_bar[slot]);
-          }
+    // the 16 boxes of a stage (4 blocks x K|V x two 64-dim halves): one lane each
+    const int b = lane >> 2, is_v = (lane >> 1) & 1, h = lane & 1;
+    int g = 0;  // global stage counter across this CTA's segments
+    for (int sg = seg0; sg < seg1; ++sg) {
+      const AttnItem it = p.items[sg];
+      const int kvh = it.pad[0];
+      const int* btab = p.block_tables + (size_t)it.seq * p.max_blocks;
+      const int first_blk = it.key_begin / kBT, last_blk = (it.key_end - 1) / kBT;
+      const int nst = (last_blk - first_blk) / kStageBlocks + 1;
+      for (int st = 0; st < nst; ++st, ++g) {
+        const int slot = g % kStages;
+        if (g >= kStages) mbar_wait(&empty_bar[slot], ((g / kStages) - 1) & 1);
+        const int b0 = first_blk + st * kStageBlocks;
+        const int nb = min(kStageBlocks, last_blk - b0 + 1);
+        if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], nb * 2 * kBlockBytes);
+        __syncwarp();
+        if (lane < 16 && b < nb) {
+          const int blk = btab[b0 + b];
+          const int row = (((blk * p.n_layers + p.layer) * 2 + is_v) * p.n_kv_heads + kvh) * kBT;
+          tma_load_2d(stage_base + slot * kStageBytes + (b * 2 + is_v) * kBlockBytes + h * 2048, &kv_map, h * 64,
+                      row, &full_bar[slot]);
         }
       }
     }

@@ -23,7 +23,11 @@ def main():
     rng = np.random.default_rng(0)
     bt = np.arange(2048, dtype=np.int32)
     out = []
-    for m, n in ((1024, 0), (4096, 0), (8192, 0), (1536, 6144), (2048, 14336), (2048, 30720)):
+    cases = ((1024, 0), (4096, 0), (8192, 0), (1536, 6144), (2048, 14336), (2048, 30720))
+    if os.environ.get("PPD_SWEEP"):
+        m0, n0 = (int(v) for v in os.environ["PPD_SWEEP"].split(","))
+        cases = ((m0, n0),)
+    for m, n in cases:
         toks = rng.integers(0, cfg.vocab, m).astype(np.int32)
         dev.step([m], [n], toks, bt)  # warm
         dev.set_profiling(True)
