@@ -27,8 +27,9 @@ constexpr int kBT = 16;
 constexpr int kDh = 128;
 constexpr int kKeys = 128;                  // keys per block
 constexpr int kTile = 32768;                // 128 x 128 bf16
-constexpr int kStages = 2;
-constexpr int kSmem = 1024 + kTile /*Q*/ + kStages * 2 * kTile /*K,V*/ + kTile /*P*/ + 256;
+constexpr int kKStages = 3;                 // K ring: released as soon as S_j retires
+constexpr int kVStages = 2;                 // V ring: released after PV_j
+constexpr int kSmem = 1024 + kTile /*Q*/ + (kKStages + kVStages) * kTile + kTile /*P*/ + 256;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;   // log2 domain
 
@@ -52,17 +53,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* q_s = smem;
-  uint8_t* kv_s = smem + kTile;                        // [stage][K|V]
-  uint8_t* p_s = kv_s + kStages * 2 * kTile;
+  uint8_t* k_s = smem + kTile;                         // [kKStages]
+  uint8_t* v_s = k_s + kKStages * kTile;               // [kVStages]
+  uint8_t* p_s = v_s + kVStages * kTile;
   uint64_t* bars = reinterpret_cast<uint64_t*>(p_s + kTile);
-  uint64_t* k_full = bars;            // [2]
-  uint64_t* v_full = bars + 2;        // [2]
-  uint64_t* kv_empty = bars + 4;      // [2]
-  uint64_t* s_full = bars + 6;        // [2]
-  uint64_t* p_ready = bars + 8;
-  uint64_t* o_done = bars + 9;
-  uint64_t* q_ready = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* k_full = bars;            // [3]
+  uint64_t* k_empty = bars + 3;       // [3]
+  uint64_t* v_full = bars + 6;        // [2]
+  uint64_t* v_empty = bars + 8;       // [2]
+  uint64_t* s_full = bars + 10;       // [2]
+  uint64_t* p_ready = bars + 12;
+  uint64_t* o_done = bars + 13;
+  uint64_t* q_ready = bars + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   pdl_wait();
   const AttnItem it = p.items[blockIdx.x];
@@ -79,12 +82,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int* btab = p.block_tables + (size_t)s * p.max_blocks;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kKStages; ++i) {
       mbar_init(&k_full[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
+      mbar_init(&k_empty[i], 1);
     }
+    for (int i = 0; i < kVStages; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) mbar_init(&s_full[i], 1);
     mbar_init(p_ready, 4);
     mbar_init(o_done, 1);
     mbar_init(q_ready, 4);
@@ -97,25 +103,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_o = tmem + 2 * kKeys;
 
-  if (warp == 0) {
-    // The 32 TMA boxes of a 128-key stage (8 paged blocks x K|V x two 64-dim
-    // halves) are issued by the 32 lanes in parallel: one lane, one box.
+  if (warp == 0 || warp == 3) {
+    // warp 0 streams K, warp 3 streams V; the 16 TMA boxes of a 128-key tile
+    // (8 paged blocks x two 64-dim halves) are issued by 16 lanes in parallel.
+    const bool is_v = warp == 3;
+    const int n_st = is_v ? kVStages : kKStages;
+    uint64_t* fullb = is_v ? v_full : k_full;
+    uint64_t* emptyb = is_v ? v_empty : k_empty;
+    uint8_t* ring = is_v ? v_s : k_s;
     const int last_blk = (key_end - 1) / kBT;
-    const int b = (lane >> 2) & 7, h = lane & 1, is_v = (lane >> 1) & 1;
+    const int b = (lane >> 1) & 7, h = lane & 1;
     for (int j = 0; j < nblk; ++j) {
-      const int st = j % kStages;
-      if (j >= kStages) mbar_wait(&kv_empty[st], ((j / kStages) - 1) & 1);
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&k_full[st], kTile);
-        mbar_arrive_expect_tx(&v_full[st], kTile);
-      }
+      const int st = j % n_st;
+      if (j >= n_st) mbar_wait(&emptyb[st], ((j / n_st) - 1) & 1);
+      if (lane == 0) mbar_arrive_expect_tx(&fullb[st], kTile);
       __syncwarp();
-      // slots past the sequence re-load its last block: finite data, masked to p = 0
-      const int pb = min(j * (kKeys / kBT) + b, last_blk);
-      const int blk = btab[pb];
-      const int row = ((((blk * p.n_layers + p.layer) * 2 + is_v) * p.n_kv_heads + kvh)) * kBT;
-      uint8_t* dst = kv_s + (st * 2 + is_v) * kTile + h * (kTile / 2) + b * 2048;
-      tc::tma_load_2d(dst, &kv_map, h * 64, row, is_v ? &v_full[st] : &k_full[st]);
+      if (lane < 16) {
+        // slots past the sequence re-load its last block: finite data, masked to p = 0
+        const int pb = min(j * (kKeys / kBT) + b, last_blk);
+        const int blk = btab[pb];
+        const int row = (((blk * p.n_layers + p.layer) * 2 + (is_v ? 1 : 0)) * p.n_kv_heads + kvh) * kBT;
+        tc::tma_load_2d(ring + st * kTile + h * (kTile / 2) + b * 2048, &kv_map, h * 64, row, &fullb[st]);
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -126,10 +135,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t qa = smem_u32(q_s), pa = smem_u32(p_s);
       for (int j = 0; j <= nblk; ++j) {
         if (j < nblk) {
-          const int st = j % kStages;
-          mbar_wait(&k_full[st], (j / kStages) & 1);
+          const int st = j % kKStages;
+          mbar_wait(&k_full[st], (j / kKStages) & 1);
           tc::fence_after();
-          const uint32_t ka = smem_u32(kv_s + (st * 2 + 0) * kTile);
+          const uint32_t ka = smem_u32(k_s + st * kTile);
 #pragma unroll
           for (int kk = 0; kk < kDh / 16; ++kk) {
             const uint32_t off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
@@ -137,13 +146,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                             id_s, kk > 0);
           }
           tc::commit(&s_full[j & 1]);
+          tc::commit(&k_empty[st]);  // K tile free once S_j retires
         }
         if (j >= 1) {
-          const int jj = j - 1, st = jj % kStages;
+          const int jj = j - 1, st = jj % kVStages;
           mbar_wait(p_ready, jj & 1);
-          mbar_wait(&v_full[st], (jj / kStages) & 1);
+          mbar_wait(&v_full[st], (jj / kVStages) & 1);
           tc::fence_after();
-          const uint32_t va = smem_u32(kv_s + (st * 2 + 1) * kTile);
+          const uint32_t va = smem_u32(v_s + st * kTile);
 #pragma unroll
           for (int kk = 0; kk < kKeys / 16; ++kk) {
             const uint32_t poff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
@@ -151,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             id_o, (jj > 0) || (kk > 0));
           }
           tc::commit(o_done);
-          tc::commit(&kv_empty[st]);
+          tc::commit(&v_empty[st]);
         }
       }
     }
