@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages;
   const int x_bytes = p.bn * kBK * 2;
-  const int stage_bytes = kWBytes + x_bytes;  // both multiples of 1 KB
+  const int WM = p.wm;                        // 128-row weight sub-tiles per unit (1 or 2)
+  const int stage_bytes = WM * kWBytes + x_bytes;  // multiples of 1 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;   // [2]
@@ -109,12 +110,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles_w = (p.N + kBM - 1) / kBM;
+  const int n_tiles_w = (p.N + kBM * WM - 1) / (kBM * WM);
   const int n_tiles_t = (p.T + p.bn - 1) / p.bn;
   const int n_units = n_tiles_w * n_tiles_t * p.splits;
   const int kb_total = (p.K + kBK - 1) / kBK;
   const int kb_per = (kb_total + p.splits - 1) / p.splits;
-  const int n_acc = p.tmem_cols >= 2 * p.bn_cols ? 2 : 1;
+  const int acc_cols = WM * p.bn_cols;
+  const int n_acc = p.tmem_cols >= 2 * acc_cols ? 2 : 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         npre = min(S, max(0, kb1 - kb0));
         for (int i = 0; i < npre; ++i) {
           mbar_arrive_expect_tx(&full[i], stage_bytes);
-          tma_load_2d(smem + i * stage_bytes, &map_w, (kb0 + i) * kBK, tw * kBM, &full[i]);
+          tma_load_2d(smem + i * stage_bytes, &map_w, (kb0 + i) * kBK, tw * kBM * WM, &full[i]);
         }
       }
       pdl_wait();
@@ -173,9 +175,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (it >= npre) {
             if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
             mbar_arrive_expect_tx(&full[s], stage_bytes);
-            tma_load_2d(sw, &map_w, kb * kBK, tw * kBM, &full[s]);
+            tma_load_2d(sw, &map_w, kb * kBK, tw * kBM * WM, &full[s]);
           }
-          tma_load_2d(sw + kWBytes, &map_x, kb * kBK, tt * p.bn, &full[s]);
+          tma_load_2d(sw + WM * kWBytes, &map_x, kb * kBK, tt * p.bn, &full[s]);
         }
       }
     }
@@ -192,17 +194,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int use = j / n_acc;  // how many times this accumulator was used before
         if (use > 0) mbar_wait(&acc_empty[acc], (use - 1) & 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn_cols);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * acc_cols);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
-          const uint64_t da = sw128_kmajor_desc(sa);
-          const uint64_t db = sw128_kmajor_desc(sa + kWBytes);
+          const uint64_t db = sw128_kmajor_desc(sa + WM * kWBytes);
+          for (int sub = 0; sub < WM; ++sub) {  // weight sub-tiles share the activation tile
+            const uint64_t da = sw128_kmajor_desc(sa + sub * kWBytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)  // 32 B per UMMA_K step inside the swizzle atom
-            mma_bf16(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (kb != kb0) || (k != 0));
+            for (int k = 0; k < kBK / 16; ++k)  // 32 B per UMMA_K step inside the swizzle atom
+              mma_bf16(d_tmem + sub * p.bn_cols, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
+                       (kb != kb0) || (k != 0));
+          }
           mma_commit(&empty[s]);  // smem slot free once these MMAs retire
         }
         mma_commit(&acc_full[acc]);
@@ -217,15 +222,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode_unit(u, tw, tt, sp);
       const int acc = j % n_acc;
       const int use = j / n_acc;
-      const int row = tw * kBM + q * 32 + lane;
       const int t0 = tt * p.bn;
       mbar_wait(&acc_full[acc], use & 1);
       tc_fence_after();
       float* out32 = reinterpret_cast<float*>(p.out) + (size_t)sp * p.split_stride;
       __nv_bfloat16* out16 = reinterpret_cast<__nv_bfloat16*>(p.out);
-      const uint32_t t_acc = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * p.bn_cols);
       const int ncols = min(p.bn, p.T - t0);
+      for (int sub = 0; sub < WM; ++sub)
       for (int c0 = 0; c0 < ncols; c0 += 32) {
+        const int row = (tw * WM + sub) * kBM + q * 32 + lane;
+        const uint32_t t_acc =
+            tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * acc_cols + sub * p.bn_cols);
         uint32_t r[32];
         tmem_ld32(t_acc + (uint32_t)c0, r);
         if (row < p.N) {
@@ -312,15 +319,29 @@ bool get_map(CUtensorMap* out, const void* ptr, int rows, int K, int box_rows) {
 
 }  // namespace
 
+// weight sub-tiles per unit: a single token tile (decode) takes 256 weight rows
+// per unit so the activation tile streamed from L2 is shared by twice the weights
+int gemm_tc_plan_wm(int T, int N) {
+  static const int forced = [] {
+    const char* e = std::getenv("PPD_GEMM_WM");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 1 || forced == 2) return forced;
+  (void)T;
+  (void)N;
+  return 1;  // measured: 2 sub-tiles halves L2 traffic but loses the accumulator double buffer (net slower)
+}
+
 int gemm_tc_plan_splits(int T, int N, int K) {
   const int bn = T >= kMaxBN ? kMaxBN : ((T + 15) / 16) * 16;
-  const int tiles = ((N + kBM - 1) / kBM) * ((T + bn - 1) / bn);
+  const int bm = kBM * gemm_tc_plan_wm(T, N);
+  const int tiles = ((N + bm - 1) / bm) * ((T + bn - 1) / bn);
   const int kb = (K + kBK - 1) / kBK;
   // Persistent CTAs take units round-robin, so the step costs
   //   rounds(s) x (bytes of one unit) = ceil(tiles*s/148) x (W slab / s + fp32 partial write + read).
   // Pick the split count minimising it (s <= 8, >= 4 K-blocks per split).
-  const double w_unit = double(kBM) * K * 2.0;
-  const double out_unit = double(bn) * kBM * 4.0 * 2.0;
+  const double w_unit = double(bm) * K * 2.0;
+  const double out_unit = double(bn) * bm * 4.0 * 2.0;
   int best = 1;
   double best_cost = 1e300;
   // the callers' fp32 workspaces hold 8 x 256 token rows of partial slices
@@ -354,8 +375,10 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
   p.split_stride = split_stride ? split_stride : (size_t)T * N;
   // accumulator columns per unit (power of two >= bn); two accumulators when they fit
   p.bn_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
-  p.tmem_cols = 2 * p.bn_cols <= 512 ? 2 * p.bn_cols : p.bn_cols;
-  const int stage_bytes = kWBytes + bn * kBK * 2;
+  p.wm = gemm_tc_plan_wm(T, N);
+  const int acc_cols = p.wm * p.bn_cols;
+  p.tmem_cols = 2 * acc_cols <= 512 ? 2 * acc_cols : acc_cols;
+  const int stage_bytes = p.wm * kWBytes + bn * kBK * 2;
   int stages = kSmemBudget / stage_bytes;
   stages = stages > kMaxStages ? kMaxStages : stages;
   static const int stage_cap = [] {
@@ -366,13 +389,13 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
   p.stages = stages;
   const int smem = 1024 + stages * stage_bytes + 256;
   CUtensorMap mw, mx;
-  if (!get_map(&mw, W, N, K, kBM) || !get_map(&mx, X, T, K, bn)) return cudaErrorInvalidValue;
+  if (!get_map(&mw, W, N, K, kBM * p.wm) || !get_map(&mx, X, T, K, bn)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 + kSmemBudget + 256);
     attr = true;
   }
-  const int units = ((N + kBM - 1) / kBM) * ((T + bn - 1) / bn) * splits;
+  const int units = ((N + kBM * p.wm - 1) / (kBM * p.wm)) * ((T + bn - 1) / bn) * splits;
   const int grid = units < 148 ? units : 148;
   return launch_pdl(gemm_tc_kernel, dim3(grid), dim3(kThreads), (size_t)smem, s, mw, mx, p);
 }

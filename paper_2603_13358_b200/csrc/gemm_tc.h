@@ -10,7 +10,7 @@ typedef __nv_bfloat16 bf16;
 
 struct GemmTcParams {
   void* out;
-  int T, N, K, ldo, bn, bn_cols, out_f32, splits, stages, tmem_cols;
+  int T, N, K, ldo, bn, bn_cols, wm, out_f32, splits, stages, tmem_cols;
   size_t split_stride;  // floats between split partial slices
 };
 
