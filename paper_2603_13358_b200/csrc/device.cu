@@ -971,7 +971,7 @@ int ppd_op_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int
 
 int ppd_op_gemm_tc(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K, int32_t out_f32,
                    int32_t splits, void* stream) {
-  CHECK_ARG(A && B && C && M > 0 && N > 0 && K > 0 && splits >= 0, "bad gemm args");
+  CHECK_ARG(A && B && C && M > 0 && N > 0 && K > 0 && splits >= 1, "bad gemm args");
   CHECK_ARG(K % 8 == 0, "K must be a multiple of 8");
   CHECK_ARG(splits == 1 || out_f32, "K-split partials need fp32 output");
   CU(gemm_tc_run(static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0, splits,

@@ -13,7 +13,6 @@ namespace ppdk {
 struct GemmContext {
   cublasHandle_t handle = nullptr;
   bool tc = true;
-  bool streamk = true;
 };
 
 GemmContext* gemm_create() {
@@ -24,10 +23,6 @@ GemmContext* gemm_create() {
   }
   const char* e = std::getenv("PPD_GEMM");
   c->tc = !(e && std::strcmp(e, "cublas") == 0);
-  const char* sched = std::getenv("PPD_GEMM_SCHED");
-  // split-K with consumer-summed slices is the default: measured faster than the
-  // stream-K owner fix-up at decode token counts (the fix-up epilogue is L2-latency bound)
-  c->streamk = sched && std::strcmp(sched, "streamk") == 0;
   return c;
 }
 
@@ -54,7 +49,7 @@ cudaError_t gemm_run_cublas(GemmContext* c, const __nv_bfloat16* A, const __nv_b
 cudaError_t gemm_run(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N, int K,
                      bool out_f32, cudaStream_t s) {
   if (!c->tc) return gemm_run_cublas(c, A, B, C, M, N, K, out_f32, s);
-  return gemm_tc_run(A, B, C, M, N, K, out_f32, c->streamk ? 0 : 1, 0, s);
+  return gemm_tc_run(A, B, C, M, N, K, out_f32, 1, 0, s);
 }
 
 cudaError_t gemm_run_split(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, float* C, int M, int N,
@@ -62,10 +57,6 @@ cudaError_t gemm_run_split(GemmContext* c, const __nv_bfloat16* A, const __nv_bf
   if (!c->tc) {
     *n_part = 1;
     return gemm_run_cublas(c, A, B, C, M, N, K, true, s);
-  }
-  if (c->streamk) {  // balanced stream-K: one final slice, no partial traffic for the consumer
-    *n_part = 1;
-    return gemm_tc_run(A, B, C, M, N, K, true, 0, 0, s);
   }
   const int splits = gemm_tc_plan_splits(M, N, K);
   *n_part = splits;

@@ -101,8 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int S = p.stages;
   const int x_bytes = p.bn * kBK * 2;
-  const int WM = p.wm;                        // 128-row weight sub-tiles per unit (1 or 2)
-  const int stage_bytes = WM * kWBytes + x_bytes;  // multiples of 1 KB
+  const int stage_bytes = kWBytes + x_bytes;  // both multiples of 1 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;   // [2]
@@ -110,13 +109,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles_w = (p.N + kBM * WM - 1) / (kBM * WM);
+  const int n_tiles_w = (p.N + kBM - 1) / kBM;
   const int n_tiles_t = (p.T + p.bn - 1) / p.bn;
   const int n_units = n_tiles_w * n_tiles_t * p.splits;
   const int kb_total = (p.K + kBK - 1) / kBK;
-  const int kb_per = p.splits > 0 ? (kb_total + p.splits - 1) / p.splits : kb_total;
-  const int acc_cols = WM * p.bn_cols;
-  const int n_acc = p.tmem_cols >= 2 * acc_cols ? 2 : 1;
+  const int kb_per = (kb_total + p.splits - 1) / p.splits;
+  const int n_acc = p.tmem_cols >= 2 * p.bn_cols ? 2 : 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -140,41 +138,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();  // the next kernel may launch; it waits for our completion itself
 
-  // Work decomposition. Split mode (p.splits >= 1): units (weight tile, token
-  // tile, K split) round-robin over CTAs, each split writing its own fp32 slice.
-  // Stream-K mode (p.splits == 0): the n_tiles x kb_total K-blocks are cut into
-  // one contiguous range of p.per blocks per CTA; a tile cut by range
-  // boundaries is finished by its first CTA (the "owner", which reaches it
-  // last in time), which adds the partials the later CTAs parked in the
-  // workspace (deterministic order) and writes the single final output.
-  const bool streamk = p.splits == 0;
-  const int n_tiles = n_tiles_w * n_tiles_t;
-  const int g_begin = streamk ? blockIdx.x * p.per : 0;
-  const int g_end = streamk ? min(n_tiles * kb_total, g_begin + p.per) : 0;
-  // piece iterator: (tile, k0, k1, split) ; returns false when the CTA is done
-  struct Piece {
-    int tw, tt, sp, k0, k1, tile;
-  };
-  auto first_piece = [&](int& cursor) { cursor = streamk ? g_begin : (int)blockIdx.x; };
-  auto next_piece = [&](int& cursor, Piece& pc) -> bool {
-    if (streamk) {
-      if (cursor >= g_end) return false;
-      pc.tile = cursor / kb_total;
-      pc.k0 = cursor % kb_total;
-      pc.k1 = min(kb_total, pc.k0 + (g_end - cursor));
-      pc.sp = 0;
-      cursor += pc.k1 - pc.k0;
-    } else {
-      if (cursor >= n_units) return false;
-      pc.sp = cursor % p.splits;
-      pc.tile = cursor / p.splits;
-      pc.k0 = pc.sp * kb_per;
-      pc.k1 = min(kb_total, pc.k0 + kb_per);
-      cursor += gridDim.x;
-    }
-    pc.tt = pc.tile % n_tiles_t;
-    pc.tw = pc.tile / n_tiles_t;
-    return true;
+  // unit -> (weight tile, token tile, split); token tile fastest
+  auto decode_unit = [&](int u, int& tw, int& tt, int& sp) {
+    sp = u % p.splits;
+    const int rest = u / p.splits;
+    tt = rest % n_tiles_t;
+    tw = rest / n_tiles_t;
   };
 
   if (warp == 0) {
@@ -182,33 +151,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Weights do not depend on the previous kernel: stream the first stages of
       // W before waiting on it (PDL), then the activations.
       int npre = 0;
-      {
-        int cur;
-        Piece pc;
-        first_piece(cur);
-        if (next_piece(cur, pc)) {
-          npre = min(S, max(0, pc.k1 - pc.k0));
-          for (int i = 0; i < npre; ++i) {
-            mbar_arrive_expect_tx(&full[i], stage_bytes);
-            tma_load_2d(smem + i * stage_bytes, &map_w, (pc.k0 + i) * kBK, pc.tw * kBM * WM, &full[i]);
-          }
+      if ((int)blockIdx.x < n_units) {
+        int tw, tt, sp;
+        decode_unit(blockIdx.x, tw, tt, sp);
+        const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+        npre = min(S, max(0, kb1 - kb0));
+        for (int i = 0; i < npre; ++i) {
+          mbar_arrive_expect_tx(&full[i], stage_bytes);
+          tma_load_2d(smem + i * stage_bytes, &map_w, (kb0 + i) * kBK, tw * kBM, &full[i]);
         }
       }
       pdl_wait();
-      int it = 0;  // global stage counter across pieces
-      int cur;
-      Piece pc;
-      first_piece(cur);
-      while (next_piece(cur, pc)) {
-        for (int kb = pc.k0; kb < pc.k1; ++kb, ++it) {
+      int it = 0;  // global stage counter across units
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int tw, tt, sp;
+        decode_unit(u, tw, tt, sp);
+        const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % S;
           uint8_t* sw = smem + s * stage_bytes;
           if (it >= npre) {
             if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
             mbar_arrive_expect_tx(&full[s], stage_bytes);
-            tma_load_2d(sw, &map_w, kb * kBK, pc.tw * kBM * WM, &full[s]);
+            tma_load_2d(sw, &map_w, kb * kBK, tw * kBM, &full[s]);
           }
-          tma_load_2d(sw + WM * kWBytes, &map_x, kb * kBK, pc.tt * p.bn, &full[s]);
+          tma_load_2d(sw + kWBytes, &map_x, kb * kBK, tt * p.bn, &full[s]);
         }
       }
     }
@@ -217,28 +184,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.bn >> 3) << 17) |
                              ((uint32_t)(kBM >> 4) << 24);
       int it = 0, j = 0;
-      int cur;
-      Piece pc;
-      first_piece(cur);
-      for (; next_piece(cur, pc); ++j) {
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
+        int tw, tt, sp;
+        decode_unit(u, tw, tt, sp);
+        const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
         const int acc = j % n_acc;
         const int use = j / n_acc;  // how many times this accumulator was used before
         if (use > 0) mbar_wait(&acc_empty[acc], (use - 1) & 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * acc_cols);
-        for (int kb = pc.k0; kb < pc.k1; ++kb, ++it) {
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn_cols);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
-          const uint64_t db = sw128_kmajor_desc(sa + WM * kWBytes);
-          for (int sub = 0; sub < WM; ++sub) {  // weight sub-tiles share the activation tile
-            const uint64_t da = sw128_kmajor_desc(sa + sub * kWBytes);
+          const uint64_t da = sw128_kmajor_desc(sa);
+          const uint64_t db = sw128_kmajor_desc(sa + kWBytes);
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)  // 32 B per UMMA_K step inside the swizzle atom
-              mma_bf16(d_tmem + sub * p.bn_cols, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
-                       (kb != pc.k0) || (k != 0));
-          }
+          for (int k = 0; k < kBK / 16; ++k)  // 32 B per UMMA_K step inside the swizzle atom
+            mma_bf16(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (kb != kb0) || (k != 0));
           mma_commit(&empty[s]);  // smem slot free once these MMAs retire
         }
         mma_commit(&acc_full[acc]);
@@ -247,63 +211,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     pdl_wait();  // outputs are written only after the predecessor retired
     const int q = warp & 3;  // TMEM lane quarter owned by this warp
-    const int etid = threadIdx.x - 128;  // 0..127 among the epilogue warps
     int j = 0;
-    int cur;
-    Piece pc;
-    first_piece(cur);
-    for (; next_piece(cur, pc); ++j) {
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
+      int tw, tt, sp;
+      decode_unit(u, tw, tt, sp);
       const int acc = j % n_acc;
       const int use = j / n_acc;
-      const int t0 = pc.tt * p.bn;
-      // stream-K role of this piece
-      int c_first = blockIdx.x, c_last = blockIdx.x;
-      if (streamk) {
-        c_first = (pc.tile * kb_total) / p.per;
-        c_last = (pc.tile * kb_total + kb_total - 1) / p.per;
-      }
-      const bool parked = streamk && (int)blockIdx.x != c_first;  // partial goes to the workspace
-      const bool owner = streamk && c_last > c_first && (int)blockIdx.x == c_first;
-      if (owner) {  // wait for the later CTAs' partials of this tile
-        if (etid == 0)
-          for (int c = c_first + 1; c <= c_last; ++c) {
-            unsigned v;
-            do {
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.flags + c) : "memory");
-            } while (v == 0u);
-          }
-        named_barrier_sync(2, 128);
-      }
+      const int row = tw * kBM + q * 32 + lane;
+      const int t0 = tt * p.bn;
       mbar_wait(&acc_full[acc], use & 1);
       tc_fence_after();
-      float* out32 = reinterpret_cast<float*>(p.out) + (size_t)pc.sp * p.split_stride;
+      float* out32 = reinterpret_cast<float*>(p.out) + (size_t)sp * p.split_stride;
       __nv_bfloat16* out16 = reinterpret_cast<__nv_bfloat16*>(p.out);
-      float* park = p.ws + (size_t)blockIdx.x * (kMaxBN * kBM * 2);
+      const uint32_t t_acc = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * p.bn_cols);
       const int ncols = min(p.bn, p.T - t0);
-      for (int sub = 0; sub < WM; ++sub)
       for (int c0 = 0; c0 < ncols; c0 += 32) {
-        const int rloc = sub * kBM + q * 32 + lane;
-        const int row = pc.tw * WM * kBM + rloc;
-        const uint32_t t_acc =
-            tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * acc_cols + sub * p.bn_cols);
         uint32_t r[32];
         tmem_ld32(t_acc + (uint32_t)c0, r);
-        const int nj = min(32, ncols - c0);
-        if (parked) {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj)
-            if (jj < nj) park[(size_t)(c0 + jj) * (kBM * WM) + rloc] = __uint_as_float(r[jj]);
-          continue;
-        }
-        if (owner) {
-          for (int c = c_first + 1; c <= c_last; ++c) {
-            const float* src = p.ws + (size_t)c * (kMaxBN * kBM * 2);
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-              if (jj < nj) r[jj] = __float_as_uint(__uint_as_float(r[jj]) + __ldcg(src + (size_t)(c0 + jj) * (kBM * WM) + rloc));
-          }
-        }
         if (row < p.N) {
+          const int nj = min(32, ncols - c0);
           if (p.out_f32) {
             float* dst = out32 + (size_t)(t0 + c0) * p.ldo + row;
 #pragma unroll
@@ -320,13 +246,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
-      if (parked) {  // publish the partial for the owner
-        __threadfence();
-        named_barrier_sync(2, 128);
-        if (etid == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.flags + blockIdx.x), "r"(1u) : "memory");
-      }
-      if (owner && etid == 0)  // reset for the next launch (each flag has exactly one reader)
-        for (int c = c_first + 1; c <= c_last; ++c) p.flags[c] = 0u;
     }
   }
   tc_fence_before();
@@ -393,29 +312,15 @@ bool get_map(CUtensorMap* out, const void* ptr, int rows, int K, int box_rows) {
 
 }  // namespace
 
-// weight sub-tiles per unit: a single token tile (decode) takes 256 weight rows
-// per unit so the activation tile streamed from L2 is shared by twice the weights
-int gemm_tc_plan_wm(int T, int N) {
-  static const int forced = [] {
-    const char* e = std::getenv("PPD_GEMM_WM");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (forced == 1 || forced == 2) return forced;
-  (void)T;
-  (void)N;
-  return 1;  // measured: 2 sub-tiles halves L2 traffic but loses the accumulator double buffer (net slower)
-}
-
 int gemm_tc_plan_splits(int T, int N, int K) {
   const int bn = T >= kMaxBN ? kMaxBN : ((T + 15) / 16) * 16;
-  const int bm = kBM * gemm_tc_plan_wm(T, N);
-  const int tiles = ((N + bm - 1) / bm) * ((T + bn - 1) / bn);
+  const int tiles = ((N + kBM - 1) / kBM) * ((T + bn - 1) / bn);
   const int kb = (K + kBK - 1) / kBK;
   // Persistent CTAs take units round-robin, so the step costs
   //   rounds(s) x (bytes of one unit) = ceil(tiles*s/148) x (W slab / s + fp32 partial write + read).
   // Pick the split count minimising it (s <= 8, >= 4 K-blocks per split).
-  const double w_unit = double(bm) * K * 2.0;
-  const double out_unit = double(bn) * bm * 4.0 * 2.0;
+  const double w_unit = double(kBM) * K * 2.0;
+  const double out_unit = double(bn) * kBM * 4.0 * 2.0;
   int best = 1;
   double best_cost = 1e300;
   // the callers' fp32 workspaces hold 8 x 256 token rows of partial slices
@@ -435,7 +340,7 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
   if (T <= 0) return cudaSuccess;
   if (K % 8 != 0) return cudaErrorInvalidValue;  // TMA row stride must be 16 B aligned
   const int bn = T >= kMaxBN ? kMaxBN : ((T + 15) / 16) * 16;
-  if (splits < 0) splits = 0;  // 0 = stream-K (single final output)
+  if (splits < 1) splits = 1;
   if (splits > 1 && !out_f32) return cudaErrorInvalidValue;
   GemmTcParams p{};
   p.out = out;
@@ -449,10 +354,8 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
   p.split_stride = split_stride ? split_stride : (size_t)T * N;
   // accumulator columns per unit (power of two >= bn); two accumulators when they fit
   p.bn_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
-  p.wm = gemm_tc_plan_wm(T, N);
-  const int acc_cols = p.wm * p.bn_cols;
-  p.tmem_cols = 2 * acc_cols <= 512 ? 2 * acc_cols : acc_cols;
-  const int stage_bytes = p.wm * kWBytes + bn * kBK * 2;
+  p.tmem_cols = 2 * p.bn_cols <= 512 ? 2 * p.bn_cols : p.bn_cols;
+  const int stage_bytes = kWBytes + bn * kBK * 2;
   int stages = kSmemBudget / stage_bytes;
   stages = stages > kMaxStages ? kMaxStages : stages;
   static const int stage_cap = [] {
@@ -463,39 +366,14 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
   p.stages = stages;
   const int smem = 1024 + stages * stage_bytes + 256;
   CUtensorMap mw, mx;
-  if (!get_map(&mw, W, N, K, kBM * p.wm) || !get_map(&mx, X, T, K, bn)) return cudaErrorInvalidValue;
+  if (!get_map(&mw, W, N, K, kBM) || !get_map(&mx, X, T, K, bn)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 + kSmemBudget + 256);
     attr = true;
   }
-  const int tiles = ((N + kBM * p.wm - 1) / (kBM * p.wm)) * ((T + bn - 1) / bn);
-  int grid;
-  if (splits == 0) {
-    // stream-K: equal K-block ranges (>= 4 blocks) over at most 148 resident CTAs
-    const long total = (long)tiles * ((K + kBK - 1) / kBK);
-    grid = (int)std::min<long>(148, std::max<long>(1, total / 4));
-    p.per = (int)((total + grid - 1) / grid);
-    grid = (int)((total + p.per - 1) / p.per);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    static std::mutex mu;
-    static std::unordered_map<int, std::pair<float*, unsigned*>> bufs;  // per device, never freed
-    {
-      std::lock_guard<std::mutex> lk(mu);
-      auto& b = bufs[dev];
-      if (!b.first) {
-        if (cudaMalloc(&b.first, (size_t)148 * kMaxBN * kBM * 2 * sizeof(float)) != cudaSuccess ||
-            cudaMalloc(&b.second, 148 * sizeof(unsigned)) != cudaSuccess || cudaMemset(b.second, 0, 148 * sizeof(unsigned)) != cudaSuccess)
-          return cudaErrorMemoryAllocation;
-      }
-      p.ws = b.first;
-      p.flags = b.second;
-    }
-  } else {
-    const int units = tiles * splits;
-    grid = units < 148 ? units : 148;
-  }
+  const int units = ((N + kBM - 1) / kBM) * ((T + bn - 1) / bn) * splits;
+  const int grid = units < 148 ? units : 148;
   return launch_pdl(gemm_tc_kernel, dim3(grid), dim3(kThreads), (size_t)smem, s, mw, mx, p);
 }
 

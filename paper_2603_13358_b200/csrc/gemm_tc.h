@@ -10,12 +10,8 @@ typedef __nv_bfloat16 bf16;
 
 struct GemmTcParams {
   void* out;
-  int T, N, K, ldo, bn, bn_cols, wm, out_f32, splits, stages, tmem_cols;
+  int T, N, K, ldo, bn, bn_cols, out_f32, splits, stages, tmem_cols;
   size_t split_stride;  // floats between split partial slices
-  // stream-K (splits == 0): K-blocks per CTA, parked partials [148][256*256], flags [148]
-  int per;
-  float* ws;
-  unsigned* flags;
 };
 
 // out[T][N] (+ split slices) = X[T][K] . W[N][K]^T ; splits > 1 needs out_f32
