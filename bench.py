@@ -305,6 +305,14 @@ def run_ours(args, rank, world, local_rank):
             ttft = [engine_ttft(D.layout_gpus(lay, world), lay, quick=args.quick) for lay in D.node_layouts(world)]
 
     pk, pk_kind = peaks()
+    traffic = None  # dram read+write per launch of the same kernel/config, from the committed ncu capture
+    try:
+        prof_ncu = json.load(open(os.path.join(REPO, "profiles", "ncu_r01_kernels.json")))
+        k0 = prof_ncu["decode_attention_B200_ctx1024_layer0"][0]
+        if B == 200 and ctx0 == 1024:
+            traffic = (float(k0["dram__bytes_read.sum"]) + float(k0["dram__bytes_write.sum"])) * 1e6
+    except Exception:
+        pass
     attn_gbs = prof["attn_bytes"] / (prof["attn_ms"] * 1e-3) / 1e9 if prof["attn_ms"] > 0 else None
     total_prof_ms = prof["step_ms"]
     step_bytes_kv = float(np.sum(ctx)) * 131072
@@ -344,14 +352,15 @@ def run_ours(args, rank, world, local_rank):
         "interference": inter,
         "ttft_pd_vs_ppd": ttft,
         "roofline": {
-            "kernel": "paged_attention_kernel (K1/K2, decode rows)",
+            "kernel": "decode_attention_kernel (K1, balanced persistent paged decode attention)",
             "bound": "hbm",
             "achieved": attn_gbs,
             "peak": pk["hbm_gbs"],
             "peak_kind": pk_kind,
             "unit": "GB/s",
             "frac": (attn_gbs / pk["hbm_gbs"]) if attn_gbs else None,
-            "traffic": None,
+            "traffic": traffic,
+            "traffic_source": "profiles/ncu_r01_kernels.json (ncu --set full, dram__bytes_read+write per launch)",
             "algorithmic_bytes_per_launch": prof["attn_bytes"] / max(prof["attn_launches"], 1),
             "attn_share_of_step": prof["attn_ms"] / total_prof_ms if total_prof_ms else None,
             "gemm_share_of_step": prof["gemm_ms"] / total_prof_ms if total_prof_ms else None,
