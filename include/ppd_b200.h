@@ -137,6 +137,36 @@ int ppd_op_gemm(const void* A, const void* B, void* C, int32_t M, int32_t N, int
                 int32_t out_f32, void* stream);
 int ppd_op_gemm_tc(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                    int32_t out_f32, int32_t splits, void* stream);
+/* The MLP up-projection with SiLU fused into the tcgen05 epilogue:
+ * m[M][N/2] = bf16(silu(g) * u), g/u the fp32 products of the interleaved
+ * gate|up weight B [N][K] (64-row groups: rows [128j, 128j+64) gate rows
+ * [64j, 64j+64), rows [128j+64, 128j+128) the matching up rows). N % 128 == 0.
+ * Asynchronous on `stream`. */
+int ppd_op_gemm_silu(const void* A, const void* B, void* m, int32_t M, int32_t N, int32_t K,
+                     void* stream);
+/* The forward step's fp32 GEMM path: C = sum of K-partial slices C + j*stride.
+ * Uniform split (kbt == 0): all n slices valid. Balanced partition: slot c owns
+ * items [c*total/slots, (c+1)*total/slots) of the (tile, k-block) space, tile
+ * t = (col / rows) * n_tiles_t + tok / bn; slices j < owner(t*kbt+kbt-1) -
+ * owner(t*kbt) + 1 are valid, owner(x) = ceil((x+1)*slots/total) - 1.
+ * C must hold max_slices * M * N floats. Asynchronous on `stream`. */
+typedef struct ppd_gemm_parts {
+  int32_t n, kbt, slots, rows, bn, n_tiles_t;
+  int64_t total;
+  uint64_t stride;
+} ppd_gemm_parts;
+int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                      int32_t max_slices, ppd_gemm_parts* parts, void* stream);
+/* process-wide kernel tuning knobs (tests and sweeps; defaults are tuned):
+ *   "gemm_pair"   -1 auto (CTA-pair tcgen05 kernel for >= 48 token rows),
+ *                  0 single-CTA kernel, 1 CTA-pair kernel for every shape
+ *   "gemm_stages"  cap on the GEMM smem ring depth (0 = as many as fit)
+ *   "gemm_sched"  -1 auto, 0 uniform K split, 1 balanced partition (fp32 path)
+ *   "mlp_fused"    1 gate|up GEMM with the SiLU epilogue, 0 (default) fp32
+ *                  partials + a separate SiLU kernel
+ * Unknown names -> PPD_ERR_INVALID. Every change makes devices re-capture
+ * their step graphs with the newly selected kernels. */
+int ppd_set_tuning(const char* name, int32_t value);
 /* deterministic random-init fill, identical to the oracle's mo_weight_bf16 */
 int ppd_op_fill_random(void* dst, uint64_t n, uint64_t seed, int32_t tensor, int32_t layer,
                        void* stream);

@@ -63,6 +63,23 @@ def qwen32b_cfg(n_layers: int = 64) -> ModelCfg:
     return ModelCfg(n_layers, 5120, 40, 8, 128, 27648, 152064, 1e-6, 1e6, 1)
 
 
+class GemmParts(ctypes.Structure):
+    """ppd_gemm_parts: how the fp32 GEMM output is spread over K-partial slices."""
+    _fields_ = [("n", ctypes.c_int32), ("kbt", ctypes.c_int32), ("slots", ctypes.c_int32),
+                ("rows", ctypes.c_int32), ("bn", ctypes.c_int32), ("n_tiles_t", ctypes.c_int32),
+                ("total", ctypes.c_int64), ("stride", ctypes.c_uint64)]
+
+    def owner(self, x):
+        return ((x + 1) * self.slots + self.total - 1) // self.total - 1
+
+    def valid(self, col, tok):
+        """Valid slice count for output column `col` of token row `tok` (numpy arrays ok)."""
+        if self.kbt == 0:
+            return col * 0 + tok * 0 + self.n
+        t = (col // self.rows) * self.n_tiles_t + tok // self.bn
+        return self.owner(t * self.kbt + self.kbt - 1) - self.owner(t * self.kbt) + 1
+
+
 class DevStats(ctypes.Structure):
     _fields_ = [
         ("steps", ctypes.c_int64), ("own_launches", ctypes.c_int64), ("lib_launches", ctypes.c_int64),
@@ -85,43 +102,54 @@ class Batch(ctypes.Structure):
 _lib = None
 
 
+def load_lib(path: str = LIB_PATH, strict: bool = True):
+    """Load a build of libppd_b200.so and declare the C-ABI signatures.
+    strict=False skips entry points an older build does not export (A/B tools)."""
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} missing: run `make -C {PKG_DIR}` (no CPU fallback)")
+    L = ctypes.CDLL(path)
+    vp, i32, u64, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int64
+    P = ctypes.POINTER
+    L.ppd_last_error.restype = ctypes.c_char_p
+    sig = {
+        "ppd_version": [],
+        "ppd_device_count": [P(i32)],
+        "ppd_dev_open": [i32, P(ModelCfg), i32, i32, P(vp)],
+        "ppd_dev_close": [vp],
+        "ppd_load_random_weights": [vp, u64],
+        "ppd_kv_pool_init": [vp, i32, i32],
+        "ppd_kv_block_bytes": [P(ModelCfg), i32, P(u64)],
+        "ppd_kv_pool_ptr": [vp, P(vp), P(u64)],
+        "ppd_step": [vp, P(Batch), vp, P(ctypes.c_float)],
+        "ppd_step_submit": [vp, P(Batch)],
+        "ppd_step_wait": [vp, vp, P(ctypes.c_float)],
+        "ppd_last_logits": [vp, vp, i64],
+        "ppd_prefill": [vp, i32, vp, i32, i32, vp, i32, vp, P(ctypes.c_float)],
+        "ppd_kv_copy": [vp, vp, vp, vp, i32, i32, i32, P(ctypes.c_float)],
+        "ppd_op_attention": [P(ModelCfg), vp, vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp],
+        "ppd_op_gemm": [vp, vp, vp, i32, i32, i32, i32, vp],
+        "ppd_op_gemm_tc": [vp, vp, vp, i32, i32, i32, i32, i32, vp],
+        "ppd_op_fill_random": [vp, u64, u64, i32, i32, vp],
+        "ppd_set_tuning": [ctypes.c_char_p, i32],
+        "ppd_op_gemm_silu": [vp, vp, vp, i32, i32, i32, vp],
+        "ppd_op_gemm_parts": [vp, vp, vp, i32, i32, i32, i32, P(GemmParts), vp],
+        "ppd_dev_set_profiling": [vp, i32],
+        "ppd_dev_get_stats": [vp, P(DevStats)],
+        "ppd_dev_reset_stats": [vp],
+    }
+    for name, args in sig.items():
+        if not strict and not hasattr(L, name):
+            continue
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    return L
+
+
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} missing: run `make -C {PKG_DIR}` (no CPU fallback)")
-        L = ctypes.CDLL(LIB_PATH)
-        vp, i32, u64, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int64
-        P = ctypes.POINTER
-        L.ppd_last_error.restype = ctypes.c_char_p
-        sig = {
-            "ppd_version": [],
-            "ppd_device_count": [P(i32)],
-            "ppd_dev_open": [i32, P(ModelCfg), i32, i32, P(vp)],
-            "ppd_dev_close": [vp],
-            "ppd_load_random_weights": [vp, u64],
-            "ppd_kv_pool_init": [vp, i32, i32],
-            "ppd_kv_block_bytes": [P(ModelCfg), i32, P(u64)],
-            "ppd_kv_pool_ptr": [vp, P(vp), P(u64)],
-            "ppd_step": [vp, P(Batch), vp, P(ctypes.c_float)],
-            "ppd_step_submit": [vp, P(Batch)],
-            "ppd_step_wait": [vp, vp, P(ctypes.c_float)],
-            "ppd_last_logits": [vp, vp, i64],
-            "ppd_prefill": [vp, i32, vp, i32, i32, vp, i32, vp, P(ctypes.c_float)],
-            "ppd_kv_copy": [vp, vp, vp, vp, i32, i32, i32, P(ctypes.c_float)],
-            "ppd_op_attention": [P(ModelCfg), vp, vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp],
-            "ppd_op_gemm": [vp, vp, vp, i32, i32, i32, i32, vp],
-            "ppd_op_gemm_tc": [vp, vp, vp, i32, i32, i32, i32, i32, vp],
-            "ppd_op_fill_random": [vp, u64, u64, i32, i32, vp],
-            "ppd_dev_set_profiling": [vp, i32],
-            "ppd_dev_get_stats": [vp, P(DevStats)],
-            "ppd_dev_reset_stats": [vp],
-        }
-        for name, args in sig.items():
-            f = getattr(L, name)
-            f.argtypes = args
-            f.restype = ctypes.c_int
-        _lib = L
+        _lib = load_lib()
     return _lib
 
 

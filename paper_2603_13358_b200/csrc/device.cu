@@ -50,6 +50,18 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kMaxRope = 1 << 17;  // positions covered by the RoPE table
+
+// process-wide tuning (ppd_set_tuning); each change bumps the epoch so devices
+// re-capture their step graphs with the newly selected kernels
+int g_tuning_epoch = 0;
+// gate|up GEMM with the SiLU epilogue (else fp32 partials + silu_mul_kernel).
+// Off by default: step-level A/B (tools/ab_step.py, 48 steps per arm) shows
+// no gain over the balanced-partition GEMM + silu_mul_kernel (within 1%).
+bool g_mlp_fused = false;
+// diagnostics only ("diag_skip" knob): skip kernel classes of the forward step
+// (1 small ops, 2 attention, 4 GEMMs) to time their marginal cost in the live
+// graph. Results are meaningless while set.
+int g_diag_skip = 0;
 constexpr int kAttnTargetCtas = 148 * 2 * 2;
 
 struct Layer {
@@ -78,6 +90,7 @@ struct ppd_dev {
   int gpu = 0;
   ppd_model_cfg cfg{};
   int max_T = 0, max_S = 0;
+  size_t ws_rows = 0;  // token rows of fp32 GEMM-output workspace (holds K-partial slices)
   cudaStream_t compute = nullptr, xfer = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, xev0 = nullptr, xev1 = nullptr, compute_done = nullptr;
   GemmContext* gemm = nullptr;
@@ -112,6 +125,7 @@ struct ppd_dev {
   std::map<std::tuple<int, int, int, int, int, int>, cudaGraphExec_t> graphs;
   std::map<std::tuple<int, int, int, int, int, int>, int> shape_seen;
   bool use_graphs = true;
+  int tuning_epoch = 0;  // ppd_set_tuning generation the cached graphs were captured under
   // instrumentation
   bool profiling = false;
   ppd_dev_stats stats{};
@@ -486,36 +500,44 @@ int forward(ppd_dev* d, const StepLayout& L) {
   const int* outrows = at<int>(m, L.off_outrows);
   const AttnItem* items = at<AttnItem>(m, L.off_items);
   const int T = L.T;
-  int np_down = 1;
+  // K-partial slices the fp32 workspaces hold for this step (Tp token rows of slices)
+  const int max_sl = std::max(1, std::min(8, (int)(d->ws_rows / (size_t)std::max(T, 1))));
+  GemmParts np_down;
 
   CU(launch_embed(tokens, d->embed, d->x, T, d_model, s));
   for (int l = 0; l < c.n_layers; ++l) {
-    int np_qkv = 1, np_o = 1, np_gu = 1;
+    GemmParts np_qkv, np_o;
     const Layer& w = d->layers[l];
     // x += down(prev) ; h = norm(x)
-    CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, np_down, nullptr, d->ones, d->h, T, d_model,
+    if (!(g_diag_skip & 1)) CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, np_down, nullptr, d->ones, d->h, T, d_model,
                           c.rms_eps, s));
     PROF(1, false);
-    CU(gemm_run_split(d->gemm, d->h, w.wqkv, d->qkv32, T, W, d_model, &np_qkv, s));
+    if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->h, w.wqkv, d->qkv32, T, W, d_model, max_sl, &np_qkv, s));
     PROF(1, true);
-    CU(launch_rope_kv_write(d->qkv32, np_qkv, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
+    if (!(g_diag_skip & 1)) CU(launch_rope_kv_write(d->qkv32, np_qkv, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
                             d->rope_sin, d->q, d->kv, T, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers,
                             l, d->bt, s));
     PROF(0, false);
-    int rc = run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items,
+    int rc = (g_diag_skip & 2) ? 0 : run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items,
                            at<int>(m, L.off_seg), L.n_cta, l, d->ws_o, d->ws_ml, d->counters, s);
     if (rc) return rc;
     PROF(0, true);
     PROF(1, false);
-    CU(gemm_run_split(d->gemm, d->attn, w.wo, d->proj32, T, d_model, qd, &np_o, s));
+    if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->attn, w.wo, d->proj32, T, d_model, qd, max_sl, &np_o, s));
     PROF(1, true);
-    CU(launch_add_rmsnorm(d->x, d->proj32, np_o, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
+    if (!(g_diag_skip & 1)) CU(launch_add_rmsnorm(d->x, d->proj32, np_o, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
     PROF(1, false);
-    CU(gemm_run_split(d->gemm, d->h, w.wgu, d->gu32, T, 2 * F, d_model, &np_gu, s));
-    PROF(1, true);
-    CU(launch_silu_mul(d->gu32, np_gu, d->m, T, F, s));
+    if (g_mlp_fused) {
+      if (!(g_diag_skip & 4)) CU(gemm_run_silu(d->gemm, d->h, w.wgu, d->m, d->gu32, T, 2 * F, d_model, s));
+      PROF(1, true);
+    } else {
+      GemmParts np_gu;
+      if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->h, w.wgu, d->gu32, T, 2 * F, d_model, max_sl, &np_gu, s));
+      PROF(1, true);
+      if (!(g_diag_skip & 1)) CU(launch_silu_mul(d->gu32, np_gu, d->m, T, F, s));
+    }
     PROF(1, false);
-    CU(gemm_run_split(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, &np_down, s));
+    if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, max_sl, &np_down, s));
     PROF(1, true);
   }
   count_launches(d, L);
@@ -538,6 +560,7 @@ int alloc_workspaces(ppd_dev* d) {
   CU(cudaMalloc(&d->hl, S * c.d_model * 2));
   // fp32 GEMM outputs also hold up to 8 K-split partial slices of a <=256-token step
   const size_t Tp = std::max<size_t>(T, 8 * 256);
+  d->ws_rows = Tp;
   CU(cudaMalloc(&d->qkv32, Tp * (qd + 2 * kd) * 4));
   CU(cudaMalloc(&d->proj32, Tp * c.d_model * 4));
   CU(cudaMalloc(&d->gu32, Tp * 2 * c.d_ff * 4));
@@ -741,6 +764,10 @@ int ppd_step_submit(ppd_dev* d, const ppd_batch* b) {
   // repeated shapes replay a captured graph (decode steps: ~300 launches -> 1)
   // every launch parameter of forward() is a function of these (grids: items, n_dec, n_cta)
   const auto key = std::make_tuple(L.n, L.T, L.maxb, L.n_out, L.n_items * 4096 + L.n_dec, L.n_ws * 8192 + L.n_cta);
+  if (d->tuning_epoch != g_tuning_epoch) {  // kernels chosen at capture time changed
+    clear_graphs(d);
+    d->tuning_epoch = g_tuning_epoch;
+  }
   const bool graph_ok = d->use_graphs && !d->profiling && d->shape_seen[key]++ > 0;
   if (graph_ok) {
     auto it = d->graphs.find(key);
@@ -976,6 +1003,58 @@ int ppd_op_gemm_tc(const void* A, const void* B, void* C, int32_t M, int32_t N, 
   CHECK_ARG(splits == 1 || out_f32, "K-split partials need fp32 output");
   CU(gemm_tc_run(static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0, splits,
                  (size_t)M * N, static_cast<cudaStream_t>(stream)));
+  return PPD_OK;
+}
+
+int ppd_op_gemm_silu(const void* A, const void* B, void* m, int32_t M, int32_t N, int32_t K, void* stream) {
+  CHECK_ARG(A && B && m && M > 0 && N > 0 && K > 0, "bad gemm args");
+  CHECK_ARG(K % 8 == 0 && N % 128 == 0, "K must be a multiple of 8 and N of 128");
+  CU(gemm_tc_run_silu(static_cast<const bf16*>(A), static_cast<const bf16*>(B), static_cast<bf16*>(m), M, N, K,
+                      static_cast<cudaStream_t>(stream)));
+  return PPD_OK;
+}
+
+int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
+                      int32_t max_slices, ppd_gemm_parts* parts, void* stream) {
+  CHECK_ARG(A && B && C && parts && M > 0 && N > 0 && K > 0 && max_slices >= 1, "bad gemm args");
+  CHECK_ARG(K % 8 == 0, "K must be a multiple of 8");
+  GemmParts g;
+  CU(gemm_tc_run_parts(static_cast<const bf16*>(A), static_cast<const bf16*>(B), static_cast<float*>(C), M, N, K,
+                       max_slices, (size_t)M * N, &g, static_cast<cudaStream_t>(stream)));
+  parts->n = g.n;
+  parts->kbt = g.kbt;
+  parts->slots = g.slots;
+  parts->rows = g.rows;
+  parts->bn = g.bn;
+  parts->n_tiles_t = g.n_tiles_t;
+  parts->total = g.total;
+  parts->stride = g.stride;
+  return PPD_OK;
+}
+
+int ppd_set_tuning(const char* name, int32_t value) {
+  static int pair = -1, stages = 0, sched = -1;
+  CHECK_ARG(name, "null tuning name");
+  if (std::strcmp(name, "gemm_pair") == 0) {
+    CHECK_ARG(value >= -1 && value <= 1, "gemm_pair must be -1, 0 or 1");
+    pair = value;
+  } else if (std::strcmp(name, "gemm_sched") == 0) {
+    CHECK_ARG(value >= -1 && value <= 1, "gemm_sched must be -1, 0 or 1");
+    sched = value;
+  } else if (std::strcmp(name, "gemm_stages") == 0) {
+    CHECK_ARG(value >= 0 && value <= 16, "gemm_stages must be in [0, 16]");
+    stages = value;
+  } else if (std::strcmp(name, "diag_skip") == 0) {
+    CHECK_ARG(value >= 0 && value <= 7, "diag_skip must be in [0, 7]");
+    g_diag_skip = value;
+  } else if (std::strcmp(name, "mlp_fused") == 0) {
+    CHECK_ARG(value == 0 || value == 1, "mlp_fused must be 0 or 1");
+    g_mlp_fused = value != 0;
+  } else {
+    return fail(PPD_ERR_INVALID, std::string("unknown tuning knob: ") + name);
+  }
+  gemm_tc_set_tuning(pair, stages, sched);
+  ++g_tuning_epoch;
   return PPD_OK;
 }
 

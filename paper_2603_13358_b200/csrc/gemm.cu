@@ -7,6 +7,7 @@
 
 #include "gemm.h"
 #include "gemm_tc.h"
+#include "kernels.h"
 
 namespace ppdk {
 
@@ -53,14 +54,24 @@ cudaError_t gemm_run(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16
 }
 
 cudaError_t gemm_run_split(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, float* C, int M, int N,
-                           int K, int* n_part, cudaStream_t s) {
+                           int K, int max_slices, GemmParts* parts, cudaStream_t s) {
   if (!c->tc) {
-    *n_part = 1;
+    *parts = GemmParts{};
+    parts->stride = (size_t)M * N;
     return gemm_run_cublas(c, A, B, C, M, N, K, true, s);
   }
-  const int splits = gemm_tc_plan_splits(M, N, K);
-  *n_part = splits;
-  return gemm_tc_run(A, B, C, M, N, K, true, splits, (size_t)M * N, s);
+  return gemm_tc_run_parts(A, B, C, M, N, K, max_slices, (size_t)M * N, parts, s);
+}
+
+cudaError_t gemm_run_silu(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, __nv_bfloat16* m,
+                          float* scratch, int M, int N, int K, cudaStream_t s) {
+  if (M == 0) return cudaSuccess;
+  if (c->tc) return gemm_tc_run_silu(A, B, m, M, N, K, s);
+  cudaError_t e = gemm_run_cublas(c, A, B, scratch, M, N, K, true, s);
+  if (e != cudaSuccess) return e;
+  GemmParts one;
+  one.stride = (size_t)M * N;
+  return launch_silu_mul(scratch, one, m, M, N / 2, s);
 }
 
 }  // namespace ppdk

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include "gemm_tc.h"
+
 namespace ppdk {
 struct GemmContext;
 GemmContext* gemm_create();
@@ -14,10 +16,16 @@ bool gemm_uses_tcgen05(const GemmContext* ctx);
 // single-slice product (no K split)
 cudaError_t gemm_run(GemmContext* ctx, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N,
                      int K, bool out_f32, cudaStream_t s);
-// fp32 product written as *n_part K-split partial slices of M*N floats each
-// (the consumer sums them); the split count fills the SMs for small M.
+// fp32 product written as K-partial slices of M*N floats each (at most
+// max_slices; *parts says which slices are valid where, the consumer sums
+// them); the planner picks the split / balanced partition that fills the SMs.
 cudaError_t gemm_run_split(GemmContext* ctx, const __nv_bfloat16* A, const __nv_bfloat16* B, float* C, int M, int N,
-                           int K, int* n_part, cudaStream_t s);
+                           int K, int max_slices, GemmParts* parts, cudaStream_t s);
+// MLP up-projection with SiLU fused: m[M][N/2] = rbf(silu(gate) * up) for the
+// interleaved gate|up weight B [N][K]. The cuBLAS path computes the fp32
+// product into `scratch` ([M][N] floats) and runs silu_mul_kernel.
+cudaError_t gemm_run_silu(GemmContext* ctx, const __nv_bfloat16* A, const __nv_bfloat16* B, __nv_bfloat16* m,
+                          float* scratch, int M, int N, int K, cudaStream_t s);
 cudaError_t gemm_run_cublas(GemmContext* ctx, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M,
                             int N, int K, bool out_f32, cudaStream_t s);
 }  // namespace ppdk

@@ -38,6 +38,9 @@ constexpr int kThreads = 256;
 constexpr int kWBytes = kBM * kBK * 2;        // 16 KB
 constexpr int kSmemBudget = 220 * 1024;
 constexpr int kMaxStages = 8;
+constexpr int kBarBytes = 256;                // mbarriers + TMEM slot after the stage ring
+constexpr int kXchgBytes = 2 * 2 * 32 * 32 * 4;  // fused epilogue: 2 buffers x 2 warps x 32x32 fp32
+constexpr int kEpiPlain = 0, kEpiSilu = 1;
 
 PPD_DEV void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
@@ -86,34 +89,158 @@ PPD_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ---- CTA-pair (cta_group::2) primitives ------------------------------------
+PPD_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cta address in this CTA -> shared::cluster address of the same offset in CTA `rank`
+PPD_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+PPD_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's smem, completion bytes counted on the leader CTA's mbarrier
+PPD_DEV void tma_load_2d_pair(void* smem, const CUtensorMap* map, int x, int y, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster)
+      : "memory");
+}
+PPD_DEV void mma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+// arrive (once the issued MMAs retire) on the barrier at this offset in both CTAs of the pair
+PPD_DEV void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+PPD_DEV void mbar_arrive_remote(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+PPD_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
 }  // namespace
 
-// Persistent: grid = min(units, 148); CTA c processes units c, c + grid, ...
-// where a unit is (weight tile, token tile, K split), weight-tile-major so the
-// CTAs running concurrently share weight tiles and token tiles through L2. The
-// producer streams stages across unit boundaries without draining; the MMA
-// warp alternates between two TMEM accumulators (when 2*BN <= 512 columns) so
-// the epilogue of unit i overlaps the MMAs of unit i+1.
+// ---- work schedule shared by the producer, MMA and epilogue roles ----------
+// A segment is a contiguous k-block range [kb0, kb1) of one (weight tile,
+// token tile) whose accumulator goes to partial slice `slice`.
+//  * uniform: units (tile, split) dealt round-robin to the slots;
+//  * balanced: slot c owns items [c*total/slots, (c+1)*total/slots) of the
+//    flattened (tile, k-block) space (GemmParts documents the slice rule).
+struct Seg {
+  int tw, tt, kb0, kb1, slice;
+};
+struct Sched {
+  int n_tiles_t, kbt, kb_per, splits, n_units, slots, c, u;
+  int balanced;
+  long long total, x, end;
+
+  PPD_DEV void begin(const GemmTcParams& p, int rows, int c_, int slots_) {
+    n_tiles_t = (p.T + p.bn - 1) / p.bn;
+    kbt = (p.K + kBK - 1) / kBK;
+    splits = p.splits;
+    kb_per = (kbt + splits - 1) / splits;
+    n_units = ((p.N + rows - 1) / rows) * n_tiles_t * splits;
+    slots = slots_;
+    c = c_;
+    u = c_;
+    balanced = p.balanced;
+    total = p.total;
+    x = end = 0;
+    if (balanced) {
+      x = (long long)c_ * total / slots_;
+      end = (long long)(c_ + 1) * total / slots_;
+    }
+  }
+  PPD_DEV int owner(long long item) const { return (int)(((item + 1) * slots + total - 1) / total) - 1; }
+  PPD_DEV bool next(Seg& s) {
+    if (!balanced) {
+      if (u >= n_units) return false;
+      s.slice = u % splits;
+      const int rest = u / splits;
+      s.tt = rest % n_tiles_t;
+      s.tw = rest / n_tiles_t;
+      s.kb0 = s.slice * kb_per;
+      s.kb1 = min(kbt, s.kb0 + kb_per);
+      u += slots;
+      return true;
+    }
+    if (x >= end) return false;
+    const long long t = x / kbt;
+    s.kb0 = (int)(x - t * kbt);
+    s.kb1 = (int)min((long long)kbt, s.kb0 + (end - x));
+    s.tt = (int)(t % n_tiles_t);
+    s.tw = (int)(t / n_tiles_t);
+    s.slice = c - owner(t * kbt);
+    x += s.kb1 - s.kb0;
+    return true;
+  }
+};
+
+// Persistent GEMM. kPair = false: one CTA per slot, 128-row weight tiles,
+// tcgen05 cta_group::1. kPair = true: a cluster of 2 CTAs on one TPC per slot,
+// 256-row weight tiles, UMMA M=256 with cta_group::2: CTA r streams weight rows
+// [128r, 128r+128) of the tile and HALF of the token tile (bn/2 rows), and
+// the leader's single-thread MMA reads both CTAs' shared memory.
+//
+// One TMA ring of stages (16 KB of weights + the k-block's activation tile,
+// one mbarrier transaction). Weights do not depend on the previous kernel:
+// the producer streams the first ring's worth of weight tiles before
+// griddepcontrol.wait (PDL), then the activations. (Measured: splitting the
+// activations into their own shallow ring with a second producer warp is
+// 20-30% slower at T=200 — tools/ab_libs.py.)
+//
+// The MMA warp alternates between two TMEM accumulators (when 2*BN <= 512
+// columns) so the epilogue of segment i overlaps the MMAs of segment i+1.
+// Pair protocol: both CTAs' TMAs complete on the LEADER's full barrier (the
+// leader alone arms it with both CTAs' bytes); the leader's commits multicast
+// to the smem-slot and accumulator barriers of both CTAs; both epilogues
+// release an accumulator on the leader's barrier (8 warp arrivals).
+template <bool kPair, int kEpi>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                    GemmTcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kCta = kPair ? 2 : 1;
   const int S = p.stages;
-  const int x_bytes = p.bn * kBK * 2;
-  const int stage_bytes = kWBytes + x_bytes;  // both multiples of 1 KB
+  const int xrows = p.bn / kCta;  // token rows this CTA loads per stage
+  const int stage_bytes = kWBytes + xrows * kBK * 2;  // both multiples of 1 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
-  uint64_t* acc_full = empty + S;   // [2]
-  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint64_t* acc_full = empty + S;      // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2] (pair: used in the leader only)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* xchg = reinterpret_cast<float*>(smem + S * stage_bytes + kBarBytes);  // fused-epilogue exchange
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_tiles_w = (p.N + kBM - 1) / kBM;
-  const int n_tiles_t = (p.T + p.bn - 1) / p.bn;
-  const int n_units = n_tiles_w * n_tiles_t * p.splits;
-  const int kb_total = (p.K + kBK - 1) / kBK;
-  const int kb_per = (kb_total + p.splits - 1) / p.splits;
+  const uint32_t rank = kPair ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int slot = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_slots = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int n_acc = p.tmem_cols >= 2 * p.bn_cols ? 2 : 1;
 
   if (threadIdx.x == 0) {
@@ -123,77 +250,97 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 4);  // one arrive per epilogue warp
+      mbar_init(&acc_empty[i], 4 * kCta);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_barrier_init();
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(p.tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(p.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(p.tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync_all();  // peer barriers initialised + TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_trigger();  // the next kernel may launch; it waits for our completion itself
 
-  // unit -> (weight tile, token tile, split); token tile fastest
-  auto decode_unit = [&](int u, int& tw, int& tt, int& sp) {
-    sp = u % p.splits;
-    const int rest = u / p.splits;
-    tt = rest % n_tiles_t;
-    tw = rest / n_tiles_t;
+  const int rows = kBM * kCta;
+  const uint32_t full_bar0 = kPair ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
+  const uint32_t acc_empty0 = kPair ? mapa_shared(smem_u32(acc_empty), 0) : smem_u32(acc_empty);
+  const int w_row0 = (int)rank * kBM;
+  const int x_row0 = (int)rank * xrows;
+  const uint32_t tx_bytes = (uint32_t)(kCta * stage_bytes);
+
+  auto load = [&](void* dst, const CUtensorMap* map, int x, int y, int s) {
+    if (kPair)
+      tma_load_2d_pair(dst, map, x, y, full_bar0 + 8u * s);
+    else
+      tma_load_2d(dst, map, x, y, &full[s]);
   };
 
   if (warp == 0) {
     if (lane == 0) {
-      // Weights do not depend on the previous kernel: stream the first stages of
-      // W before waiting on it (PDL), then the activations.
+      Sched sc;
+      sc.begin(p, rows, slot, n_slots);
+      Seg sg;
       int npre = 0;
-      if ((int)blockIdx.x < n_units) {
-        int tw, tt, sp;
-        decode_unit(blockIdx.x, tw, tt, sp);
-        const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
-        npre = min(S, max(0, kb1 - kb0));
-        for (int i = 0; i < npre; ++i) {
-          mbar_arrive_expect_tx(&full[i], stage_bytes);
-          tma_load_2d(smem + i * stage_bytes, &map_w, (kb0 + i) * kBK, tw * kBM, &full[i]);
+      {
+        Sched pre = sc;
+        while (npre < S && pre.next(sg)) {
+          for (int kb = sg.kb0; kb < sg.kb1 && npre < S; ++kb, ++npre) {
+            if (leader) mbar_arrive_expect_tx(&full[npre], tx_bytes);
+            load(smem + npre * stage_bytes, &map_w, kb * kBK, sg.tw * rows + w_row0, npre);
+          }
         }
       }
       pdl_wait();
-      int it = 0;  // global stage counter across units
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        int tw, tt, sp;
-        decode_unit(u, tw, tt, sp);
-        const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+      int it = 0;  // global stage counter across segments
+      while (sc.next(sg)) {
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
           const int s = it % S;
           uint8_t* sw = smem + s * stage_bytes;
           if (it >= npre) {
-            if (it >= S) mbar_wait(&empty[s], ((it / S) - 1) & 1);
-            mbar_arrive_expect_tx(&full[s], stage_bytes);
-            tma_load_2d(sw, &map_w, kb * kBK, tw * kBM, &full[s]);
+            if (it >= S) {
+              if (kPair)
+                mbar_wait_cluster(&empty[s], ((it / S) - 1) & 1);
+              else
+                mbar_wait(&empty[s], ((it / S) - 1) & 1);
+            }
+            if (leader) mbar_arrive_expect_tx(&full[s], tx_bytes);
+            load(sw, &map_w, kb * kBK, sg.tw * rows + w_row0, s);
           }
-          tma_load_2d(sw + kWBytes, &map_x, kb * kBK, tt * p.bn, &full[s]);
+          load(sw + kWBytes, &map_x, kb * kBK, sg.tt * p.bn + x_row0, s);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.bn >> 3) << 17) |
-                             ((uint32_t)(kBM >> 4) << 24);
+                             ((uint32_t)(rows >> 4) << 24);
+      Sched sc;
+      sc.begin(p, rows, slot, n_slots);
+      Seg sg;
       int it = 0, j = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
-        int tw, tt, sp;
-        decode_unit(u, tw, tt, sp);
-        const int kb0 = sp * kb_per, kb1 = min(kb_total, kb0 + kb_per);
+      for (; sc.next(sg); ++j) {
         const int acc = j % n_acc;
         const int use = j / n_acc;  // how many times this accumulator was used before
-        if (use > 0) mbar_wait(&acc_empty[acc], (use - 1) & 1);
+        if (use > 0) {
+          if (kPair)
+            mbar_wait_cluster(&acc_empty[acc], (use - 1) & 1);
+          else
+            mbar_wait(&acc_empty[acc], (use - 1) & 1);
+        }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn_cols);
-        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
           const int s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
@@ -201,30 +348,73 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t da = sw128_kmajor_desc(sa);
           const uint64_t db = sw128_kmajor_desc(sa + kWBytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)  // 32 B per UMMA_K step inside the swizzle atom
-            mma_bf16(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (kb != kb0) || (k != 0));
-          mma_commit(&empty[s]);  // smem slot free once these MMAs retire
+          for (int k = 0; k < kBK / 16; ++k) {  // 32 B per UMMA_K step inside the swizzle atom
+            const uint32_t accum = (kb != sg.kb0) || (k != 0);
+            if (kPair)
+              mma_bf16_pair(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, accum);
+            else
+              mma_bf16(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, accum);
+          }
+          if (kPair)
+            mma_commit_pair(&empty[s]);  // smem slot (in both CTAs) free once these MMAs retire
+          else
+            mma_commit(&empty[s]);
         }
-        mma_commit(&acc_full[acc]);
+        if (kPair)
+          mma_commit_pair(&acc_full[acc]);
+        else
+          mma_commit(&acc_full[acc]);
       }
     }
   } else if (warp >= 4) {
     pdl_wait();  // outputs are written only after the predecessor retired
     const int q = warp & 3;  // TMEM lane quarter owned by this warp
-    int j = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
-      int tw, tt, sp;
-      decode_unit(u, tw, tt, sp);
+    Sched sc;
+    sc.begin(p, rows, slot, n_slots);
+    Seg sg;
+    for (int j = 0; sc.next(sg); ++j) {
       const int acc = j % n_acc;
       const int use = j / n_acc;
-      const int row = tw * kBM + q * 32 + lane;
-      const int t0 = tt * p.bn;
+      const int row = sg.tw * rows + w_row0 + q * 32 + lane;
+      const int t0 = sg.tt * p.bn;
       mbar_wait(&acc_full[acc], use & 1);
       tc_fence_after();
-      float* out32 = reinterpret_cast<float*>(p.out) + (size_t)sp * p.split_stride;
+      float* out32 = reinterpret_cast<float*>(p.out) + (size_t)sg.slice * p.split_stride;
       __nv_bfloat16* out16 = reinterpret_cast<__nv_bfloat16*>(p.out);
       const uint32_t t_acc = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * p.bn_cols);
       const int ncols = min(p.bn, p.T - t0);
+      if (kEpi == kEpiSilu) {
+        // Fused SiLU(gate) * up. The 128-row slab of this CTA is one interleaved
+        // gate|up group (launch_fill_gate_up): TMEM lanes 0-63 = gate rows,
+        // 64-127 = the matching up rows. Warps 2-3 hand their up values to
+        // warps 0-1 through a double-buffered smem exchange; warps 0-1 write
+        // m[t][64*group + lane'] = rbf(silu(g) * u) (same fp32 formula as
+        // silu_mul_kernel, so the unfused path gives the same bits).
+        const int grp = (sg.tw * rows + w_row0) / kBM;
+        __nv_bfloat16* m = reinterpret_cast<__nv_bfloat16*>(p.out);
+        for (int c0 = 0, buf = 0; c0 < ncols; c0 += 32, buf ^= 1) {
+          uint32_t r[32];
+          tmem_ld32(t_acc + (uint32_t)c0, r);
+          float* xb = xchg + buf * 2048;
+          if (q >= 2) {
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) xb[(q - 2) * 1024 + jj * 32 + lane] = __uint_as_float(r[jj]);
+          }
+          named_barrier_sync(1, 128);
+          if (q < 2 && grp * kBM < p.N) {
+            const int nj = min(32, ncols - c0);
+            __nv_bfloat16* dst = m + (size_t)(t0 + c0) * p.ldo + grp * 64 + q * 32 + lane;
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              if (jj < nj) {
+                const float g = __uint_as_float(r[jj]);
+                const float u = xb[q * 1024 + jj * 32 + lane];
+                dst[(size_t)jj * p.ldo] = __float2bfloat16_rn(__fmul_rn(__fdividef(g, __fadd_rn(1.0f, __expf(-g))), u));
+              }
+            }
+          }
+        }
+      } else
       for (int c0 = 0; c0 < ncols; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(t_acc + (uint32_t)c0, r);
@@ -245,13 +435,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (lane == 0) {
+        if (kPair)
+          mbar_arrive_remote(acc_empty0 + 8u * acc);
+        else
+          mbar_arrive(&acc_empty[acc]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync_all();  // the leader's MMAs may read the peer's smem until here
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
+    if (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
   }
 }
 
@@ -311,70 +510,234 @@ bool get_map(CUtensorMap* out, const void* ptr, int rows, int K, int box_rows) {
 }
 
 }  // namespace
+// Tuning knobs (ppd_set_tuning): pair = -1 auto / 0 single-CTA / 1 CTA pair;
+// stages = cap on the smem ring depth (0 = as many as fit); sched = -1 auto /
+// 0 uniform K split / 1 balanced partition.
+static int g_pair_mode = -1;
+static int g_stage_cap = 0;
+static int g_sched = -1;
 
-int gemm_tc_plan_splits(int T, int N, int K) {
-  const int bn = T >= kMaxBN ? kMaxBN : ((T + 15) / 16) * 16;
-  const int tiles = ((N + kBM - 1) / kBM) * ((T + bn - 1) / bn);
-  const int kb = (K + kBK - 1) / kBK;
-  // Persistent CTAs take units round-robin, so the step costs
-  //   rounds(s) x (bytes of one unit) = ceil(tiles*s/148) x (W slab / s + fp32 partial write + read).
-  // Pick the split count minimising it (s <= 8, >= 4 K-blocks per split).
-  const double w_unit = double(kBM) * K * 2.0;
-  const double out_unit = double(bn) * kBM * 4.0 * 2.0;
-  int best = 1;
+
+
+// Auto policy for the CTA-pair kernel (measured, tools/gemm_tprobe.py): pairs
+// pay off only when the activation ingress matters (>= 48 token rows) AND each
+// slot streams several tiles (the pair's cluster launch/sync costs dominate
+// one-tile-per-CTA GEMMs such as QKV / o-proj / down-proj of a decode step).
+constexpr int kPairMinT = 48;
+constexpr double kPairMinTilesPerSm = 1.4;
+
+void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched) {
+  g_pair_mode = pair_mode;
+  g_stage_cap = stage_cap;
+  g_sched = sched;
+}
+
+namespace {
+
+struct Shape {
+  bool pair;
+  int bn, rows, stages, stage_bytes, smem, slots;  // slots = co-resident CTAs (single) or pairs
+};
+
+void set_smem_attrs() {
+  static bool done = false;
+  if (done) return;
+  const int bytes = 1024 + kSmemBudget + kBarBytes;
+  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiSilu>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiSilu>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  done = true;
+}
+
+int max_pair_slots(int smem) {
+  static std::mutex mu;
+  static std::unordered_map<int, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(smem);
+  if (it != cache.end()) return it->second;
+  set_smem_attrs();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * 74);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<true, kEpiPlain>, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache.emplace(smem, n);
+  return n;
+}
+
+Shape shape_for(int T, int N, int extra_smem = 0, bool force_single = false) {
+  Shape sh{};
+  sh.bn = T >= kMaxBN ? kMaxBN : ((T + 15) / 16) * 16;
+  const double tiles1 = double((N + kBM - 1) / kBM) * ((T + sh.bn - 1) / sh.bn);
+  const bool auto_pair = T >= kPairMinT && tiles1 >= kPairMinTilesPerSm * 148;
+  sh.pair = !force_single && (g_pair_mode == 1 || (g_pair_mode < 0 && auto_pair));
+  sh.rows = sh.pair ? 2 * kBM : kBM;
+  sh.stage_bytes = kWBytes + (sh.pair ? sh.bn / 2 : sh.bn) * kBK * 2;
+  int stages = (kSmemBudget - extra_smem) / sh.stage_bytes;
+  stages = stages > kMaxStages ? kMaxStages : stages;
+  if (g_stage_cap > 0 && g_stage_cap < stages) stages = g_stage_cap;
+  sh.stages = stages;
+  sh.smem = 1024 + stages * sh.stage_bytes + kBarBytes + extra_smem;
+  sh.slots = 148;
+  if (sh.pair) {
+    sh.slots = max_pair_slots(sh.smem);
+    if (sh.slots <= 0) return shape_for(T, N, extra_smem, true);  // no co-resident pair fits: single-CTA kernel
+  }
+  return sh;
+}
+
+struct Plan {
+  bool balanced;
+  int splits;       // uniform: K splits
+  int slots;        // CTAs (pairs) launched
+  int n_slices;     // partial slices written
+  long long total;  // balanced: tiles * kbt
+};
+
+// Persistent CTAs (pairs) each stream their share of the weights; a step
+// costs the busiest slot's bytes:
+//   uniform(s): ceil(tiles*s/slots) units x (W slab / s + partial tile out)
+//   balanced  : ceil(total/slots) k-blocks of W + (segments) partial tiles out
+// Slices are capped so the callers' workspaces (max_slices slices) hold them.
+Plan plan_for(const Shape& sh, int T, int N, int K, int max_slices) {
+  const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.bn - 1) / sh.bn);
+  const int kbt = (K + kBK - 1) / kBK;
+  const double w_kb = double(kBM) * kBK * 2.0;  // bytes of W one CTA streams per k-block
+  // a partial tile is written here and re-read from L2 by the consumer: count the write
+  const double out_tile = double(sh.bn) * kBM * 4.0;
+  Plan best{false, 1, 0, 1, 0};
   double best_cost = 1e300;
-  // the callers' fp32 workspaces hold 8 x 256 token rows of partial slices
-  for (int s = 1; s <= 8 && kb / s >= 4 && s * T <= 8 * 256; ++s) {
-    const int rounds = (tiles * s + 147) / 148;
-    const double cost = rounds * (w_unit / s + (s > 1 ? out_unit : out_unit * 0.5));
+  for (int s = 1; s <= max_slices && s <= 8 && kbt / s >= 4; ++s) {
+    const int units = tiles * s;
+    const int rounds = (units + sh.slots - 1) / sh.slots;
+    const double cost = rounds * (w_kb * ((kbt + s - 1) / s) + out_tile);
     if (cost < best_cost * 0.97) {  // prefer fewer partial slices unless clearly better
       best_cost = cost;
-      best = s;
+      best = Plan{false, s, units < sh.slots ? units : sh.slots, s, 0};
     }
+  }
+  if (g_sched != 0 && max_slices >= 2) {
+    const long long total = (long long)tiles * kbt;
+    const int slots = (int)(total < sh.slots ? total : sh.slots);
+    const long long share = (total + slots - 1) / slots;
+    // slices = most ranges touching one tile; segments = most tiles one range touches
+    GemmParts g;
+    g.kbt = kbt;
+    g.slots = slots;
+    g.total = total;
+    int n_slices = 1;
+    for (long long t = 0; t < tiles; ++t) {
+      const int v = g.owner(t * kbt + kbt - 1) - g.owner(t * kbt) + 1;
+      n_slices = v > n_slices ? v : n_slices;
+    }
+    const long long segs = (share + kbt - 1) / kbt + 1;
+    const double cost = w_kb * share + segs * out_tile;
+    const bool want = g_sched == 1 || cost < best_cost * 0.95;
+    if (want && n_slices <= max_slices) best = Plan{true, 1, slots, n_slices, total};
   }
   return best;
 }
 
-cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, int K, bool out_f32, int splits,
-                        size_t split_stride, cudaStream_t s) {
-  if (T <= 0) return cudaSuccess;
-  if (K % 8 != 0) return cudaErrorInvalidValue;  // TMA row stride must be 16 B aligned
-  const int bn = T >= kMaxBN ? kMaxBN : ((T + 15) / 16) * 16;
-  if (splits < 1) splits = 1;
-  if (splits > 1 && !out_f32) return cudaErrorInvalidValue;
+}  // namespace
+
+int gemm_tc_plan_splits(int T, int N, int K) {
+  const Shape sh = shape_for(T, N);
+  const int cap = 8 * 256 / (T > 0 ? T : 1);
+  const int saved = g_sched;
+  g_sched = 0;
+  const Plan pl = plan_for(sh, T, N, K, cap < 1 ? 1 : cap);
+  g_sched = saved;
+  return pl.splits;
+}
+
+namespace {
+
+cudaError_t launch(const Shape& sh, const Plan& pl, const bf16* X, const bf16* W, void* out, int T, int N, int K,
+                   bool out_f32, size_t split_stride, cudaStream_t s, int epi = kEpiPlain) {
+  if (sh.stages < 2) return cudaErrorInvalidValue;  // ring does not fit
   GemmTcParams p{};
   p.out = out;
   p.T = T;
   p.N = N;
   p.K = K;
-  p.ldo = N;
-  p.bn = bn;
+  p.ldo = epi == kEpiSilu ? N / 2 : N;
+  p.epi = epi;
+  p.bn = sh.bn;
   p.out_f32 = out_f32 ? 1 : 0;
-  p.splits = splits;
+  p.splits = pl.balanced ? 1 : pl.splits;
   p.split_stride = split_stride ? split_stride : (size_t)T * N;
-  // accumulator columns per unit (power of two >= bn); two accumulators when they fit
-  p.bn_cols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+  // accumulator columns per segment (power of two >= bn); two accumulators when they fit
+  p.bn_cols = sh.bn <= 32 ? 32 : sh.bn <= 64 ? 64 : sh.bn <= 128 ? 128 : 256;
   p.tmem_cols = 2 * p.bn_cols <= 512 ? 2 * p.bn_cols : p.bn_cols;
-  const int stage_bytes = kWBytes + bn * kBK * 2;
-  int stages = kSmemBudget / stage_bytes;
-  stages = stages > kMaxStages ? kMaxStages : stages;
-  static const int stage_cap = [] {
-    const char* e = std::getenv("PPD_GEMM_STAGES");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (stage_cap > 0 && stage_cap < stages) stages = stage_cap;
-  p.stages = stages;
-  const int smem = 1024 + stages * stage_bytes + 256;
+  p.stages = sh.stages;
+  p.balanced = pl.balanced ? 1 : 0;
+  p.slots = pl.slots;
+  p.total = pl.total;
   CUtensorMap mw, mx;
-  if (!get_map(&mw, W, N, K, kBM) || !get_map(&mx, X, T, K, bn)) return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 + kSmemBudget + 256);
-    attr = true;
-  }
-  const int units = ((N + kBM - 1) / kBM) * ((T + bn - 1) / bn) * splits;
-  const int grid = units < 148 ? units : 148;
-  return launch_pdl(gemm_tc_kernel, dim3(grid), dim3(kThreads), (size_t)smem, s, mw, mx, p);
+  if (!get_map(&mw, W, N, K, kBM) || !get_map(&mx, X, T, K, sh.pair ? sh.bn / 2 : sh.bn))
+    return cudaErrorInvalidValue;
+  set_smem_attrs();
+  if (sh.pair)
+    return launch_pdl_cluster(epi == kEpiSilu ? gemm_tc_kernel<true, kEpiSilu> : gemm_tc_kernel<true, kEpiPlain>,
+                              dim3(2 * pl.slots), dim3(kThreads), (size_t)sh.smem, 2, s, mw,
+                              mx, p);
+  return launch_pdl(epi == kEpiSilu ? gemm_tc_kernel<false, kEpiSilu> : gemm_tc_kernel<false, kEpiPlain>,
+                    dim3(pl.slots), dim3(kThreads), (size_t)sh.smem, s, mw, mx, p);
+}
+
+}  // namespace
+
+cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, int K, bool out_f32, int splits,
+                        size_t split_stride, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  if (K % 8 != 0) return cudaErrorInvalidValue;  // TMA row stride must be 16 B aligned
+  if (splits < 1) splits = 1;
+  if (splits > 1 && !out_f32) return cudaErrorInvalidValue;
+  const Shape sh = shape_for(T, N);
+  const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.bn - 1) / sh.bn);
+  const int units = tiles * splits;
+  const Plan pl{false, splits, units < sh.slots ? units : sh.slots, splits, 0};
+  return launch(sh, pl, X, W, out, T, N, K, out_f32, split_stride, s);
+}
+
+cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, int N, int K, int max_slices,
+                              size_t split_stride, GemmParts* parts, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  if (K % 8 != 0 || max_slices < 1) return cudaErrorInvalidValue;
+  const Shape sh = shape_for(T, N);
+  const Plan pl = plan_for(sh, T, N, K, max_slices);
+  GemmParts g;
+  g.n = pl.n_slices;
+  g.stride = split_stride ? split_stride : (size_t)T * N;
+  g.kbt = pl.balanced ? (K + kBK - 1) / kBK : 0;
+  g.slots = pl.slots;
+  g.rows = sh.rows;
+  g.bn = sh.bn;
+  g.n_tiles_t = (T + sh.bn - 1) / sh.bn;
+  g.total = pl.balanced ? pl.total : 1;
+  *parts = g;
+  return launch(sh, pl, X, W, out, T, N, K, true, g.stride, s);
+}
+
+cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N, int K, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  if (K % 8 != 0 || N % kBM != 0) return cudaErrorInvalidValue;  // whole gate|up groups per 128-row slab
+  const Shape sh = shape_for(T, N, kXchgBytes);
+  const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.bn - 1) / sh.bn);
+  const Plan pl{false, 1, tiles < sh.slots ? tiles : sh.slots, 1, 0};
+  return launch(sh, pl, X, W, m, T, N, K, false, 0, s, kEpiSilu);
 }
 
 }  // namespace ppdk

@@ -1,4 +1,5 @@
-// gemm_tc.h — tcgen05 GEMM launcher (gemm_tc.cu).
+// gemm_tc.h — tcgen05 GEMM launcher (gemm_tc.cu) and the description of how
+// its fp32 output is spread over K-partial slices (read by the consumers).
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -8,15 +9,59 @@ namespace ppdk {
 
 typedef __nv_bfloat16 bf16;
 
+// How a GEMM's fp32 output C[T][N] is stored as partial slices
+// out + j*stride, j < n; C = sum of the slices that are VALID for the element.
+//  * uniform split (kbt == 0): every slice is valid everywhere.
+//  * balanced (stream-K) partition: the flattened (tile, k-block) space of
+//    `total` = tiles*kbt items is cut into `slots` equal contiguous ranges, one
+//    per persistent CTA (pair); the j-th range touching a tile writes slice j,
+//    so a tile has (owner(last item) - owner(first item) + 1) valid slices.
+// Slices are summed in order j = 0, 1, ... (fixed order: deterministic).
+struct GemmParts {
+  int n = 1;            // slices
+  size_t stride = 0;    // floats between slices
+  int kbt = 0;          // k-blocks per tile (0 = uniform split)
+  int slots = 1;        // ranges (persistent CTAs / pairs)
+  int rows = 128;       // weight rows (output columns) per tile
+  int bn = 256;         // token rows per tile
+  int n_tiles_t = 1;    // token tiles
+  long long total = 1;  // tiles * kbt
+
+  __host__ __device__ __forceinline__ int owner(long long x) const {
+    return (int)(((x + 1) * slots + total - 1) / total) - 1;
+  }
+  // valid slices for output column `col` of token row `tok`
+  __host__ __device__ __forceinline__ int valid(int col, int tok) const {
+    if (kbt == 0) return n;
+    const long long t = (long long)(col / rows) * n_tiles_t + tok / bn;
+    return owner(t * kbt + kbt - 1) - owner(t * kbt) + 1;
+  }
+};
+
 struct GemmTcParams {
   void* out;
   int T, N, K, ldo, bn, bn_cols, out_f32, splits, stages, tmem_cols;
   size_t split_stride;  // floats between split partial slices
+  int balanced;         // 1: stream-K ranges (GemmParts), 0: units of uniform K splits
+  int slots;            // persistent CTAs (pairs) the schedule is cut for
+  long long total;      // tiles * k-blocks per tile (balanced)
+  int epi;              // 0: write C (fp32 slices / bf16); 1: fused SiLU(gate)*up -> bf16 [T][N/2]
 };
 
 // out[T][N] (+ split slices) = X[T][K] . W[N][K]^T ; splits > 1 needs out_f32
 cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, int K, bool out_f32, int splits,
                         size_t split_stride, cudaStream_t s);
+// fp32 output into partial slices chosen by the planner (uniform split or a
+// balanced partition), at most `max_slices` slices of split_stride floats.
+cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, int N, int K, int max_slices,
+                              size_t split_stride, GemmParts* parts, cudaStream_t s);
+// m[T][N/2] = rbf(silu(gate) * up) for the interleaved gate|up weight [N][K]
+// (64-row groups, launch_fill_gate_up): the MLP up-projection with SiLU fused
+// into the epilogue (no K split; no fp32 round trip through HBM).
+cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N, int K, cudaStream_t s);
+// pair_mode: -1 auto, 0 single-CTA kernel, 1 CTA-pair kernel; stage_cap 0 = no cap;
+// sched: -1 auto, 0 uniform K split, 1 balanced partition
+void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched);
 // K-split count that fills the 148 SMs for this shape (1 when the tile grid already does)
 int gemm_tc_plan_splits(int T, int N, int K);
 

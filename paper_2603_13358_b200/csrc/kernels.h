@@ -6,6 +6,8 @@
 
 #include <utility>
 
+#include "gemm_tc.h"
+
 namespace ppdk {
 
 typedef __nv_bfloat16 bf16;
@@ -64,21 +66,21 @@ cudaError_t launch_fill_const(bf16* dst, uint64_t n, float v, cudaStream_t s);
 
 cudaError_t launch_embed(const int* tokens, const bf16* embed, bf16* x, int T, int d, cudaStream_t s);
 // x = rbf(x + rbf(delta)) (if delta); h = rbf(rmsnorm(x) * w). delta may be fp32 split partials
-// (n_part slices of [T][d]) summed first, or bf16 when delta_bf16 != null.
-cudaError_t launch_add_rmsnorm(bf16* x, const float* delta_f32, int n_part, const bf16* delta_bf16,
+// (the valid slices of `parts`, summed in slice order first), or bf16 when delta_bf16 != null.
+cudaError_t launch_add_rmsnorm(bf16* x, const float* delta_f32, const GemmParts& parts, const bf16* delta_bf16,
                                const bf16* w, bf16* h, int T, int d, float eps, cudaStream_t s);
 // final: for each selected row r = rows[i]: v = x[r] (+ delta[r]); out[i] = rbf(rmsnorm(v) * w)
-cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, int n_part,
+cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, const GemmParts& parts,
                               const bf16* delta_bf16, const int* rows, int n_rows, const bf16* w,
                               bf16* out, int T, int d, float eps, cudaStream_t s);
 // qkv fp32 [T][qd+2kd] (+bias) -> q bf16 [T][Hq][Dh] roped; k roped, v -> paged pool
-cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias, const int* row_seq,
+cudaError_t launch_rope_kv_write(const float* qkv, const GemmParts& parts, const float* bias, const int* row_seq,
                                  const int* row_pos, const int* block_tables, int max_blocks,
                                  const float* rope_cos, const float* rope_sin, bf16* q_out,
                                  bf16* kv_pool, int T, int Hq, int Hkv, int Dh, int n_layers,
                                  int layer, int block_tokens, cudaStream_t s);
 // gate/up fp32 [T][2F] interleaved (see launch_fill_gate_up) -> m = rbf(silu(g) * u) [T][F]
-cudaError_t launch_silu_mul(const float* gu, int n_part, bf16* m, int T, int F, cudaStream_t s);
+cudaError_t launch_silu_mul(const float* gu, const GemmParts& parts, bf16* m, int T, int F, cudaStream_t s);
 cudaError_t launch_argmax(const float* logits, int n, int V, int* out, cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t s);
 
@@ -113,6 +115,26 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+// same, as clusters of `cluster_x` CTAs (grid.x must be a multiple)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, int cluster_x,
+                               cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster_x;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 }  // namespace ppdk

@@ -123,7 +123,7 @@ cudaError_t launch_embed(const int* tokens, const bf16* embed, bf16* x, int T, i
 // v = x (+ rbf(sum of delta partials) | + delta_bf16); x <- v ; out = rbf(rbf(v) * inv_rms) * w
 template <bool kWriteX>
 __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
-    bf16* x, const float* df, int n_part, size_t part_stride, const bf16* db, const bf16* w,
+    bf16* x, const float* df, GemmParts parts, const bf16* db, const bf16* w,
     bf16* out, const int* rows, int d, float eps) {
   __shared__ float red[33];
   pdl_wait();
@@ -142,9 +142,10 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
         const float* base = df + row * d + (size_t)c * 8;
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        const int n_part = parts.valid(c * 8, (int)row);
         for (int pp = 0; pp < n_part; ++pp) {
-          float4 a = reinterpret_cast<const float4*>(base + pp * part_stride)[0];
-          float4 b = reinterpret_cast<const float4*>(base + pp * part_stride)[1];
+          float4 a = reinterpret_cast<const float4*>(base + pp * parts.stride)[0];
+          float4 b = reinterpret_cast<const float4*>(base + pp * parts.stride)[1];
           acc[0] = __fadd_rn(acc[0], a.x); acc[1] = __fadd_rn(acc[1], a.y);
           acc[2] = __fadd_rn(acc[2], a.z); acc[3] = __fadd_rn(acc[3], a.w);
           acc[4] = __fadd_rn(acc[4], b.x); acc[5] = __fadd_rn(acc[5], b.y);
@@ -179,19 +180,19 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
   }
 }
 
-cudaError_t launch_add_rmsnorm(bf16* x, const float* delta_f32, int n_part, const bf16* delta_bf16,
+cudaError_t launch_add_rmsnorm(bf16* x, const float* delta_f32, const GemmParts& parts, const bf16* delta_bf16,
                                const bf16* w, bf16* h, int T, int d, float eps, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  return launch_pdl(add_rmsnorm_kernel<true>, dim3(T), dim3(kNormThreads), 0, s, x, delta_f32, n_part,
-                    (size_t)T * d, delta_bf16, w, h, (const int*)nullptr, d, eps);
+  return launch_pdl(add_rmsnorm_kernel<true>, dim3(T), dim3(kNormThreads), 0, s, x, delta_f32, parts, delta_bf16,
+                    w, h, (const int*)nullptr, d, eps);
 }
 
-cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, int n_part,
+cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, const GemmParts& parts,
                               const bf16* delta_bf16, const int* rows, int n_rows, const bf16* w,
                               bf16* out, int T, int d, float eps, cudaStream_t s) {
   if (n_rows == 0) return cudaSuccess;
   return launch_pdl(add_rmsnorm_kernel<false>, dim3(n_rows), dim3(kNormThreads), 0, s, const_cast<bf16*>(x),
-                    delta_f32, n_part, (size_t)T * d, delta_bf16, w, out, rows, d, eps);
+                    delta_f32, parts, delta_bf16, w, out, rows, d, eps);
 }
 
 // ------------------------------------------------------- RoPE + KV write
@@ -199,10 +200,11 @@ cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, int n_part,
 // i+64..i+67) of one q/k head, or 4 consecutive dims of one v head, and reads
 // the fp32 GEMM output (all K-split partial slices) with 16-byte loads.
 template <bool kRound = true>
-PPD_DEV float4 ld_sum4(const float* base, int n_part, size_t part_stride, const float* bias, int col) {
+PPD_DEV float4 ld_sum4(const float* base, const GemmParts& parts, int tok, const float* bias, int col) {
   float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int n_part = parts.valid(col, tok);
   for (int pp = 0; pp < n_part; ++pp) {
-    const float4 v = *reinterpret_cast<const float4*>(base + pp * part_stride + col);
+    const float4 v = *reinterpret_cast<const float4*>(base + pp * parts.stride + col);
     a.x = __fadd_rn(a.x, v.x);
     a.y = __fadd_rn(a.y, v.y);
     a.z = __fadd_rn(a.z, v.z);
@@ -223,7 +225,7 @@ PPD_DEV void st_bf16x4(bf16* dst, float a, float b, float c, float d) {
   *reinterpret_cast<uint2*>(dst) = make_uint2(pack2(a, b), pack2(c, d));
 }
 
-__global__ void rope_kv_kernel(const float* qkv, int n_part, size_t part_stride, const float* bias,
+__global__ void rope_kv_kernel(const float* qkv, GemmParts parts, const float* bias,
                                const int* row_seq, const int* row_pos, const int* block_tables,
                                int max_blocks, const float* rope_cos, const float* rope_sin,
                                bf16* q_out, bf16* kv, int Hq, int Hkv, int Dh, int n_layers,
@@ -246,8 +248,8 @@ __global__ void rope_kv_kernel(const float* qkv, int n_part, size_t part_stride,
     if (u < n_rot) {
       const int head = u / per_head, i = (u % per_head) * 4;
       const int col = head * Dh + i;  // k heads follow q heads in the fused layout
-      const float4 x1 = ld_sum4(row, n_part, part_stride, bias, col);
-      const float4 x2 = ld_sum4(row, n_part, part_stride, bias, col + half);
+      const float4 x1 = ld_sum4(row, parts, r, bias, col);
+      const float4 x2 = ld_sum4(row, parts, r, bias, col + half);
       const float4 c = *reinterpret_cast<const float4*>(cs + i);
       const float4 sv = *reinterpret_cast<const float4*>(sn + i);
       const float a0 = rbf(__fsub_rn(__fmul_rn(x1.x, c.x), __fmul_rn(x2.x, sv.x)));
@@ -269,14 +271,14 @@ __global__ void rope_kv_kernel(const float* qkv, int n_part, size_t part_stride,
     } else {
       const int v = (u - n_rot) * 4;
       const int hk = v / Dh, dd = v % Dh;
-      const float4 x = ld_sum4(row, n_part, part_stride, bias, qd + kd + v);
+      const float4 x = ld_sum4(row, parts, r, bias, qd + kd + v);
       bf16* dst = kv + ((((size_t)blk * n_layers + layer) * 2 + 1) * Hkv + hk) * BT * Dh + (size_t)tok * Dh + dd;
       st_bf16x4(dst, x.x, x.y, x.z, x.w);
     }
   }
 }
 
-cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias, const int* row_seq,
+cudaError_t launch_rope_kv_write(const float* qkv, const GemmParts& parts, const float* bias, const int* row_seq,
                                  const int* row_pos, const int* block_tables, int max_blocks,
                                  const float* rope_cos, const float* rope_sin, bf16* q_out,
                                  bf16* kv_pool, int T, int Hq, int Hkv, int Dh, int n_layers,
@@ -284,7 +286,7 @@ cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias
   if (T == 0) return cudaSuccess;
   const size_t W = (size_t)(Hq + 2 * Hkv) * Dh;
   // (row, quarter of the row's rotary/v units): 4 CTAs per token row for memory parallelism
-  return launch_pdl(rope_kv_kernel, dim3(T, 4), dim3(128), 0, s, qkv, n_part, (size_t)T * W, bias, row_seq, row_pos,
+  return launch_pdl(rope_kv_kernel, dim3(T, 4), dim3(128), 0, s, qkv, parts, bias, row_seq, row_pos,
                     block_tables, max_blocks, rope_cos, rope_sin, q_out, kv_pool, Hq, Hkv, Dh, n_layers, layer,
                     block_tokens);
 }
@@ -292,15 +294,15 @@ cudaError_t launch_rope_kv_write(const float* qkv, int n_part, const float* bias
 // ------------------------------------------------------------- SiLU * up
 // gate/up come interleaved in 64-column groups (launch_fill_gate_up layout);
 // each thread produces 4 outputs from one float4 of gate and one of up.
-__global__ void silu_mul_kernel(const float* gu, int n_part, size_t part_stride, bf16* m, int F) {
+__global__ void silu_mul_kernel(const float* gu, GemmParts parts, bf16* m, int F) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.y;
   const float* row = gu + (size_t)r * 2 * F;
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4) {
     const int grp = j >> 6, within = j & 63;
-    const float4 g = ld_sum4<false>(row, n_part, part_stride, nullptr, grp * 128 + within);
-    const float4 u = ld_sum4<false>(row, n_part, part_stride, nullptr, grp * 128 + 64 + within);
+    const float4 g = ld_sum4<false>(row, parts, r, nullptr, grp * 128 + within);
+    const float4 u = ld_sum4<false>(row, parts, r, nullptr, grp * 128 + 64 + within);
     const float gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
     float o[4];
 #pragma unroll
@@ -309,10 +311,10 @@ __global__ void silu_mul_kernel(const float* gu, int n_part, size_t part_stride,
     st_bf16x4(m + (size_t)r * F + j, o[0], o[1], o[2], o[3]);
   }
 }
-cudaError_t launch_silu_mul(const float* gu, int n_part, bf16* m, int T, int F, cudaStream_t s) {
+cudaError_t launch_silu_mul(const float* gu, const GemmParts& parts, bf16* m, int T, int F, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   dim3 grid((F / 4 + 255) / 256, T);
-  return launch_pdl(silu_mul_kernel, grid, dim3(256), 0, s, gu, n_part, (size_t)T * 2 * F, m, F);
+  return launch_pdl(silu_mul_kernel, grid, dim3(256), 0, s, gu, parts, m, F);
 }
 
 // ---------------------------------------------------------------- argmax

@@ -65,6 +65,24 @@ def test_prefill_decode_append_parity(pair):
         ctx += 1
 
 
+@pytest.mark.parametrize("knobs", [
+    {"gemm_pair": 1, "gemm_sched": 1, "mlp_fused": 1},   # CTA-pair GEMM, balanced partition, fused SiLU
+    {"gemm_pair": 0, "gemm_sched": 1, "mlp_fused": 0},   # single-CTA, balanced partition + silu_mul
+    {"gemm_pair": 1, "gemm_sched": 0, "mlp_fused": 0},   # CTA-pair, uniform K split
+], ids=["pair-balanced-fused", "single-balanced", "pair-uniform"])
+def test_step_parity_under_gemm_variants(pair, knobs):
+    """Every GEMM schedule / epilogue variant the tuning knobs select keeps the
+    forward step at oracle parity (graphs are re-captured on each change)."""
+    L = ppd.lib()
+    try:
+        for k, v in knobs.items():
+            ppd.check(L.ppd_set_tuning(k.encode(), v))
+        test_prefill_decode_append_parity(pair)
+    finally:
+        for k, v in (("gemm_pair", -1), ("gemm_sched", -1), ("mlp_fused", 0)):
+            ppd.check(L.ppd_set_tuning(k.encode(), v))
+
+
 def test_kv_pool_contents_match_oracle(pair):
     cfg, dev, model, pool = pair
     import torch
