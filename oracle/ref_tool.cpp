@@ -10,8 +10,18 @@
 //                                                        (costmodel.cpp:318-379)
 //   op=decide        a sequence of routing::decide calls  (routing.cpp:340-387)
 //   op=aggregate     metrics::aggregate over given records (metrics.cpp:79-107)
+//   op=sweep         sweep::run_sweep + results_csv, mean_over_seeds,
+//                    winner_inputs/winner_distribution, compare_modes (sweep.cpp)
+//   op=pareto        metrics::pareto_frontier                (metrics.cpp:109-132)
+//   op=winner        metrics::winner_distribution + render   (metrics.cpp:134-225)
+//   op=weight_sweep  sweep::weight_sweep                     (sweep.cpp:456-547)
+//   op=plan_default  SweepPlan::full_default + to_json/hash  (sweep.cpp:44-166)
+//   op=ingest_trace  workload::ingest_trace                  (workload.cpp:121-194)
 // One JSON object on stdin, one JSON object on stdout.
 #include <chrono>
+#include <cmath>
+#include <filesystem>
+#include <optional>
 #include <iostream>
 #include <iterator>
 #include <memory>
@@ -25,6 +35,7 @@
 #include "ppd/metrics.hpp"
 #include "ppd/routing.hpp"
 #include "ppd/simulator.hpp"
+#include "ppd/sweep.hpp"
 #include "ppd/workload.hpp"
 
 using nlohmann::json;
@@ -212,6 +223,128 @@ json op_decide(const json& job) {
   return {{"decisions", out}};
 }
 
+json cell_json(const sweep::CellResult& c) { return json::parse(c.to_json()); }
+
+json winner_json(const metrics::WinnerDistribution& d) {
+  json rows = json::array();
+  for (const auto& [cat, w] : d.rows) rows.push_back({cat, w.ttft_pct, w.tpot_pct, w.throughput_pct, w.avg});
+  return {{"render", d.render()}, {"rows", rows}, {"cells", d.cells}, {"all_degraded_cells", d.all_degraded_cells},
+          {"disagreement_fraction", d.disagreement_fraction}};
+}
+
+json nan_null(double v) { return std::isnan(v) ? json(nullptr) : json(v); }
+
+metrics::AggregateMetrics agg_from_manifest(const json& j) {
+  return sweep::CellResult::from_json(json{{"config_label", ""}, {"shape", ""}, {"x_mode", ""}, {"category", ""},
+                                           {"workload_id", ""}, {"qps", 0.0}, {"seed", 0}, {"failed", false},
+                                           {"metrics", j}}
+                                          .dump())
+      .m;
+}
+
+json op_sweep(const json& job) {
+  auto plan = sweep::SweepPlan::from_json(job.at("plan").dump());
+  auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
+  std::shared_ptr<const routing::DecisionTable> table;
+  if (job.contains("table_json"))
+    table = std::make_shared<routing::DecisionTable>(
+        routing::DecisionTable::from_json(job["table_json"].get<std::string>()));
+  std::optional<std::filesystem::path> manifest;
+  if (job.contains("manifest_dir")) manifest = job["manifest_dir"].get<std::string>();
+  auto rs = sweep::run_sweep(plan, calib, job.value("parallelism", 1), manifest, table);
+  json cells = json::array();
+  for (const auto& c : rs.cells) cells.push_back(cell_json(c));
+  json means = json::array();
+  for (const auto& [key, m] : sweep::mean_over_seeds(rs)) {
+    sweep::CellResult holder;
+    holder.m = m;
+    means.push_back({std::get<0>(key), std::get<1>(key), std::get<2>(key), cell_json(holder)["metrics"]});
+  }
+  json out{{"plan_hash", rs.plan_hash}, {"calibration_hash", rs.calibration_hash}, {"cells", cells},
+           {"csv", sweep::results_csv(rs)}, {"means", means}};
+  try {
+    out["winner"] = winner_json(metrics::winner_distribution(sweep::winner_inputs(rs)));
+  } catch (const std::invalid_argument& e) {
+    out["winner"] = {{"error", e.what()}};
+  }
+  json cmp = json::object();
+  for (const auto& c : job.value("compare", json::array())) {
+    json rows = json::array();
+    for (const auto& r : sweep::compare_modes(rs, c[0].get<std::string>(), c[1].get<std::string>(),
+                                              c[2].get<std::string>()))
+      rows.push_back({r.shape, nan_null(r.low), nan_null(r.med), nan_null(r.high), r.low_n, r.med_n, r.high_n});
+    cmp[c[0].get<std::string>() + "|" + c[1].get<std::string>() + "|" + c[2].get<std::string>()] = rows;
+  }
+  out["compare"] = cmp;
+  return out;
+}
+
+json op_pareto(const json& job) {
+  std::vector<metrics::ParetoPoint> pts;
+  for (const auto& p : job.at("points")) pts.push_back({p[0].get<double>(), p[1].get<double>(), p[2].get<std::string>()});
+  json f = json::array();
+  for (const auto& p : metrics::pareto_frontier(pts)) f.push_back({p.ttft_p99, p.tps, p.label});
+  return {{"frontier", f}};
+}
+
+json op_winner(const json& job) {
+  std::vector<metrics::WinnerCell> cells;
+  for (const auto& c : job.at("cells")) {
+    metrics::WinnerCell w;
+    w.workload_id = c.at("workload_id").get<std::string>();
+    w.qps = c.at("qps").get<double>();
+    w.config_label = c.at("config_label").get<std::string>();
+    w.category = c.at("category").get<std::string>();
+    w.m = agg_from_manifest(c.at("metrics"));
+    cells.push_back(w);
+  }
+  return winner_json(metrics::winner_distribution(cells));
+}
+
+json op_weight_sweep(const json& job) {
+  auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
+  auto tmp = sweep::SweepPlan::from_json(json{{"configs", json::array()}, {"workloads", json::array({job.at("base")})},
+                                              {"qps_levels", json::array()}, {"seeds", json::array()},
+                                              {"duration_s", 0.0}}
+                                             .dump());
+  std::vector<routing::GridSpec> grid = routing::default_grid();
+  if (job.contains("grid_keys")) {
+    std::vector<routing::GridSpec> sub;
+    for (const auto& k : job["grid_keys"])
+      for (const auto& g : grid)
+        if (g.key.str() == k.get<std::string>()) sub.push_back(g);
+    grid = sub;
+  }
+  json rows = json::array();
+  for (const auto& r : sweep::weight_sweep(job.at("shape").get<std::string>(), tmp.workloads.at(0),
+                                           job.at("qps_levels").get<std::vector<double>>(),
+                                           job.at("w_tpot_list").get<std::vector<double>>(), calib, grid,
+                                           job.at("seeds").get<std::vector<std::uint64_t>>()))
+    rows.push_back({r.w_tpot, nan_null(r.ttft_change), nan_null(r.tpot_change), r.d_local_ratio});
+  return {{"rows", rows}};
+}
+
+json op_plan_default() {
+  auto p = sweep::SweepPlan::full_default();
+  return {{"plan_json", p.to_json()}, {"hash", p.hash()}, {"cell_count", p.cell_count()}};
+}
+
+json op_ingest_trace(const json& job) {
+  std::istringstream in(job.at("trace_jsonl").get<std::string>());
+  workload::TraceFilter f;
+  f.min_turns = job.value("min_turns", 2);
+  f.min_turn2_input_output_ratio = job.value("min_ratio", 0.0);
+  if (job.contains("sample_size")) f.sample_size = job["sample_size"].get<std::size_t>();
+  f.sample_seed = job.value("sample_seed", 0ull);
+  json convs = json::array();
+  for (const auto& c : workload::ingest_trace(in, f)) {
+    json turns = json::array();
+    for (const auto& t : c.turns) turns.push_back({t.new_input_tokens, t.target_output_tokens, t.cached_context_tokens});
+    convs.push_back({{"conv_id", c.conv_id}, {"turns", turns}});
+  }
+  return {{"conversations", convs}};
+}
+
 }  // namespace
 
 int main() {
@@ -227,6 +360,12 @@ int main() {
       out = {{"json", c.to_json()}, {"hash", c.hash()}};
     } else if (op == "costs") out = op_costs(job);
     else if (op == "decide") out = op_decide(job);
+    else if (op == "sweep") out = op_sweep(job);
+    else if (op == "pareto") out = op_pareto(job);
+    else if (op == "winner") out = op_winner(job);
+    else if (op == "weight_sweep") out = op_weight_sweep(job);
+    else if (op == "plan_default") out = op_plan_default();
+    else if (op == "ingest_trace") out = op_ingest_trace(job);
     else throw std::invalid_argument("unknown op " + op);
     std::cout << out.dump() << "\n";
     return 0;

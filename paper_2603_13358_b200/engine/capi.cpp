@@ -1,5 +1,8 @@
 // capi.cpp — JSON front door of the engine (include/ppd_engine.h).
 #include <chrono>
+#include <cmath>
+#include <filesystem>
+#include <optional>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -14,6 +17,7 @@
 #include "ppd/metrics.hpp"
 #include "ppd/routing.hpp"
 #include "ppd/simulator.hpp"
+#include "ppd/sweep.hpp"
 #include "ppd/workload.hpp"
 
 using nlohmann::json;
@@ -176,11 +180,153 @@ std::string build_table(const json& job) {
   return json{{"table_json", t.to_json()}, {"calib_hash", calib->hash()}}.dump();
 }
 
+// ---- §8f-2 / §8f-4: sweep harness, analyses, trace ingest -----------------
+json cell_json(const sweep::CellResult& c) { return json::parse(c.to_json()); }
+
+metrics::AggregateMetrics agg_from(const json& j) {
+  // the manifest format (reference fields); missing optionals stay empty
+  sweep::CellResult c = sweep::CellResult::from_json(
+      json{{"config_label", ""}, {"shape", ""}, {"x_mode", ""}, {"category", ""}, {"workload_id", ""},
+           {"qps", 0.0}, {"seed", 0}, {"failed", false}, {"metrics", j}}
+          .dump());
+  return c.m;
+}
+
+json winner_json(const metrics::WinnerDistribution& d) {
+  json rows = json::array();
+  for (const auto& [cat, w] : d.rows) rows.push_back({cat, w.ttft_pct, w.tpot_pct, w.throughput_pct, w.avg});
+  return {{"render", d.render()}, {"rows", rows}, {"cells", d.cells}, {"all_degraded_cells", d.all_degraded_cells},
+          {"disagreement_fraction", d.disagreement_fraction}};
+}
+
+json nan_null(double v) { return std::isnan(v) ? json(nullptr) : json(v); }
+
+// op=sweep: run a SweepPlan (reference plan JSON) on the virtual clock or, with
+// "clock": "device", every cell on the GPUs; returns cells, CSV, seed means,
+// the winner distribution and the requested mode comparisons.
+std::string op_sweep(const json& job) {
+  const sweep::SweepPlan plan = sweep::SweepPlan::from_json(job.at("plan").dump());
+  auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
+  std::shared_ptr<const routing::DecisionTable> table;
+  if (job.contains("table_json"))
+    table = std::make_shared<routing::DecisionTable>(
+        routing::DecisionTable::from_json(job["table_json"].get<std::string>()));
+  std::optional<std::filesystem::path> manifest;
+  if (job.contains("manifest_dir")) manifest = job["manifest_dir"].get<std::string>();
+  const auto t0 = std::chrono::steady_clock::now();
+  sweep::ResultSet rs;
+  if (job.value("clock", std::string("virtual")) == "device") {
+    const engine::DeviceOptions opt = engine::DeviceOptions::from_json(job.value("device", json::object()).dump());
+    rs = sweep::run_sweep_on_device(plan, calib, opt, manifest, table);
+  } else {
+    rs = sweep::run_sweep(plan, calib, job.value("parallelism", 1), manifest, table);
+  }
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  json cells = json::array();
+  for (const auto& c : rs.cells) cells.push_back(cell_json(c));
+  json means = json::array();
+  for (const auto& [key, m] : sweep::mean_over_seeds(rs))
+  {
+    sweep::CellResult holder;
+    holder.m = m;
+    means.push_back({std::get<0>(key), std::get<1>(key), std::get<2>(key), cell_json(holder)["metrics"]});
+  }
+  json out{{"plan_hash", rs.plan_hash}, {"calibration_hash", rs.calibration_hash}, {"cells", cells},
+           {"csv", sweep::results_csv(rs)}, {"means", means}, {"wall_s", wall}};
+  try {
+    out["winner"] = winner_json(metrics::winner_distribution(sweep::winner_inputs(rs)));
+  } catch (const std::invalid_argument& e) {
+    out["winner"] = {{"error", e.what()}};
+  }
+  json cmp = json::object();
+  for (const json& c : job.value("compare", json::array())) {
+    json rows = json::array();
+    for (const auto& r : sweep::compare_modes(rs, c[0].get<std::string>(), c[1].get<std::string>(),
+                                              c[2].get<std::string>()))
+      rows.push_back({r.shape, nan_null(r.low), nan_null(r.med), nan_null(r.high), r.low_n, r.med_n, r.high_n});
+    cmp[c[0].get<std::string>() + "|" + c[1].get<std::string>() + "|" + c[2].get<std::string>()] = rows;
+  }
+  out["compare"] = cmp;
+  return out.dump();
+}
+
+std::string op_pareto(const json& job) {
+  std::vector<metrics::ParetoPoint> pts;
+  for (const json& p : job.at("points")) pts.push_back({p[0].get<double>(), p[1].get<double>(), p[2].get<std::string>()});
+  json f = json::array();
+  for (const auto& p : metrics::pareto_frontier(pts)) f.push_back({p.ttft_p99, p.tps, p.label});
+  return json{{"frontier", f}}.dump();
+}
+
+std::string op_winner(const json& job) {
+  std::vector<metrics::WinnerCell> cells;
+  for (const json& c : job.at("cells"))
+    cells.push_back({c.at("workload_id").get<std::string>(), c.at("qps").get<double>(),
+                     c.at("config_label").get<std::string>(), c.at("category").get<std::string>(),
+                     agg_from(c.at("metrics"))});
+  return winner_json(metrics::winner_distribution(cells)).dump();
+}
+
+std::vector<routing::GridSpec> grid_from(const json& job) {
+  std::vector<routing::GridSpec> grid = routing::default_grid();
+  if (job.contains("grid_keys")) {  // subset of the default grid by key string
+    std::vector<routing::GridSpec> sub;
+    for (const json& k : job["grid_keys"])
+      for (const auto& g : grid)
+        if (g.key.str() == k.get<std::string>()) sub.push_back(g);
+    grid = sub;
+  }
+  return grid;
+}
+
+std::string op_weight_sweep(const json& job) {
+  auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
+  sweep::SweepPlan tmp = sweep::SweepPlan::from_json(
+      json{{"configs", json::array()}, {"workloads", json::array({job.at("base")})}, {"qps_levels", json::array()},
+           {"seeds", json::array()}, {"duration_s", 0.0}}
+          .dump());
+  json rows = json::array();
+  for (const auto& r : sweep::weight_sweep(job.at("shape").get<std::string>(), tmp.workloads.at(0),
+                                           job.at("qps_levels").get<std::vector<double>>(),
+                                           job.at("w_tpot_list").get<std::vector<double>>(), calib, grid_from(job),
+                                           job.at("seeds").get<std::vector<std::uint64_t>>()))
+    rows.push_back({r.w_tpot, nan_null(r.ttft_change), nan_null(r.tpot_change), r.d_local_ratio});
+  return json{{"rows", rows}}.dump();
+}
+
+std::string op_plan_default() {
+  const sweep::SweepPlan p = sweep::SweepPlan::full_default();
+  return json{{"plan_json", p.to_json()}, {"hash", p.hash()}, {"cell_count", p.cell_count()}}.dump();
+}
+
+std::string op_ingest_trace(const json& job) {
+  std::istringstream in(job.at("trace_jsonl").get<std::string>());
+  workload::TraceFilter f;
+  f.min_turns = job.value("min_turns", 2);
+  f.min_turn2_input_output_ratio = job.value("min_ratio", 0.0);
+  if (job.contains("sample_size")) f.sample_size = job["sample_size"].get<std::size_t>();
+  f.sample_seed = job.value("sample_seed", std::uint64_t{0});
+  json convs = json::array();
+  for (const auto& c : workload::ingest_trace(in, f)) {
+    json turns = json::array();
+    for (const auto& t : c.turns)
+      turns.push_back({t.new_input_tokens, t.target_output_tokens, t.cached_context_tokens});
+    convs.push_back({{"conv_id", c.conv_id}, {"turns", turns}});
+  }
+  return json{{"conversations", convs}}.dump();
+}
+
 std::string run(const std::string& text) {
   const json job = json::parse(text);
   const std::string op = job.value("op", std::string("simulate"));
   if (op == "fit_calibration") return fit(job);
   if (op == "build_table") return build_table(job);
+  if (op == "sweep") return op_sweep(job);
+  if (op == "pareto") return op_pareto(job);
+  if (op == "winner") return op_winner(job);
+  if (op == "weight_sweep") return op_weight_sweep(job);
+  if (op == "plan_default") return op_plan_default();
+  if (op == "ingest_trace") return op_ingest_trace(job);
   auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
   sim::ClusterConfig cfg = sim::ClusterConfig::from_name(job.at("cluster").get<std::string>(), policy_from(job), calib);
   if (job.contains("max_decode_batch")) cfg.max_decode_batch = job["max_decode_batch"].get<int>();

@@ -101,3 +101,30 @@ def test_device_timeouts_and_hybrid(gpu):
         else:
             assert "R_local" not in rs
     assert all(x["status"] == "completed" for x in E.records(h))
+
+
+def test_device_clock_sweep_manifest_readable_by_reference(gpu, tmp_path):
+    """§8f-2 on real runs: a sweep plan whose every cell executes on the GPU
+    (engine device clock). Cells complete, the CSV has one row per cell, and
+    the manifest directory is read back unchanged by the reference's own
+    run_sweep (it resumes from our cells instead of simulating them)."""
+    wl = {"id": "tiny_bal", "turn1": {"input_tokens": 48, "output_tokens": 6},
+          "turn2plus": {"input_tokens": 24, "output_tokens": 6}, "num_turns": 2, "qps": 1.0,
+          "duration_s": 1.5, "think_time_s": 0.0, "jitter_pct": 0.0}
+    plan = {"schema_version": 1,
+            "configs": [{"shape": "1P_1D", "x_mode": "x0"}, {"shape": "1P_1D", "x_mode": "x1"},
+                        {"shape": "2R", "x_mode": "replica"}],
+            "workloads": [wl], "qps_levels": [2.0], "seeds": [1], "duration_s": 1.5}
+    job = {"op": "sweep", "plan": plan, "clock": "device", "manifest_dir": str(tmp_path),
+           "device": {"model": "tiny", "weight_seed": 5, "token_seed": 9, "gpus": [0], "prefill_chunk": 64},
+           "compare": [["x0", "x1", "ttft_t2_mean"]]}
+    r = E.run(job)
+    assert len(r["cells"]) == 3 and not any(c["failed"] for c in r["cells"])
+    assert all(c["metrics"]["success_rate"] == 1.0 for c in r["cells"])
+    assert r["csv"].count("\n") == 4
+    assert "render" in r["winner"]
+    ref = O.ref_tool({"op": "sweep", "plan": plan, "manifest_dir": str(tmp_path)})
+    assert ref["cells"] == r["cells"] and ref["csv"] == r["csv"] and ref["winner"] == r["winner"]
+    # the virtual clock disagrees with the device clock on these numbers
+    virt = E.run({"op": "sweep", "plan": plan})
+    assert virt["cells"] != r["cells"]
