@@ -47,6 +47,15 @@ cost::CalibrationTable calib_from(const json& job) {
 }
 
 std::vector<workload::Conversation> convs_from(const json& job) {
+  if (job.contains("trace_jsonl")) {  // real-trace replay (workload.cpp ingest_trace)
+    std::istringstream in(job["trace_jsonl"].get<std::string>());
+    workload::TraceFilter f;
+    f.min_turns = job.value("min_turns", 2);
+    f.min_turn2_input_output_ratio = job.value("min_ratio", 0.0);
+    if (job.contains("sample_size")) f.sample_size = job["sample_size"].get<std::size_t>();
+    f.sample_seed = job.value("sample_seed", std::uint64_t{0});
+    return workload::ingest_trace(in, f);
+  }
   if (job.contains("workload")) {
     const json& w = job["workload"];
     workload::WorkloadSpec s;

@@ -128,3 +128,27 @@ def test_device_clock_sweep_manifest_readable_by_reference(gpu, tmp_path):
     # the virtual clock disagrees with the device clock on these numbers
     virt = E.run({"op": "sweep", "plan": plan})
     assert virt["cells"] != r["cells"]
+
+
+def test_device_clock_trace_replay(gpu):
+    """§8f-4 on the device: a JSONL trace (ingest_trace filters) replayed at a
+    fixed QPS through the engine's device clock; every request completes with
+    exactly its target output and the routes follow x (x=1: turn 2+ local)."""
+    import json as _json
+    rng = np.random.default_rng(3)
+    lines = []
+    for i in range(8):
+        turns = [{"input_tokens": int(rng.integers(8, 64)), "output_tokens": int(rng.integers(2, 7))}
+                 for _ in range(int(rng.integers(1, 4)))]
+        lines.append(_json.dumps({"conv_id": f"t{i}", "turns": turns}))
+    job = {"cluster": "1P_1D", "x": 1.0, "clock": "device", "trace_jsonl": "\n".join(lines) + "\n",
+           "min_turns": 2, "qps_replay": 4.0, "seed": 2,
+           "device": {"model": "tiny", "weight_seed": 5, "token_seed": 9, "gpus": [0], "prefill_chunk": 64}}
+    r = E.run(job)
+    recs = E.records(r)
+    kept = E.run({"op": "ingest_trace", "trace_jsonl": job["trace_jsonl"], "min_turns": 2})["conversations"]
+    assert len(recs) == sum(len(c["turns"]) for c in kept) > 0
+    want = {(c["conv_id"], i + 1): t[1] for c in kept for i, t in enumerate(c["turns"])}
+    assert all(x["status"] == "completed" and x["output_tokens_emitted"] == want[(x["conv_id"], x["turn_index"])]
+               for x in recs)
+    assert all(x["route"] == "D_local" for x in recs if x["turn_index"] > 1)

@@ -200,3 +200,17 @@ def test_compare_modes_nan_bands():
     assert rows and rows[0][3] is None and rows[0][6] == 0
     assert ours["compare"] == O.ref_tool(job)["compare"]
     assert not any(isinstance(v, float) and math.isnan(v) for v in rows[0][1:3])
+
+
+@pytest.mark.parametrize("cluster,x,qps", [("1P_3D", 0.0, 2.0), ("2P_2D", 1.0, 6.0), ("1R_1P_2D", 0.5, 4.0)])
+def test_trace_replay_matches_reference(cluster, x, qps):
+    """§8f-4: a ShareGPT-shaped JSONL trace, ingested (filters + sampling) and
+    replayed at a target QPS, gives the reference's records byte for byte."""
+    text = trace_jsonl(random.Random(21), 80)
+    job = {"cluster": cluster, "x": x, "trace_jsonl": text, "min_turns": 2, "sample_size": 30, "sample_seed": 4,
+           "qps_replay": qps, "seed": 7}
+    ours, ref = E.run({"op": "simulate", **job}), O.ref_tool({"op": "simulate", **job})
+    assert ours["records_jsonl"] == ref["records_jsonl"]
+    for k in ("link_transfers", "link_bytes", "makespan", "node_stats"):
+        assert ours[k] == ref[k], k
+    assert len(E.records(ours)) > 30
