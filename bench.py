@@ -133,11 +133,12 @@ def engine_ttft(gpus, layout: str, quick: bool = False):
     on the DEVICE clock: every prefill chunk, decode iteration and P->D KV hop
     runs on the GPUs listed (node i -> gpus[i]); each node's clock advances by
     the CUDA-event time of its own work. 1P_1D uses the BASELINE configs[2]
-    trace (4 turns of 1536 in / 128 out); the 8-node layouts use configs[3]
+    trace (4 turns of 1536 in / 512 out); the 8-node layouts use configs[3]
     (2048 then 2x1024 in, 128 out, high load)."""
     from paper_2603_13358_b200 import engine as E
     if layout in ("1P_1D", "1R"):
-        wl = {"id": "cfg3", "turn1": [1536, 128], "turn2plus": [1536, 128], "num_turns": 4,
+        # BASELINE configs[2]: 4 turns, +2048 tokens of context per turn (1536 in, 512 out)
+        wl = {"id": "cfg3", "turn1": [1536, 512], "turn2plus": [1536, 512], "num_turns": 4,
               "qps": 1.0, "duration_s": 4.0 if quick else 8.0}
     else:
         wl = {"id": "cfg4", "turn1": [2048, 128], "turn2plus": [1024, 128], "num_turns": 3,
@@ -149,7 +150,7 @@ def engine_ttft(gpus, layout: str, quick: bool = False):
     for x in (0.0, 1.0):
         job = {"cluster": layout, "x": x, "clock": "device", "seed": 3, "workload": wl,
                "device": {"model": "llama8b", "weight_seed": SEED, "token_seed": 3, "gpus": gpus,
-                          "kv_blocks_per_node": 4096, "prefill_chunk": 2048, "record_tokens": False}}
+                          "kv_blocks_per_node": 8192, "prefill_chunk": 2048, "record_tokens": False}}
         t0 = time.perf_counter()
         r = E.run(job)
         agg = r["aggregate"]

@@ -58,6 +58,8 @@ int g_tuning_epoch = 0;
 // Off by default: step-level A/B (tools/ab_step.py, 48 steps per arm) shows
 // no gain over the balanced-partition GEMM + silu_mul_kernel (within 1%).
 bool g_mlp_fused = false;
+bool g_ops_w_tiled = false;
+int g_gemm_diag = 0, g_gemm_promo = 2;  // ppd_op_gemm_tc/_silu/_parts: B is k-block tiled (ppd_op_tile_matrix)
 // diagnostics only ("diag_skip" knob): skip kernel classes of the forward step
 // (1 small ops, 2 attention, 4 GEMMs) to time their marginal cost in the live
 // graph. Results are meaningless while set.
@@ -100,6 +102,7 @@ struct ppd_dev {
   bf16 *embed = nullptr, *lm_head = nullptr, *ones = nullptr;
   std::vector<Layer> layers;
   bool weights_ready = false;
+  bool w_tiled = false;  // GEMM weights stored k-block tiled (ppd_load_random_weights)
   float *rope_cos = nullptr, *rope_sin = nullptr;
   // KV pool
   bf16* kv = nullptr;
@@ -698,8 +701,16 @@ int ppd_load_random_weights(ppd_dev* d, uint64_t seed) {
   d->embed = reinterpret_cast<bf16*>(take(V * dm * 2));
   d->lm_head = reinterpret_cast<bf16*>(take(V * dm * 2));
   d->ones = reinterpret_cast<bf16*>(take(dm * 2));
+  // GEMM weights are stored k-block tiled for the tcgen05 path (one contiguous
+  // 16 KB HBM run per TMA box: the decode step streams them at full DRAM
+  // efficiency); row-major for the cuBLAS reference path
+  const bool tiled = gemm_uses_tcgen05(d->gemm) && (qd + 2 * kd) % 128 == 0 && dm % 128 == 0 &&
+                     (2 * F) % 128 == 0 && V % 128 == 0 && dm % 64 == 0 && qd % 64 == 0 && F % 64 == 0;
+  gemm_set_weights_tiled(d->gemm, tiled);
+  d->w_tiled = tiled;
+  const int ti = tiled ? 1 : 0;
   CU(launch_fill_random(d->embed, V * dm, seed, 0, 0, s));
-  CU(launch_fill_random(d->lm_head, V * dm, seed, 8, 0, s));
+  CU(launch_fill_matrix(d->lm_head, V, dm, seed, 8, 0, ti, s));
   CU(launch_fill_const(d->ones, dm, 1.0f, s));
   d->layers.assign(c.n_layers, Layer{});
   for (int l = 0; l < c.n_layers; ++l) {
@@ -710,10 +721,10 @@ int ppd_load_random_weights(ppd_dev* d, uint64_t seed) {
     w.wdown = reinterpret_cast<bf16*>(take(dm * F * 2));
     float* b = reinterpret_cast<float*>(take((qd + 2 * kd) * 4));
     w.bqkv = c.qkv_bias ? b : nullptr;
-    CU(launch_fill_qkv(w.wqkv, (int)qd, (int)kd, (int)dm, seed, l, s));
-    CU(launch_fill_random(w.wo, dm * qd, seed, 4, l, s));
-    CU(launch_fill_gate_up(w.wgu, (int)F, (int)dm, seed, l, s));
-    CU(launch_fill_random(w.wdown, dm * F, seed, 7, l, s));
+    CU(launch_fill_qkv(w.wqkv, (int)qd, (int)kd, (int)dm, seed, l, ti, s));
+    CU(launch_fill_matrix(w.wo, dm, qd, seed, 4, l, ti, s));
+    CU(launch_fill_gate_up(w.wgu, (int)F, (int)dm, seed, l, ti, s));
+    CU(launch_fill_matrix(w.wdown, dm, F, seed, 7, l, ti, s));
     if (c.qkv_bias) CU(launch_fill_bias(w.bqkv, (int)qd, (int)kd, seed, l, s));
   }
   CU(cudaStreamSynchronize(s));
@@ -1002,7 +1013,7 @@ int ppd_op_gemm_tc(const void* A, const void* B, void* C, int32_t M, int32_t N, 
   CHECK_ARG(K % 8 == 0, "K must be a multiple of 8");
   CHECK_ARG(splits == 1 || out_f32, "K-split partials need fp32 output");
   CU(gemm_tc_run(static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0, splits,
-                 (size_t)M * N, static_cast<cudaStream_t>(stream)));
+                 (size_t)M * N, static_cast<cudaStream_t>(stream), g_ops_w_tiled));
   return PPD_OK;
 }
 
@@ -1010,7 +1021,7 @@ int ppd_op_gemm_silu(const void* A, const void* B, void* m, int32_t M, int32_t N
   CHECK_ARG(A && B && m && M > 0 && N > 0 && K > 0, "bad gemm args");
   CHECK_ARG(K % 8 == 0 && N % 128 == 0, "K must be a multiple of 8 and N of 128");
   CU(gemm_tc_run_silu(static_cast<const bf16*>(A), static_cast<const bf16*>(B), static_cast<bf16*>(m), M, N, K,
-                      static_cast<cudaStream_t>(stream)));
+                      static_cast<cudaStream_t>(stream), g_ops_w_tiled));
   return PPD_OK;
 }
 
@@ -1020,7 +1031,7 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
   CHECK_ARG(K % 8 == 0, "K must be a multiple of 8");
   GemmParts g;
   CU(gemm_tc_run_parts(static_cast<const bf16*>(A), static_cast<const bf16*>(B), static_cast<float*>(C), M, N, K,
-                       max_slices, (size_t)M * N, &g, static_cast<cudaStream_t>(stream)));
+                       max_slices, (size_t)M * N, &g, static_cast<cudaStream_t>(stream), g_ops_w_tiled));
   parts->n = g.n;
   parts->kbt = g.kbt;
   parts->slots = g.slots;
@@ -1047,6 +1058,26 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "diag_skip") == 0) {
     CHECK_ARG(value >= 0 && value <= 7, "diag_skip must be in [0, 7]");
     g_diag_skip = value;
+  } else if (std::strcmp(name, "gemm_diag") == 0) {
+    CHECK_ARG(value >= 0 && value <= 7, "gemm_diag must be in [0, 7]");
+    g_gemm_diag = value;
+    gemm_tc_set_diag(g_gemm_diag, g_gemm_promo);
+  } else if (std::strcmp(name, "gemm_w_promo") == 0) {
+    CHECK_ARG(value >= 0 && value <= 2, "gemm_w_promo must be in [0, 2]");
+    g_gemm_promo = value;
+    gemm_tc_set_diag(g_gemm_diag, g_gemm_promo);
+  } else if (std::strcmp(name, "gemm_wsplit") == 0) {
+    CHECK_ARG(value == 1 || value == 2 || value == 4 || value == 8, "gemm_wsplit must be 1, 2, 4 or 8");
+    gemm_tc_set_w_split(value);
+  } else if (std::strcmp(name, "gemm_occ2") == 0) {
+    CHECK_ARG(value >= -1 && value <= 1, "gemm_occ2 must be -1, 0 or 1");
+    gemm_tc_set_occ2(value);
+  } else if (std::strcmp(name, "gemm_multi_sub") == 0) {
+    CHECK_ARG(value == 0 || value == 1, "gemm_multi_sub must be 0 or 1");
+    gemm_tc_set_multi_sub(value != 0);
+  } else if (std::strcmp(name, "ops_w_tiled") == 0) {
+    CHECK_ARG(value == 0 || value == 1, "ops_w_tiled must be 0 or 1");
+    g_ops_w_tiled = value != 0;
   } else if (std::strcmp(name, "mlp_fused") == 0) {
     CHECK_ARG(value == 0 || value == 1, "mlp_fused must be 0 or 1");
     g_mlp_fused = value != 0;
@@ -1055,6 +1086,21 @@ int ppd_set_tuning(const char* name, int32_t value) {
   }
   gemm_tc_set_tuning(pair, stages, sched);
   ++g_tuning_epoch;
+  return PPD_OK;
+}
+
+int ppd_op_gemm_timeline(uint64_t* out, int32_t max_ctas) {
+  CHECK_ARG(out && max_ctas > 0, "bad timeline args");
+  const int n = gemm_tc_read_timeline(reinterpret_cast<unsigned long long*>(out), max_ctas);
+  if (n < 0) return fail(PPD_ERR_CUDA, "timeline read");
+  return n;
+}
+
+int ppd_op_tile_matrix(const void* src, void* dst, int32_t N, int32_t K, void* stream) {
+  CHECK_ARG(src && dst && N > 0 && K > 0, "bad tile args");
+  CHECK_ARG(N % 128 == 0 && K % 64 == 0, "tiled layout needs N % 128 == 0 and K % 64 == 0");
+  CU(launch_tile_matrix(static_cast<const bf16*>(src), static_cast<bf16*>(dst), (uint64_t)N, (uint64_t)K,
+                        static_cast<cudaStream_t>(stream)));
   return PPD_OK;
 }
 

@@ -50,6 +50,15 @@ PPD_DEV void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint6
       : "memory");
 }
 
+// one 16 KB k-block tile of a k-block-tiled weight (3-D map: 64 x 128 x tiles)
+PPD_DEV void tma_load_tile(void* smem, const CUtensorMap* map, int y, int tile, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(tile), "r"(smem_u32(bar))
+      : "memory");
+}
+
 PPD_DEV uint64_t sw128_kmajor_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);   // start address
@@ -112,6 +121,13 @@ PPD_DEV void tma_load_2d_pair(void* smem, const CUtensorMap* map, int x, int y, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster)
       : "memory");
 }
+PPD_DEV void tma_load_tile_pair(void* smem, const CUtensorMap* map, int y, int tile, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(tile), "r"(bar_cluster)
+      : "memory");
+}
 PPD_DEV void mma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -144,6 +160,20 @@ PPD_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
 
 }  // namespace
 
+// ---- timing probe (gemm_diag bit 2) ------------------------------------------
+constexpr int kMaxTsCtas = 512;
+__device__ unsigned long long g_gemm_ts[kMaxTsCtas][6];
+PPD_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+int gemm_tc_read_timeline(unsigned long long* out, int max_ctas) {
+  const int n = max_ctas < kMaxTsCtas ? max_ctas : kMaxTsCtas;
+  return cudaMemcpyFromSymbol(out, g_gemm_ts, (size_t)n * 6 * sizeof(unsigned long long)) == cudaSuccess ? n : -1;
+}
+
 // ---- work schedule shared by the producer, MMA and epilogue roles ----------
 // A segment is a contiguous k-block range [kb0, kb1) of one (weight tile,
 // token tile) whose accumulator goes to partial slice `slice`.
@@ -159,7 +189,7 @@ struct Sched {
   long long total, x, end;
 
   PPD_DEV void begin(const GemmTcParams& p, int rows, int c_, int slots_) {
-    n_tiles_t = (p.T + p.bn - 1) / p.bn;
+    n_tiles_t = (p.T + p.bn * p.n_sub - 1) / (p.bn * p.n_sub);
     kbt = (p.K + kBK - 1) / kBK;
     splits = p.splits;
     kb_per = (kbt + splits - 1) / splits;
@@ -219,16 +249,19 @@ struct Sched {
 // leader alone arms it with both CTAs' bytes); the leader's commits multicast
 // to the smem-slot and accumulator barriers of both CTAs; both epilogues
 // release an accumulator on the leader's barrier (8 warp arrivals).
-template <bool kPair, int kEpi>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool kPair, int kEpi, int kOcc>
+__global__ void __launch_bounds__(kThreads, kOcc)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                    GemmTcParams p) {
+  const unsigned long long t_entry = (p.diag & 4) ? globaltimer_ns() : 0ull;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kCta = kPair ? 2 : 1;
   const int S = p.stages;
-  const int xrows = p.bn / kCta;  // token rows this CTA loads per stage
-  const int stage_bytes = kWBytes + xrows * kBK * 2;  // both multiples of 1 KB
+  const int xrows = p.bn / kCta;  // token rows this CTA loads per stage and token sub-tile
+  const int n_sub = p.n_sub;      // token sub-tiles of bn rows per unit (one weight stage feeds all)
+  const int unit_t = p.bn * n_sub;
+  const int stage_bytes = kWBytes + n_sub * xrows * kBK * 2;  // multiples of 1 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;      // [2]
@@ -241,7 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool leader = rank == 0;
   const int slot = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int n_slots = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int n_acc = p.tmem_cols >= 2 * p.bn_cols ? 2 : 1;
+  const int acc_cols = n_sub * p.bn_cols;  // TMEM columns of one accumulator set
+  const int n_acc = p.tmem_cols >= 2 * acc_cols ? 2 : 1;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -270,6 +304,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (kPair) cluster_sync_all();  // peer barriers initialised + TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // diag bit 2: per-CTA timeline (globaltimer ns) into g_gemm_ts[blockIdx.x][0..5]
+  unsigned long long* ts = (p.diag & 4) && blockIdx.x < kMaxTsCtas ? g_gemm_ts[blockIdx.x] : nullptr;
+  if (ts && threadIdx.x == 0) {
+    ts[0] = t_entry;
+    ts[1] = globaltimer_ns();
+  }
   pdl_trigger();  // the next kernel may launch; it waits for our completion itself
 
   const int rows = kBM * kCta;
@@ -277,7 +317,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t acc_empty0 = kPair ? mapa_shared(smem_u32(acc_empty), 0) : smem_u32(acc_empty);
   const int w_row0 = (int)rank * kBM;
   const int x_row0 = (int)rank * xrows;
-  const uint32_t tx_bytes = (uint32_t)(kCta * stage_bytes);
+  // diag bit 0: skip the activation loads (timing probe only)
+  const uint32_t tx_bytes = (uint32_t)(kCta * ((p.diag & 1) ? kWBytes : stage_bytes));
 
   auto load = [&](void* dst, const CUtensorMap* map, int x, int y, int s) {
     if (kPair)
@@ -285,9 +326,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     else
       tma_load_2d(dst, map, x, y, &full[s]);
   };
+  // sub-box `i` (of p.w_split) of the 128 x 64 weight box of k-block kb at
+  // weight row `row` (a multiple of 128): rows [i*128/ws, (i+1)*128/ws)
+  const int w_kbt = (p.K + kBK - 1) / kBK;
+  const int ws = p.w_split, ws_rows = kBM / ws;
+  auto load_w = [&](void* dst, int kb, int row, int s, int i) {
+    dst = static_cast<uint8_t*>(dst) + i * (kWBytes / ws);
+    if (p.w_tiled) {
+      const int tile = (row / kBM) * w_kbt + kb;
+      if (kPair)
+        tma_load_tile_pair(dst, &map_w, i * ws_rows, tile, full_bar0 + 8u * s);
+      else
+        tma_load_tile(dst, &map_w, i * ws_rows, tile, &full[s]);
+    } else {
+      load(dst, &map_w, kb * kBK, row + i * ws_rows, s);
+    }
+  };
 
   if (warp == 0) {
-    if (lane == 0) {
+    // The whole warp walks the schedule; lane 0 arms each stage's barrier,
+    // then lanes [0, ws) issue the weight sub-boxes and lanes [16, 16+n_sub)
+    // the activation boxes in parallel (several TMA boxes in flight per stage).
+    {
       Sched sc;
       sc.begin(p, rows, slot, n_slots);
       Seg sg;
@@ -296,8 +356,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         Sched pre = sc;
         while (npre < S && pre.next(sg)) {
           for (int kb = sg.kb0; kb < sg.kb1 && npre < S; ++kb, ++npre) {
-            if (leader) mbar_arrive_expect_tx(&full[npre], tx_bytes);
-            load(smem + npre * stage_bytes, &map_w, kb * kBK, sg.tw * rows + w_row0, npre);
+            if (leader && lane == 0) mbar_arrive_expect_tx(&full[npre], tx_bytes);
+            __syncwarp();
+            if (lane < ws) load_w(smem + npre * stage_bytes, kb, sg.tw * rows + w_row0, npre, lane);
           }
         }
       }
@@ -314,10 +375,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               else
                 mbar_wait(&empty[s], ((it / S) - 1) & 1);
             }
-            if (leader) mbar_arrive_expect_tx(&full[s], tx_bytes);
-            load(sw, &map_w, kb * kBK, sg.tw * rows + w_row0, s);
+            if (leader && lane == 0) mbar_arrive_expect_tx(&full[s], tx_bytes);
+            __syncwarp();
+            if (lane < ws) load_w(sw, kb, sg.tw * rows + w_row0, s, lane);
           }
-          load(sw + kWBytes, &map_x, kb * kBK, sg.tt * p.bn + x_row0, s);
+          const int jx = lane - 16;
+          if (jx >= 0 && jx < n_sub && !(p.diag & 1))
+            load(sw + kWBytes + jx * xrows * (kBK * 2), &map_x, kb * kBK, sg.tt * unit_t + jx * p.bn + x_row0, s);
         }
       }
     }
@@ -339,21 +403,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&acc_empty[acc], (use - 1) & 1);
         }
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * p.bn_cols);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * acc_cols);
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
           const int s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
           const uint64_t da = sw128_kmajor_desc(sa);
-          const uint64_t db = sw128_kmajor_desc(sa + kWBytes);
+          if (ts && it == 0) ts[2] = globaltimer_ns();
+          for (int js = 0; js < n_sub; ++js) {
+            const uint64_t db = sw128_kmajor_desc(sa + kWBytes + js * xrows * (kBK * 2));
+            const uint32_t dj = d_tmem + (uint32_t)(js * p.bn_cols);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {  // 32 B per UMMA_K step inside the swizzle atom
-            const uint32_t accum = (kb != sg.kb0) || (k != 0);
-            if (kPair)
-              mma_bf16_pair(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, accum);
-            else
-              mma_bf16(d_tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, accum);
+            for (int k = 0; k < kBK / 16 && !(p.diag & 2); ++k) {  // 32 B per UMMA_K inside the atom
+              const uint32_t accum = (kb != sg.kb0) || (k != 0);
+              if (kPair)
+                mma_bf16_pair(dj, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, accum);
+              else
+                mma_bf16(dj, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, accum);
+            }
           }
           if (kPair)
             mma_commit_pair(&empty[s]);  // smem slot (in both CTAs) free once these MMAs retire
@@ -365,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
           mma_commit(&acc_full[acc]);
       }
+      if (ts) ts[3] = globaltimer_ns();
     }
   } else if (warp >= 4) {
     pdl_wait();  // outputs are written only after the predecessor retired
@@ -376,12 +445,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int acc = j % n_acc;
       const int use = j / n_acc;
       const int row = sg.tw * rows + w_row0 + q * 32 + lane;
-      const int t0 = sg.tt * p.bn;
       mbar_wait(&acc_full[acc], use & 1);
       tc_fence_after();
       float* out32 = reinterpret_cast<float*>(p.out) + (size_t)sg.slice * p.split_stride;
       __nv_bfloat16* out16 = reinterpret_cast<__nv_bfloat16*>(p.out);
-      const uint32_t t_acc = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * p.bn_cols);
+      int buf = 0;  // exchange buffer parity runs on across sub-tiles (double buffering)
+      for (int jsub = 0; jsub < n_sub; ++jsub) {
+      const int t0 = sg.tt * unit_t + jsub * p.bn;
+      const uint32_t t_acc =
+          tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * acc_cols + jsub * p.bn_cols);
       const int ncols = min(p.bn, p.T - t0);
       if (kEpi == kEpiSilu) {
         // Fused SiLU(gate) * up. The 128-row slab of this CTA is one interleaved
@@ -392,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // silu_mul_kernel, so the unfused path gives the same bits).
         const int grp = (sg.tw * rows + w_row0) / kBM;
         __nv_bfloat16* m = reinterpret_cast<__nv_bfloat16*>(p.out);
-        for (int c0 = 0, buf = 0; c0 < ncols; c0 += 32, buf ^= 1) {
+        for (int c0 = 0; c0 < ncols; c0 += 32, buf ^= 1) {
           uint32_t r[32];
           tmem_ld32(t_acc + (uint32_t)c0, r);
           float* xb = xchg + buf * 2048;
@@ -420,19 +492,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(t_acc + (uint32_t)c0, r);
         if (row < p.N) {
           const int nj = min(32, ncols - c0);
+          // one running pointer (not 32 precomputed addresses): keeps the
+          // epilogue's register footprint small enough for 2 CTAs per SM
           if (p.out_f32) {
             float* dst = out32 + (size_t)(t0 + c0) * p.ldo + row;
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-              if (jj < nj) dst[(size_t)jj * p.ldo] = __uint_as_float(r[jj]);
+            for (int jj = 0; jj < 32; ++jj) {
+              if (jj < nj) *dst = __uint_as_float(r[jj]);
+              dst += p.ldo;
+            }
           } else {
             __nv_bfloat16* dst = out16 + (size_t)(t0 + c0) * p.ldo + row;
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-              if (jj < nj) dst[(size_t)jj * p.ldo] = __float2bfloat16_rn(__uint_as_float(r[jj]));
+            for (int jj = 0; jj < 32; ++jj) {
+              if (jj < nj) *dst = __float2bfloat16_rn(__uint_as_float(r[jj]));
+              dst += p.ldo;
+            }
           }
         }
       }
+      }  // token sub-tiles
+      if (ts && q == 0 && lane == 0) ts[4] = globaltimer_ns();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -446,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (kPair) cluster_sync_all();  // the leader's MMAs may read the peer's smem until here
+  if (ts && threadIdx.x == 0) ts[5] = globaltimer_ns();
   if (warp == 2) {
     if (kPair)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
@@ -509,6 +590,43 @@ bool get_map(CUtensorMap* out, const void* ptr, int rows, int K, int box_rows) {
   return true;
 }
 
+// k-block tiled [N][K] weight: a 3-D view {64 k, 128 rows, tiles} whose box
+// {64, 128, 1} is one contiguous 16 KB tile; the 128 B swizzle lands it in smem
+// exactly like the 2-D box of the row-major layout.
+int g_w_promo = 2;  // L2 promotion of weight boxes: 0 none, 1 128 B, 2 256 B
+CUtensorMapL2promotion w_promo() {
+  return g_w_promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+         : g_w_promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
+bool get_map_tiled(CUtensorMap* out, const void* ptr, int N, int K, int ws) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  MapKey key{ptr, N, K, -1 - g_w_promo - 4 * ws};
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return true;
+  }
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t tiles = (cuuint64_t)(N / kBM) * (cuuint64_t)(K / kBK);
+  cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)kBM, tiles};
+  cuuint64_t strides[2] = {(cuuint64_t)kBK * 2, (cuuint64_t)kWBytes};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)(kBM / ws), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUtensorMap m;
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, w_promo(),
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, m);
+  *out = m;
+  return true;
+}
+
 }  // namespace
 // Tuning knobs (ppd_set_tuning): pair = -1 auto / 0 single-CTA / 1 CTA pair;
 // stages = cap on the smem ring depth (0 = as many as fit); sched = -1 auto /
@@ -516,6 +634,13 @@ bool get_map(CUtensorMap* out, const void* ptr, int rows, int K, int box_rows) {
 static int g_pair_mode = -1;
 static int g_stage_cap = 0;
 static int g_sched = -1;
+static bool g_multi_sub = true;  // T in (256, 512]: one unit covers both token sub-tiles
+// two co-resident single CTAs per SM: -1 auto (<= kOcc2MaxT tokens; measured
+// tools/gemm_knobs.py: +10-20% weight streaming at T = 64 / 128, neutral at
+// T = 200, a loss with CTA pairs), 0 off, 1 whenever the shape allows
+static int g_occ2 = -1;
+constexpr int kOcc2MaxT = 128;
+constexpr int kOcc2Smem = 113 * 1024;
 
 
 
@@ -525,6 +650,16 @@ static int g_sched = -1;
 // one-tile-per-CTA GEMMs such as QKV / o-proj / down-proj of a decode step).
 constexpr int kPairMinT = 48;
 constexpr double kPairMinTilesPerSm = 1.4;
+
+void gemm_tc_set_multi_sub(bool on) { g_multi_sub = on; }
+static int g_diag = 0;
+static int g_w_split = 1;
+void gemm_tc_set_diag(int diag, int w_promo) {
+  g_diag = diag;
+  g_w_promo = w_promo;
+}
+void gemm_tc_set_w_split(int ws) { g_w_split = ws; }
+void gemm_tc_set_occ2(int mode) { g_occ2 = mode; }
 
 void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched) {
   g_pair_mode = pair_mode;
@@ -537,24 +672,32 @@ namespace {
 struct Shape {
   bool pair;
   int bn, rows, stages, stage_bytes, smem, slots;  // slots = co-resident CTAs (single) or pairs
+  int n_sub;   // token sub-tiles of bn rows per unit: a decode + append step of T <= 512 rows
+               // streams each weight stage ONCE for all its tokens (2 MMAs of N = bn)
+  int unit_t;  // token rows per unit = bn * n_sub
+  int occ;     // co-resident CTAs per SM: 2 = half the smem ring and one 256-column
+               // accumulator each, so one CTA's fill / epilogue tail (and the next
+               // kernel's PDL prologue) overlaps the other's weight streaming
 };
 
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
   const int bytes = 1024 + kSmemBudget + kBarBytes;
-  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiPlain>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiSilu>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiSilu>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiPlain, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiPlain, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiSilu, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiSilu, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiPlain, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOcc2Smem);
+  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiPlain, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOcc2Smem);
   done = true;
 }
 
-int max_pair_slots(int smem) {
+int max_pair_slots(int smem, int occ) {
   static std::mutex mu;
   static std::unordered_map<int, int> cache;
   std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(smem);
+  auto it = cache.find(smem * 4 + occ);
   if (it != cache.end()) return it->second;
   set_smem_attrs();
   cudaLaunchConfig_t cfg{};
@@ -569,30 +712,46 @@ int max_pair_slots(int smem) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<true, kEpiPlain>, &cfg) != cudaSuccess || n <= 0) {
+  cfg.gridDim = dim3(2 * 74 * occ);
+  const cudaError_t e = occ == 2 ? cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<true, kEpiPlain, 2>, &cfg)
+                                 : cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<true, kEpiPlain, 1>, &cfg);
+  if (e != cudaSuccess || n <= 0) {
     cudaGetLastError();
     n = 0;
   }
-  cache.emplace(smem, n);
+  cache.emplace(smem * 4 + occ, n);
   return n;
 }
 
 Shape shape_for(int T, int N, int extra_smem = 0, bool force_single = false) {
   Shape sh{};
-  sh.bn = T >= kMaxBN ? kMaxBN : ((T + 15) / 16) * 16;
-  const double tiles1 = double((N + kBM - 1) / kBM) * ((T + sh.bn - 1) / sh.bn);
+  if (T <= kMaxBN) {
+    sh.n_sub = 1;
+    sh.bn = ((T + 15) / 16) * 16;
+  } else if (T <= 2 * kMaxBN && g_multi_sub) {
+    sh.n_sub = 2;
+    sh.bn = (((T + 1) / 2 + 15) / 16) * 16;
+  } else {
+    sh.n_sub = 1;
+    sh.bn = kMaxBN;
+  }
+  sh.unit_t = sh.bn * sh.n_sub;
+  const double tiles1 = double((N + kBM - 1) / kBM) * ((T + sh.unit_t - 1) / sh.unit_t);
   const bool auto_pair = T >= kPairMinT && tiles1 >= kPairMinTilesPerSm * 148;
-  sh.pair = !force_single && (g_pair_mode == 1 || (g_pair_mode < 0 && auto_pair));
+  const bool want_occ2 = sh.n_sub == 1 && extra_smem == 0 && (g_occ2 == 1 || (g_occ2 < 0 && T <= kOcc2MaxT));
+  sh.pair = !force_single && (g_pair_mode == 1 || (g_pair_mode < 0 && auto_pair && !want_occ2));
   sh.rows = sh.pair ? 2 * kBM : kBM;
-  sh.stage_bytes = kWBytes + (sh.pair ? sh.bn / 2 : sh.bn) * kBK * 2;
-  int stages = (kSmemBudget - extra_smem) / sh.stage_bytes;
+  sh.stage_bytes = kWBytes + sh.n_sub * (sh.pair ? sh.bn / 2 : sh.bn) * kBK * 2;
+  sh.occ = (want_occ2 && (!sh.pair || g_occ2 == 1) && (kOcc2Smem - 1024 - kBarBytes) / sh.stage_bytes >= 3) ? 2 : 1;
+  const int budget = sh.occ == 2 ? kOcc2Smem - 1024 - kBarBytes : kSmemBudget;
+  int stages = (budget - extra_smem) / sh.stage_bytes;
   stages = stages > kMaxStages ? kMaxStages : stages;
   if (g_stage_cap > 0 && g_stage_cap < stages) stages = g_stage_cap;
   sh.stages = stages;
   sh.smem = 1024 + stages * sh.stage_bytes + kBarBytes + extra_smem;
-  sh.slots = 148;
+  sh.slots = 148 * sh.occ;
   if (sh.pair) {
-    sh.slots = max_pair_slots(sh.smem);
+    sh.slots = max_pair_slots(sh.smem, sh.occ);
     if (sh.slots <= 0) return shape_for(T, N, extra_smem, true);  // no co-resident pair fits: single-CTA kernel
   }
   return sh;
@@ -612,11 +771,11 @@ struct Plan {
 //   balanced  : ceil(total/slots) k-blocks of W + (segments) partial tiles out
 // Slices are capped so the callers' workspaces (max_slices slices) hold them.
 Plan plan_for(const Shape& sh, int T, int N, int K, int max_slices) {
-  const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.bn - 1) / sh.bn);
+  const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.unit_t - 1) / sh.unit_t);
   const int kbt = (K + kBK - 1) / kBK;
   const double w_kb = double(kBM) * kBK * 2.0;  // bytes of W one CTA streams per k-block
   // a partial tile is written here and re-read from L2 by the consumer: count the write
-  const double out_tile = double(sh.bn) * kBM * 4.0;
+  const double out_tile = double(sh.unit_t) * kBM * 4.0;
   Plan best{false, 1, 0, 1, 0};
   double best_cost = 1e300;
   for (int s = 1; s <= max_slices && s <= 8 && kbt / s >= 4; ++s) {
@@ -665,8 +824,9 @@ int gemm_tc_plan_splits(int T, int N, int K) {
 namespace {
 
 cudaError_t launch(const Shape& sh, const Plan& pl, const bf16* X, const bf16* W, void* out, int T, int N, int K,
-                   bool out_f32, size_t split_stride, cudaStream_t s, int epi = kEpiPlain) {
+                   bool out_f32, size_t split_stride, cudaStream_t s, int epi = kEpiPlain, bool w_tiled = false) {
   if (sh.stages < 2) return cudaErrorInvalidValue;  // ring does not fit
+  if (w_tiled && (N % kBM != 0 || K % kBK != 0)) return cudaErrorInvalidValue;
   GemmTcParams p{};
   p.out = out;
   p.T = T;
@@ -675,45 +835,55 @@ cudaError_t launch(const Shape& sh, const Plan& pl, const bf16* X, const bf16* W
   p.ldo = epi == kEpiSilu ? N / 2 : N;
   p.epi = epi;
   p.bn = sh.bn;
+  p.n_sub = sh.n_sub;
+  p.diag = g_diag;
   p.out_f32 = out_f32 ? 1 : 0;
   p.splits = pl.balanced ? 1 : pl.splits;
   p.split_stride = split_stride ? split_stride : (size_t)T * N;
   // accumulator columns per segment (power of two >= bn); two accumulators when they fit
   p.bn_cols = sh.bn <= 32 ? 32 : sh.bn <= 64 ? 64 : sh.bn <= 128 ? 128 : 256;
-  p.tmem_cols = 2 * p.bn_cols <= 512 ? 2 * p.bn_cols : p.bn_cols;
+  p.tmem_cols = 2 * sh.n_sub * p.bn_cols <= 512 ? 2 * sh.n_sub * p.bn_cols : sh.n_sub * p.bn_cols;
+  if (sh.occ == 2) p.tmem_cols = p.bn_cols;  // two CTAs share the SM's 512 columns
   p.stages = sh.stages;
   p.balanced = pl.balanced ? 1 : 0;
   p.slots = pl.slots;
   p.total = pl.total;
   CUtensorMap mw, mx;
-  if (!get_map(&mw, W, N, K, kBM) || !get_map(&mx, X, T, K, sh.pair ? sh.bn / 2 : sh.bn))
+  p.w_tiled = w_tiled ? 1 : 0;
+  p.w_split = g_w_split;
+  const bool ok_w = w_tiled ? get_map_tiled(&mw, W, N, K, p.w_split) : get_map(&mw, W, N, K, kBM / p.w_split);
+  if (!ok_w || !get_map(&mx, X, T, K, sh.pair ? sh.bn / 2 : sh.bn))
     return cudaErrorInvalidValue;
   set_smem_attrs();
   if (sh.pair)
-    return launch_pdl_cluster(epi == kEpiSilu ? gemm_tc_kernel<true, kEpiSilu> : gemm_tc_kernel<true, kEpiPlain>,
+    return launch_pdl_cluster(sh.occ == 2          ? gemm_tc_kernel<true, kEpiPlain, 2>
+                              : epi == kEpiSilu    ? gemm_tc_kernel<true, kEpiSilu, 1>
+                                                   : gemm_tc_kernel<true, kEpiPlain, 1>,
                               dim3(2 * pl.slots), dim3(kThreads), (size_t)sh.smem, 2, s, mw,
                               mx, p);
-  return launch_pdl(epi == kEpiSilu ? gemm_tc_kernel<false, kEpiSilu> : gemm_tc_kernel<false, kEpiPlain>,
+  return launch_pdl(sh.occ == 2       ? gemm_tc_kernel<false, kEpiPlain, 2>
+                    : epi == kEpiSilu ? gemm_tc_kernel<false, kEpiSilu, 1>
+                                      : gemm_tc_kernel<false, kEpiPlain, 1>,
                     dim3(pl.slots), dim3(kThreads), (size_t)sh.smem, s, mw, mx, p);
 }
 
 }  // namespace
 
 cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, int K, bool out_f32, int splits,
-                        size_t split_stride, cudaStream_t s) {
+                        size_t split_stride, cudaStream_t s, bool w_tiled) {
   if (T <= 0) return cudaSuccess;
   if (K % 8 != 0) return cudaErrorInvalidValue;  // TMA row stride must be 16 B aligned
   if (splits < 1) splits = 1;
   if (splits > 1 && !out_f32) return cudaErrorInvalidValue;
   const Shape sh = shape_for(T, N);
-  const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.bn - 1) / sh.bn);
+  const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.unit_t - 1) / sh.unit_t);
   const int units = tiles * splits;
   const Plan pl{false, splits, units < sh.slots ? units : sh.slots, splits, 0};
-  return launch(sh, pl, X, W, out, T, N, K, out_f32, split_stride, s);
+  return launch(sh, pl, X, W, out, T, N, K, out_f32, split_stride, s, kEpiPlain, w_tiled);
 }
 
 cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, int N, int K, int max_slices,
-                              size_t split_stride, GemmParts* parts, cudaStream_t s) {
+                              size_t split_stride, GemmParts* parts, cudaStream_t s, bool w_tiled) {
   if (T <= 0) return cudaSuccess;
   if (K % 8 != 0 || max_slices < 1) return cudaErrorInvalidValue;
   const Shape sh = shape_for(T, N);
@@ -724,20 +894,21 @@ cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, i
   g.kbt = pl.balanced ? (K + kBK - 1) / kBK : 0;
   g.slots = pl.slots;
   g.rows = sh.rows;
-  g.bn = sh.bn;
-  g.n_tiles_t = (T + sh.bn - 1) / sh.bn;
+  g.bn = sh.unit_t;
+  g.n_tiles_t = (T + sh.unit_t - 1) / sh.unit_t;
   g.total = pl.balanced ? pl.total : 1;
   *parts = g;
-  return launch(sh, pl, X, W, out, T, N, K, true, g.stride, s);
+  return launch(sh, pl, X, W, out, T, N, K, true, g.stride, s, kEpiPlain, w_tiled);
 }
 
-cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N, int K, cudaStream_t s) {
+cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N, int K, cudaStream_t s,
+                             bool w_tiled) {
   if (T <= 0) return cudaSuccess;
   if (K % 8 != 0 || N % kBM != 0) return cudaErrorInvalidValue;  // whole gate|up groups per 128-row slab
   const Shape sh = shape_for(T, N, kXchgBytes);
-  const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.bn - 1) / sh.bn);
+  const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.unit_t - 1) / sh.unit_t);
   const Plan pl{false, 1, tiles < sh.slots ? tiles : sh.slots, 1, 0};
-  return launch(sh, pl, X, W, m, T, N, K, false, 0, s, kEpiSilu);
+  return launch(sh, pl, X, W, m, T, N, K, false, 0, s, kEpiSilu, w_tiled);
 }
 
 }  // namespace ppdk
