@@ -164,31 +164,15 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
  *   "gemm_sched"  -1 auto, 0 uniform K split, 1 balanced partition (fp32 path)
  *   "mlp_fused"    1 gate|up GEMM with the SiLU epilogue, 0 (default) fp32
  *                  partials + a separate SiLU kernel
- *   "gemm_diag"    timing probes only (outputs invalid): bit 0 skip activation
- *                  loads, bit 1 skip MMAs; bit 2 (valid outputs) records the
- *                  per-CTA timeline read by ppd_op_gemm_timeline
- *   "gemm_w_promo" L2 promotion of tiled weight boxes: 0 none, 1 128 B, 2 256 B
  *   "gemm_multi_sub" 1 (default): 257..512 token rows run as one unit of two
  *                  token sub-tiles per weight stage; 0: separate 256-row tiles
  *   "gemm_occ2"    -1 auto (<= 128 token rows), 0 off, 1 on: two co-resident
  *                  CTAs per SM with half-depth rings
- *   "gemm_wsplit"  1 (default) / 2 / 4 / 8 TMA sub-boxes per weight box
- *   "ops_w_tiled"  1: ppd_op_gemm_tc / _silu / _parts read B in the k-block
- *                  tiled layout of ppd_op_tile_matrix (the model's own weight
- *                  layout on the tcgen05 path), 0 (default) row-major
+ *   "attn_fused"   1 (default): a mixed decode + prefill step runs its
+ *                  attention as ONE launch (K2); 0: decode and prefill launches
  * Unknown names -> PPD_ERR_INVALID. Every change makes devices re-capture
  * their step graphs with the newly selected kernels. */
 int ppd_set_tuning(const char* name, int32_t value);
-/* row-major bf16 [N][K] -> the k-block tiled layout the device stores GEMM
- * weights in: 128-row x 64-column tiles of 16 KB, each contiguous, ordered
- * (row tile, k-block); element (n, k) at ((n/128)*(K/64) + k/64)*8192 +
- * (n%128)*64 + k%64. N % 128 == 0, K % 64 == 0. Asynchronous on `stream`. */
-int ppd_op_tile_matrix(const void* src, void* dst, int32_t N, int32_t K, void* stream);
-/* GEMM timing probe: per-CTA globaltimer timeline of the last tcgen05 GEMM
- * launched with tuning "gemm_diag" bit 2 set: out[cta*6 + i] = entry, setup
- * done, first stage consumed, last MMA issued, last epilogue done, exit (ns).
- * Returns the number of CTA rows written (<= max_ctas) or a negative status. */
-int ppd_op_gemm_timeline(uint64_t* out, int32_t max_ctas);
 /* deterministic random-init fill, identical to the oracle's mo_weight_bf16 */
 int ppd_op_fill_random(void* dst, uint64_t n, uint64_t seed, int32_t tensor, int32_t layer,
                        void* stream);

@@ -130,8 +130,6 @@ def load_lib(path: str = LIB_PATH, strict: bool = True):
         "ppd_op_gemm": [vp, vp, vp, i32, i32, i32, i32, vp],
         "ppd_op_gemm_tc": [vp, vp, vp, i32, i32, i32, i32, i32, vp],
         "ppd_op_fill_random": [vp, u64, u64, i32, i32, vp],
-        "ppd_op_tile_matrix": [vp, vp, i32, i32, vp],
-        "ppd_op_gemm_timeline": [vp, i32],
         "ppd_set_tuning": [ctypes.c_char_p, i32],
         "ppd_op_gemm_silu": [vp, vp, vp, i32, i32, i32, vp],
         "ppd_op_gemm_parts": [vp, vp, vp, i32, i32, i32, i32, P(GemmParts), vp],

@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include "attention_tc_body.cuh"
 #include "common.cuh"
 #include "kernels.h"
 
@@ -413,10 +414,12 @@ constexpr int kDecMaxG = 5;  // Llama-3 (4) and Qwen2.5 (5) groups; larger group
 constexpr int kDecSmem = 1024 + kStages * kStageBytes + kConsumerWarps * kDecMaxG * (kDh + 2) * 4 + 256;
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 2)
-    decode_attention_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+// One decode instance = 5 warps (warp 4 = TMA producer, warps 0-3 consumers)
+// over the segments of virtual CTA `vcta`, on `smem` (kDecSmemInst bytes,
+// 1024-aligned). bar_init (160 threads) / bar_cons (128 consumer threads) are
+// the instance's named barriers.
+PPD_DEV void decode_body(const CUtensorMap* kv_map, const AttnParams& p, uint8_t* smem, int vcta, int warp, int lane,
+                         int bar_init, int bar_cons) {
   uint8_t* stage_base = smem;
   float* mo = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [warp][G][Dh]
   float* mml = mo + kConsumerWarps * kDecMaxG * kDh;                    // [warp][G][2]
@@ -424,19 +427,17 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t* empty_bar = full_bar + kStages;
   int* flag = reinterpret_cast<int*>(empty_bar + kStages);
 
-  pdl_wait();
   const int G = p.group;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seg0 = p.seg_start[blockIdx.x], seg1 = p.seg_start[blockIdx.x + 1];
+  const int seg0 = p.seg_start[vcta], seg1 = p.seg_start[vcta + 1];
 
-  if (threadIdx.x == 0) {
+  if (warp == 0 && lane == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], kConsumerWarps);
     }
     fence_barrier_init();
   }
-  __syncthreads();
+  named_barrier_sync(bar_init, kThreads);
 
   if (warp == kConsumerWarps) {
     // the 16 boxes of a stage (4 blocks x K|V x two 64-dim halves): one lane each
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (lane < 16 && b < nb) {
           const int blk = btab[b0 + b];
           const int row = (((blk * p.n_layers + p.layer) * 2 + is_v) * p.n_kv_heads + kvh) * kBT;
-          tma_load_2d(stage_base + slot * kStageBytes + (b * 2 + is_v) * kBlockBytes + h * 2048, &kv_map, h * 64,
+          tma_load_2d(stage_base + slot * kStageBytes + (b * 2 + is_v) * kBlockBytes + h * 2048, kv_map, h * 64,
                       row, &full_bar[slot]);
         }
       }
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   // ---------------- consumer warps ----------------
   const int g8 = lane >> 2, t = lane & 3;
   const float sl2 = p.scale_log2;
-  const int tid = threadIdx.x;  // 0..127
+  const int tid = warp * 32 + lane;  // 0..127
   int g = 0;
   for (int sg = seg0; sg < seg1; ++sg) {
     const AttnItem it = p.items[sg];
@@ -582,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         mml[(warp * kDecMaxG + g8) * 2 + 1] = l0;
       }
     }
-    named_barrier_sync(1, kConsumerWarps * 32);
+    named_barrier_sync(bar_cons, kConsumerWarps * 32);
     const bool split = it.n_splits > 1;
     for (int r = 0; r < G; ++r) {
       float mm = -INFINITY;
@@ -607,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     if (split) {
       __threadfence();
-      named_barrier_sync(1, kConsumerWarps * 32);
+      named_barrier_sync(bar_cons, kConsumerWarps * 32);
       if (tid == 0) {
         int* ctr = p.counters + (size_t)s * p.n_kv_heads + kvh;
         const int prev = atomicAdd(ctr, 1);
@@ -615,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (last) *ctr = 0;
         *flag = last;
       }
-      named_barrier_sync(1, kConsumerWarps * 32);
+      named_barrier_sync(bar_cons, kConsumerWarps * 32);
       if (*flag) {
         __threadfence();
         const int ws0 = it.ws_index - it.split;
@@ -635,9 +636,87 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
-    named_barrier_sync(1, kConsumerWarps * 32);  // merge buffer / flag reused by the next segment
+    named_barrier_sync(bar_cons, kConsumerWarps * 32);  // merge buffer / flag reused by the next segment
   }
   pdl_trigger();
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    decode_attention_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  pdl_wait();
+  decode_body(&kv_map, p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31, 0, 1);
+}
+
+// ===========================================================================
+// K2: ONE launch for a mixed decode + (append-)prefill step.
+//
+// The first n_pf CTAs are tcgen05 prefill CTAs: warps 0-7 run the K3/K4 tile
+// (attention_tc_body.cuh) over tiles t = blockIdx.x, +n_pf, ... (tiles come
+// longest first), re-arming their mbarriers per tile; TMEM is allocated once.
+// Every other CTA runs TWO decode instances (warps 0-4 and 5-9, each its own
+// smem ring and named barriers) over the balanced decode schedule the host
+// cut for 2 x (gridDim.x - n_pf) virtual CTAs. HBM-bound decode streaming
+// and tensor-core-bound prefill tiles run concurrently on disjoint SMs of
+// the same launch, so the append prefill rides inside the decode step.
+// ===========================================================================
+namespace {
+constexpr int kMixThreads = 2 * kThreads;  // 320
+constexpr int kDecSmemInst = (kDecSmem - 1024 + 1023) / 1024 * 1024;
+constexpr int kMixSmem = pftc::kSmem > 1024 + 2 * kDecSmemInst ? pftc::kSmem : 1024 + 2 * kDecSmemInst;
+}  // namespace
+
+__global__ void __launch_bounds__(kMixThreads, 1)
+    mixed_attention_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p, const AttnItem* pf_items,
+                           int n_pf, int n_pf_tiles, int n_vcta) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if ((int)blockIdx.x < n_pf) {
+    if (warp >= 8) return;  // the prefill role uses 8 warps (named barrier 1, 256 threads)
+    const pftc::Smem S(smem);
+    if (threadIdx.x == 0) pftc::init_barriers(S, false);
+    if (warp == 2) tc::alloc(S.tmem_slot, pftc::kTmemCols);
+    tc::fence_before();
+    named_barrier_sync(1, pftc::kThreads);
+    tc::fence_after();
+    const uint32_t tmem = *S.tmem_slot;
+    for (int t = blockIdx.x; t < n_pf_tiles; t += n_pf) {
+      if (t != (int)blockIdx.x) {  // previous tile fully retired (its epilogue waited on o_done)
+        tc::fence_before();
+        named_barrier_sync(1, pftc::kThreads);
+        if (threadIdx.x == 0) pftc::init_barriers(S, true);
+        named_barrier_sync(1, pftc::kThreads);
+        tc::fence_after();
+      }
+      const AttnItem it = pf_items[t / p.n_kv_heads];
+      pftc::tile(&kv_map, p, S, it, t % p.n_kv_heads, tmem, warp, lane, t + n_pf >= n_pf_tiles);
+    }
+    tc::fence_before();
+    named_barrier_sync(1, pftc::kThreads);
+    if (warp == 2) tc::dealloc(tmem, pftc::kTmemCols);
+    return;
+  }
+  const int inst = threadIdx.x / kThreads;
+  const int vcta = ((int)blockIdx.x - n_pf) * 2 + inst;
+  if (vcta >= n_vcta) return;
+  const int lt = threadIdx.x - inst * kThreads;
+  decode_body(&kv_map, p, smem + inst * kDecSmemInst, vcta, lt >> 5, lt & 31, 2 + inst, 4 + inst);
+}
+
+cudaError_t launch_mixed_attention(const void* kv_map, const AttnParams& p, const AttnItem* pf_items, int n_pf,
+                                   int n_pf_tiles, int n_vcta, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(mixed_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMixSmem);
+    attr = true;
+  }
+  if (p.group > kDecMaxG || n_pf <= 0 || n_pf > n_pf_tiles) return cudaErrorInvalidValue;
+  const int grid = n_pf + (n_vcta + 1) / 2;
+  return launch_pdl(mixed_attention_kernel, dim3(grid), dim3(kMixThreads), kMixSmem, stream,
+                    *reinterpret_cast<const CUtensorMap*>(kv_map), p, pf_items, n_pf, n_pf_tiles, n_vcta);
 }
 
 cudaError_t launch_decode_attention(const void* kv_map, const AttnParams& p, int n_cta, int group,

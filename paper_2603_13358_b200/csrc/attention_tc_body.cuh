@@ -1,0 +1,292 @@
+// attention_tc_body.cuh — the K3/K4 tcgen05 prefill tile (full / append
+// prefill attention over the paged pool), shared by the standalone kernel
+// (attention_tc.cu, one CTA per tile) and the fused mixed decode + prefill
+// launch (attention.cu, mixed_attention_kernel: prefill CTAs loop over tiles).
+// See attention_tc.cu for the warp roles.
+#pragma once
+#include <cuda.h>
+
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace ppdk {
+namespace pftc {
+
+constexpr int kThreads = 256;
+constexpr int kBT = 16;
+constexpr int kDh = 128;
+constexpr int kKeys = 128;                  // keys per block
+constexpr int kTile = 32768;                // 128 x 128 bf16
+constexpr int kKStages = 3;                 // K ring: released as soon as S_j retires
+constexpr int kVStages = 2;                 // V ring: released after PV_j
+constexpr int kSmem = 1024 + kTile /*Q*/ + (kKStages + kVStages) * kTile + kTile /*P*/ + 256;
+constexpr uint32_t kTmemCols = 512;
+constexpr float kRescaleThreshold = 8.0f;   // log2 domain
+constexpr int kNumBars = 15;
+
+PPD_DEV float ex2_sfu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 2^x = 2^floor(x) * p(frac(x)), p a minimax cubic on [0, 1) with p(0) = 1
+PPD_DEV float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);  // -inf (masked keys) -> ~0
+  const float fi = floorf(x);
+  const float f = x - fi;
+  const float p = fmaf(fmaf(fmaf(0.07706209f, f, 0.22765041f), f, 0.69511558f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float2int_rn(fi) << 23));
+}
+
+// shared-memory carve-up of one prefill CTA (smem 1024-byte aligned)
+struct Smem {
+  uint8_t *q_s, *k_s, *v_s, *p_s;
+  uint64_t *bars, *k_full, *k_empty, *v_full, *v_empty, *s_full, *p_ready, *o_done, *q_ready;
+  uint32_t* tmem_slot;
+  PPD_DEV explicit Smem(uint8_t* smem) {
+    q_s = smem;
+    k_s = smem + kTile;              // [kKStages]
+    v_s = k_s + kKStages * kTile;    // [kVStages]
+    p_s = v_s + kVStages * kTile;
+    bars = reinterpret_cast<uint64_t*>(p_s + kTile);
+    k_full = bars;        // [3]
+    k_empty = bars + 3;   // [3]
+    v_full = bars + 6;    // [2]
+    v_empty = bars + 8;   // [2]
+    s_full = bars + 10;   // [2]
+    p_ready = bars + 12;
+    o_done = bars + 13;
+    q_ready = bars + 14;
+    tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
+  }
+};
+
+// one thread: (re)initialise the tile's mbarriers
+PPD_DEV void init_barriers(const Smem& S, bool reinit) {
+  if (reinit)
+    for (int i = 0; i < kNumBars; ++i)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(S.bars + i)) : "memory");
+  for (int i = 0; i < kKStages; ++i) {
+    mbar_init(&S.k_full[i], 1);
+    mbar_init(&S.k_empty[i], 1);
+  }
+  for (int i = 0; i < kVStages; ++i) {
+    mbar_init(&S.v_full[i], 1);
+    mbar_init(&S.v_empty[i], 1);
+  }
+  for (int i = 0; i < 2; ++i) mbar_init(&S.s_full[i], 1);
+  mbar_init(S.p_ready, 4);
+  mbar_init(S.o_done, 1);
+  mbar_init(S.q_ready, 4);
+  fence_barrier_init();
+}
+
+// One 128-row tile (128/G query tokens x the G query heads of kv head `kvh`)
+// of prefill item `it`, run by warps 0..7 of the calling CTA. Barriers are
+// freshly initialised; `tmem` holds kTmemCols columns (S0 | S1 | O).
+PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S, const AttnItem& it, int kvh,
+                  uint32_t tmem, int warp, int lane, bool trigger_pdl) {
+  uint8_t* q_s = S.q_s;
+  uint8_t* k_s = S.k_s;
+  uint8_t* v_s = S.v_s;
+  uint8_t* p_s = S.p_s;
+  uint64_t* k_full = S.k_full;
+  uint64_t* k_empty = S.k_empty;
+  uint64_t* v_full = S.v_full;
+  uint64_t* v_empty = S.v_empty;
+  uint64_t* s_full = S.s_full;
+  uint64_t* p_ready = S.p_ready;
+  uint64_t* o_done = S.o_done;
+  uint64_t* q_ready = S.q_ready;
+  const int G = p.group;
+  const int s = it.seq;
+  const int ctx = p.ctx[s];
+  const int q_base = p.q_start[s];
+  const int rows = it.n_q * G;
+  const int key_end = ctx + it.q_tok0 + it.n_q;
+  const int nblk = (key_end + kKeys - 1) / kKeys;
+  const int* btab = p.block_tables + (size_t)s * p.max_blocks;
+
+  const uint32_t t_o = tmem + 2 * kKeys;
+
+  if (warp == 0 || warp == 3) {
+    // warp 0 streams K, warp 3 streams V; the 16 TMA boxes of a 128-key tile
+    // (8 paged blocks x two 64-dim halves) are issued by 16 lanes in parallel.
+    const bool is_v = warp == 3;
+    const int n_st = is_v ? kVStages : kKStages;
+    uint64_t* fullb = is_v ? v_full : k_full;
+    uint64_t* emptyb = is_v ? v_empty : k_empty;
+    uint8_t* ring = is_v ? v_s : k_s;
+    const int last_blk = (key_end - 1) / kBT;
+    const int b = (lane >> 1) & 7, h = lane & 1;
+    for (int j = 0; j < nblk; ++j) {
+      const int st = j % n_st;
+      if (j >= n_st) mbar_wait(&emptyb[st], ((j / n_st) - 1) & 1);
+      if (lane == 0) mbar_arrive_expect_tx(&fullb[st], kTile);
+      __syncwarp();
+      if (lane < 16) {
+        // slots past the sequence re-load its last block: finite data, masked to p = 0
+        const int pb = min(j * (kKeys / kBT) + b, last_blk);
+        const int blk = btab[pb];
+        const int row = (((blk * p.n_layers + p.layer) * 2 + (is_v ? 1 : 0)) * p.n_kv_heads + kvh) * kBT;
+        tc::tma_load_2d(ring + st * kTile + h * (kTile / 2) + b * 2048, kv_map, h * 64, row, &fullb[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = tc::idesc_bf16(128, kKeys, false);
+      const uint32_t id_o = tc::idesc_bf16(128, kDh, true);
+      mbar_wait(q_ready, 0);
+      tc::fence_after();
+      const uint32_t qa = smem_u32(q_s), pa = smem_u32(p_s);
+      for (int j = 0; j <= nblk; ++j) {
+        if (j < nblk) {
+          const int st = j % kKStages;
+          mbar_wait(&k_full[st], (j / kKStages) & 1);
+          tc::fence_after();
+          const uint32_t ka = smem_u32(k_s + st * kTile);
+#pragma unroll
+          for (int kk = 0; kk < kDh / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+            tc::mma_bf16_ss(tmem + (j & 1) * kKeys, tc::desc_kmajor_sw128(qa + off), tc::desc_kmajor_sw128(ka + off),
+                            id_s, kk > 0);
+          }
+          tc::commit(&s_full[j & 1]);
+          tc::commit(&k_empty[st]);  // K tile free once S_j retires
+        }
+        if (j >= 1) {
+          const int jj = j - 1, st = jj % kVStages;
+          mbar_wait(p_ready, jj & 1);
+          mbar_wait(&v_full[st], (jj / kVStages) & 1);
+          tc::fence_after();
+          const uint32_t va = smem_u32(v_s + st * kTile);
+#pragma unroll
+          for (int kk = 0; kk < kKeys / 16; ++kk) {
+            const uint32_t poff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+            tc::mma_bf16_ss(t_o, tc::desc_kmajor_sw128(pa + poff), tc::desc_mnmajor_sw128(va + kk * 2048, kTile / 2),
+                            id_o, (jj > 0) || (kk > 0));
+          }
+          tc::commit(o_done);
+          tc::commit(&v_empty[st]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int r = warp * 32 + lane - 128;  // query row == TMEM lane
+    const int q4 = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    // ---- Q row -> shared (K-major, 128 B swizzle, two 64-dim atoms)
+    {
+      const uint4* src = nullptr;
+      if (r < rows)
+        src = reinterpret_cast<const uint4*>(p.q + ((size_t)(q_base + it.q_tok0 + r / G) * p.n_q_heads + kvh * G + r % G) * kDh);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const uint4 v = src ? src[c] : make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(q_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_ready);
+    }
+    const int pos = r < rows ? ctx + it.q_tok0 + r / G : -1;
+    const float sl2 = p.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc::fence_after();
+      // one warp per SM sub-partition runs this: keep every reduction chain
+      // short (8 independent partial max / sum accumulators) and the four
+      // TMEM loads in flight together
+      uint32_t raw[kKeys];
+#pragma unroll
+      for (int c0 = 0; c0 < kKeys; c0 += 32) tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + c0, raw + c0);
+      tc::wait_ld();
+      float sv[kKeys];
+      const int key0 = j * kKeys;
+      float mxp[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mxp[i] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kKeys; ++c) {
+        sv[c] = (key0 + c <= pos) ? __uint_as_float(raw[c]) * sl2 : -INFINITY;
+        mxp[c & 7] = fmaxf(mxp[c & 7], sv[c]);
+      }
+      const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+      float alpha = 1.f;
+      bool rescale = false;
+      if (m == -INFINITY) {
+        m = mx;  // first keys this row sees (O holds zeros for it so far)
+      } else if (mx > m + kRescaleThreshold) {
+        alpha = exp2f(m - mx);
+        m = mx;
+        rescale = true;
+      }
+      const float base = m == -INFINITY ? 0.f : m;
+      // exp2 on two pipes: even keys on the SFU (ex2.approx), odd keys by a
+      // degree-3 polynomial on the FMA pipe (max rel. error 8.6e-5 << bf16 ulp)
+      float rsp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[kKeys / 2];
+#pragma unroll
+      for (int c = 0; c < kKeys; c += 2) {
+        const float p0 = ex2_sfu(sv[c] - base), p1 = ex2_poly(sv[c + 1] - base);
+        rsp[(c >> 1) & 7] += p0 + p1;
+        pk[c >> 1] = pack2(p0, p1);
+      }
+      const float rs = ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
+      // P_{j-1} and O must have been consumed by PV_{j-1} before we overwrite / rescale
+      if (j >= 1) {
+        mbar_wait(o_done, (j - 1) & 1);
+        tc::fence_after();
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const uint4 v = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+        *reinterpret_cast<uint4*>(p_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+      }
+      if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c0 = 0; c0 < kDh; c0 += 32) {
+          uint32_t o[32];
+          tc::ld32x32(t_o + lane_base + c0, o);
+          tc::wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+          tc::st32x32(t_o + lane_base + c0, o);
+        }
+        tc::wait_st();
+      }
+      l = l * alpha + rs;
+      fence_proxy_async();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_ready);
+    }
+    // ---- epilogue: O / l -> bf16
+    if (trigger_pdl) pdl_trigger();
+    mbar_wait(o_done, (nblk - 1) & 1);
+    tc::fence_after();
+    const float inv = 1.f / l;
+    bf16* dst = r < rows ? p.out + ((size_t)(q_base + it.q_tok0 + r / G) * p.n_q_heads + kvh * G + r % G) * kDh
+                         : nullptr;
+#pragma unroll
+    for (int c0 = 0; c0 < kDh; c0 += 32) {
+      uint32_t o[32];
+      tc::ld32x32(t_o + lane_base + c0, o);
+      tc::wait_ld();
+      if (dst) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 8) {
+          float f[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(o[c + e]) * inv;
+          *reinterpret_cast<uint4*>(dst + c0 + c) = pack8(f);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace pftc
+}  // namespace ppdk

@@ -58,8 +58,6 @@ int g_tuning_epoch = 0;
 // Off by default: step-level A/B (tools/ab_step.py, 48 steps per arm) shows
 // no gain over the balanced-partition GEMM + silu_mul_kernel (within 1%).
 bool g_mlp_fused = false;
-bool g_ops_w_tiled = false;
-int g_gemm_diag = 0, g_gemm_promo = 2;  // ppd_op_gemm_tc/_silu/_parts: B is k-block tiled (ppd_op_tile_matrix)
 // diagnostics only ("diag_skip" knob): skip kernel classes of the forward step
 // (1 small ops, 2 attention, 4 GEMMs) to time their marginal cost in the live
 // graph. Results are meaningless while set.
@@ -102,7 +100,6 @@ struct ppd_dev {
   bf16 *embed = nullptr, *lm_head = nullptr, *ones = nullptr;
   std::vector<Layer> layers;
   bool weights_ready = false;
-  bool w_tiled = false;  // GEMM weights stored k-block tiled (ppd_load_random_weights)
   float *rope_cos = nullptr, *rope_sin = nullptr;
   // KV pool
   bf16* kv = nullptr;
@@ -142,6 +139,7 @@ namespace {
 // ------------------------------------------------------------ metadata
 struct StepLayout {
   int n, T, maxb, n_out, n_items, n_ws, n_dec, n_cta;
+  int n_pf;  // K2: prefill CTAs of the one-launch mixed attention (0 = not a mixed step)
   size_t off_seg;
   double attn_bytes;  // algorithmic bytes of one attention launch (one layer)
   size_t off_qstart, off_ctx, off_tokens, off_bt, off_rowseq, off_rowpos, off_outrows, off_items,
@@ -234,8 +232,8 @@ bool decode_persistent_enabled(int group) {
 // the split workspace. Replaces the decode items of `items` (kept first) and
 // fills seg_start[n_cta + 1].
 void balance_decode(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads, std::vector<AttnItem>& items,
-                    int& n_ws, int& n_dec, std::vector<int>& seg_start) {
-  constexpr int kStageKeys = 64, kMaxCtas = 148 * 2;
+                    int& n_ws, int& n_dec, std::vector<int>& seg_start, int kMaxCtas = 148 * 2) {
+  constexpr int kStageKeys = 64;
   long U = 0;
   for (int s = 0; s < n; ++s)
     if (q_len[s] == 1) U += (long)((ctx[s] + 1 + kStageKeys - 1) / kStageKeys) * n_kv_heads;
@@ -291,6 +289,65 @@ void balance_decode(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_he
   }
   n_dec = (int)items.size();
   items.insert(items.end(), rest.begin(), rest.end());
+}
+
+// K2 split of the 148 SMs for a mixed decode + prefill step (one launch,
+// mixed_attention_kernel): n_pf SMs run the prefill tiles, the rest two
+// decode instances each. Cost model (B200 measurements of the standalone
+// kernels): decode streams its K/V at min(5.6 TB/s, 44 GB/s per SM); a prefill
+// tile costs ~3 us per 128-key block on one SM (QK^T + PV at ~400 TF/s chip
+// wide). Picks n_pf minimising the later finisher; tiles are dealt round robin
+// longest first. Returns 0 (no fusion) when either side is empty.
+int plan_mixed_split(double dec_bytes, const std::vector<double>& tile_cost) {
+  const int n_tiles = (int)tile_cost.size();
+  if (dec_bytes <= 0 || n_tiles == 0) return 0;
+  int best = 1;
+  double best_t = 1e30;
+  for (int n_pf = 1; n_pf <= std::min(n_tiles, 146); ++n_pf) {
+    double t_pf = 0;
+    for (int c = 0; c < n_pf; ++c) {
+      double t = 0;
+      for (int i = c; i < n_tiles; i += n_pf) t += tile_cost[i];
+      t_pf = std::max(t_pf, t);
+    }
+    const double bw = std::min(5.6e12, (148 - n_pf) * 44e9);
+    const double t = std::max(t_pf, dec_bytes / bw);
+    if (t < best_t * 0.999) {
+      best_t = t;
+      best = n_pf;
+    }
+  }
+  return best;
+}
+
+bool g_attn_fused = true;  // tuning "attn_fused": K2 one-launch mixed attention
+
+// The attention work of one step: decode items (balanced schedule), prefill
+// tiles (longest first) and, for a mixed step, the K2 SM split n_pf.
+void plan_attention(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads, int G,
+                    std::vector<AttnItem>& items, int& n_ws, int& n_dec, std::vector<int>& seg_start, int& n_pf) {
+  build_items(n, q_len, ctx, n_kv_heads, G, items, n_ws, n_dec);
+  seg_start.clear();
+  n_pf = 0;
+  if (!decode_persistent_enabled(G)) return;
+  if (attention_tc_enabled() && g_attn_fused && n_dec > 0 && (int)items.size() > n_dec) {
+    // longest prefill tiles first (round-robin dealing in mixed_attention_kernel)
+    std::stable_sort(items.begin() + n_dec, items.end(), [&](const AttnItem& a, const AttnItem& b) {
+      return ctx[a.seq] + a.q_tok0 + a.n_q > ctx[b.seq] + b.q_tok0 + b.n_q;
+    });
+    std::vector<double> cost;
+    for (size_t i = n_dec; i < items.size(); ++i) {
+      const AttnItem& it = items[i];
+      const double blocks = (ctx[it.seq] + it.q_tok0 + it.n_q + 127) / 128;
+      for (int h = 0; h < n_kv_heads; ++h) cost.push_back(3.0e-6 * blocks);
+    }
+    double dec_bytes = 0;
+    for (int s = 0; s < n; ++s)
+      if (q_len[s] == 1) dec_bytes += (double)(ctx[s] + 1) * n_kv_heads * 2 * 128 * 2;
+    n_pf = plan_mixed_split(dec_bytes, cost);
+  }
+  balance_decode(n, q_len, ctx, n_kv_heads, items, n_ws, n_dec, seg_start, n_pf > 0 ? 2 * (148 - n_pf) : 296);
+  if (seg_start.empty()) n_pf = 0;
 }
 
 void clear_graphs(ppd_dev* d) {
@@ -366,10 +423,8 @@ int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnIt
   for (int i = 0; i < L.T; ++i)
     CHECK_ARG(b->tokens[i] >= 0 && b->tokens[i] < d->cfg.vocab, "batch: token id out of range");
   const int G = d->cfg.n_q_heads / d->cfg.n_kv_heads;
-  build_items(L.n, b->q_len, b->ctx, d->cfg.n_kv_heads, G, items, L.n_ws, L.n_dec);
   std::vector<int> seg_start;
-  if (decode_persistent_enabled(G))
-    balance_decode(L.n, b->q_len, b->ctx, d->cfg.n_kv_heads, items, L.n_ws, L.n_dec, seg_start);
+  plan_attention(L.n, b->q_len, b->ctx, d->cfg.n_kv_heads, G, items, L.n_ws, L.n_dec, seg_start, L.n_pf);
   L.n_cta = seg_start.empty() ? 0 : (int)seg_start.size() - 1;
   L.n_items = (int)items.size();
   size_t o = 0;
@@ -417,7 +472,7 @@ int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnIt
 
 int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf16* out,
                   const int* d_qstart, const int* d_ctx, const int* d_bt, int maxb,
-                  const AttnItem* d_items, int n_dec, int n_items, const int* d_seg, int n_cta, int layer,
+                  const AttnItem* d_items, int n_dec, int n_items, const int* d_seg, int n_cta, int n_pf, int layer,
                   float* ws_o, float* ws_ml, int* counters, cudaStream_t s) {
   AttnParams p{};
   p.seg_start = d_seg;
@@ -437,6 +492,11 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   p.ws_o = ws_o;
   p.ws_ml = ws_ml;
   p.counters = counters;
+  // K2: a mixed step is ONE launch (prefill CTAs + decode CTAs)
+  if (n_pf > 0) {
+    CU(launch_mixed_attention(kv_map, p, d_items + n_dec, n_pf, (n_items - n_dec) * c.n_kv_heads, n_cta, s));
+    return PPD_OK;
+  }
   // decode rows: the balanced persistent kernel (n_cta > 0) or one CTA per item
   if (n_cta > 0) {
     CU(launch_decode_attention(kv_map, p, n_cta, p.group, s));
@@ -522,7 +582,7 @@ int forward(ppd_dev* d, const StepLayout& L) {
                             l, d->bt, s));
     PROF(0, false);
     int rc = (g_diag_skip & 2) ? 0 : run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items,
-                           at<int>(m, L.off_seg), L.n_cta, l, d->ws_o, d->ws_ml, d->counters, s);
+                           at<int>(m, L.off_seg), L.n_cta, L.n_pf, l, d->ws_o, d->ws_ml, d->counters, s);
     if (rc) return rc;
     PROF(0, true);
     PROF(1, false);
@@ -701,16 +761,8 @@ int ppd_load_random_weights(ppd_dev* d, uint64_t seed) {
   d->embed = reinterpret_cast<bf16*>(take(V * dm * 2));
   d->lm_head = reinterpret_cast<bf16*>(take(V * dm * 2));
   d->ones = reinterpret_cast<bf16*>(take(dm * 2));
-  // GEMM weights are stored k-block tiled for the tcgen05 path (one contiguous
-  // 16 KB HBM run per TMA box: the decode step streams them at full DRAM
-  // efficiency); row-major for the cuBLAS reference path
-  const bool tiled = gemm_uses_tcgen05(d->gemm) && (qd + 2 * kd) % 128 == 0 && dm % 128 == 0 &&
-                     (2 * F) % 128 == 0 && V % 128 == 0 && dm % 64 == 0 && qd % 64 == 0 && F % 64 == 0;
-  gemm_set_weights_tiled(d->gemm, tiled);
-  d->w_tiled = tiled;
-  const int ti = tiled ? 1 : 0;
   CU(launch_fill_random(d->embed, V * dm, seed, 0, 0, s));
-  CU(launch_fill_matrix(d->lm_head, V, dm, seed, 8, 0, ti, s));
+  CU(launch_fill_matrix(d->lm_head, V, dm, seed, 8, 0, s));
   CU(launch_fill_const(d->ones, dm, 1.0f, s));
   d->layers.assign(c.n_layers, Layer{});
   for (int l = 0; l < c.n_layers; ++l) {
@@ -721,10 +773,10 @@ int ppd_load_random_weights(ppd_dev* d, uint64_t seed) {
     w.wdown = reinterpret_cast<bf16*>(take(dm * F * 2));
     float* b = reinterpret_cast<float*>(take((qd + 2 * kd) * 4));
     w.bqkv = c.qkv_bias ? b : nullptr;
-    CU(launch_fill_qkv(w.wqkv, (int)qd, (int)kd, (int)dm, seed, l, ti, s));
-    CU(launch_fill_matrix(w.wo, dm, qd, seed, 4, l, ti, s));
-    CU(launch_fill_gate_up(w.wgu, (int)F, (int)dm, seed, l, ti, s));
-    CU(launch_fill_matrix(w.wdown, dm, F, seed, 7, l, ti, s));
+    CU(launch_fill_qkv(w.wqkv, (int)qd, (int)kd, (int)dm, seed, l, s));
+    CU(launch_fill_matrix(w.wo, dm, qd, seed, 4, l, s));
+    CU(launch_fill_gate_up(w.wgu, (int)F, (int)dm, seed, l, s));
+    CU(launch_fill_matrix(w.wdown, dm, F, seed, 7, l, s));
     if (c.qkv_bias) CU(launch_fill_bias(w.bqkv, (int)qd, (int)kd, seed, l, s));
   }
   CU(cudaStreamSynchronize(s));
@@ -774,7 +826,8 @@ int ppd_step_submit(ppd_dev* d, const ppd_batch* b) {
   CU(cudaEventRecord(d->ev0, d->compute));
   // repeated shapes replay a captured graph (decode steps: ~300 launches -> 1)
   // every launch parameter of forward() is a function of these (grids: items, n_dec, n_cta)
-  const auto key = std::make_tuple(L.n, L.T, L.maxb, L.n_out, L.n_items * 4096 + L.n_dec, L.n_ws * 8192 + L.n_cta);
+  const auto key = std::make_tuple(L.n, L.T, L.maxb, L.n_out, L.n_items * 4096 + L.n_dec,
+                                   (L.n_ws * 8192 + L.n_cta) * 256 + L.n_pf);
   if (d->tuning_epoch != g_tuning_epoch) {  // kernels chosen at capture time changed
     clear_graphs(d);
     d->tuning_epoch = g_tuning_epoch;
@@ -957,9 +1010,9 @@ int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_poo
   std::vector<AttnItem> items;
   int n_ws = 0;
   int n_dec = 0;
-  build_items(n_seqs, qlen.data(), ctx, cfg->n_kv_heads, G, items, n_ws, n_dec);
   std::vector<int> seg_start;
-  if (decode_persistent_enabled(G)) balance_decode(n_seqs, qlen.data(), ctx, cfg->n_kv_heads, items, n_ws, n_dec, seg_start);
+  int n_pf = 0;
+  plan_attention(n_seqs, qlen.data(), ctx, cfg->n_kv_heads, G, items, n_ws, n_dec, seg_start, n_pf);
   const int n_cta = seg_start.empty() ? 0 : (int)seg_start.size() - 1;
   alignas(128) uint8_t map[128];
   uint64_t rows = (uint64_t)num_blocks * cfg->n_layers * 2 * cfg->n_kv_heads * block_tokens;
@@ -985,7 +1038,7 @@ int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_poo
   int* d_seg = reinterpret_cast<int*>(d_items + items.size());
   if (!seg_start.empty()) CU(cudaMemcpy(d_seg, seg_start.data(), seg_start.size() * 4, cudaMemcpyHostToDevice));
   rc = run_attention(*cfg, map, static_cast<const bf16*>(q), static_cast<bf16*>(out), d_qs, d_ctx,
-                     d_bt, max_blocks, d_items, n_dec, (int)items.size(), d_seg, n_cta, layer, ws_o, ws_ml, ctr, s);
+                     d_bt, max_blocks, d_items, n_dec, (int)items.size(), d_seg, n_cta, n_pf, layer, ws_o, ws_ml, ctr, s);
   cudaStreamSynchronize(s);
   cudaFree(dm);
   cudaFree(ws_o);
@@ -1013,7 +1066,7 @@ int ppd_op_gemm_tc(const void* A, const void* B, void* C, int32_t M, int32_t N, 
   CHECK_ARG(K % 8 == 0, "K must be a multiple of 8");
   CHECK_ARG(splits == 1 || out_f32, "K-split partials need fp32 output");
   CU(gemm_tc_run(static_cast<const bf16*>(A), static_cast<const bf16*>(B), C, M, N, K, out_f32 != 0, splits,
-                 (size_t)M * N, static_cast<cudaStream_t>(stream), g_ops_w_tiled));
+                 (size_t)M * N, static_cast<cudaStream_t>(stream)));
   return PPD_OK;
 }
 
@@ -1021,7 +1074,7 @@ int ppd_op_gemm_silu(const void* A, const void* B, void* m, int32_t M, int32_t N
   CHECK_ARG(A && B && m && M > 0 && N > 0 && K > 0, "bad gemm args");
   CHECK_ARG(K % 8 == 0 && N % 128 == 0, "K must be a multiple of 8 and N of 128");
   CU(gemm_tc_run_silu(static_cast<const bf16*>(A), static_cast<const bf16*>(B), static_cast<bf16*>(m), M, N, K,
-                      static_cast<cudaStream_t>(stream), g_ops_w_tiled));
+                      static_cast<cudaStream_t>(stream)));
   return PPD_OK;
 }
 
@@ -1031,7 +1084,7 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
   CHECK_ARG(K % 8 == 0, "K must be a multiple of 8");
   GemmParts g;
   CU(gemm_tc_run_parts(static_cast<const bf16*>(A), static_cast<const bf16*>(B), static_cast<float*>(C), M, N, K,
-                       max_slices, (size_t)M * N, &g, static_cast<cudaStream_t>(stream), g_ops_w_tiled));
+                       max_slices, (size_t)M * N, &g, static_cast<cudaStream_t>(stream)));
   parts->n = g.n;
   parts->kbt = g.kbt;
   parts->slots = g.slots;
@@ -1058,26 +1111,15 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "diag_skip") == 0) {
     CHECK_ARG(value >= 0 && value <= 7, "diag_skip must be in [0, 7]");
     g_diag_skip = value;
-  } else if (std::strcmp(name, "gemm_diag") == 0) {
-    CHECK_ARG(value >= 0 && value <= 7, "gemm_diag must be in [0, 7]");
-    g_gemm_diag = value;
-    gemm_tc_set_diag(g_gemm_diag, g_gemm_promo);
-  } else if (std::strcmp(name, "gemm_w_promo") == 0) {
-    CHECK_ARG(value >= 0 && value <= 2, "gemm_w_promo must be in [0, 2]");
-    g_gemm_promo = value;
-    gemm_tc_set_diag(g_gemm_diag, g_gemm_promo);
-  } else if (std::strcmp(name, "gemm_wsplit") == 0) {
-    CHECK_ARG(value == 1 || value == 2 || value == 4 || value == 8, "gemm_wsplit must be 1, 2, 4 or 8");
-    gemm_tc_set_w_split(value);
+  } else if (std::strcmp(name, "attn_fused") == 0) {
+    CHECK_ARG(value == 0 || value == 1, "attn_fused must be 0 or 1");
+    g_attn_fused = value != 0;
   } else if (std::strcmp(name, "gemm_occ2") == 0) {
     CHECK_ARG(value >= -1 && value <= 1, "gemm_occ2 must be -1, 0 or 1");
     gemm_tc_set_occ2(value);
   } else if (std::strcmp(name, "gemm_multi_sub") == 0) {
     CHECK_ARG(value == 0 || value == 1, "gemm_multi_sub must be 0 or 1");
     gemm_tc_set_multi_sub(value != 0);
-  } else if (std::strcmp(name, "ops_w_tiled") == 0) {
-    CHECK_ARG(value == 0 || value == 1, "ops_w_tiled must be 0 or 1");
-    g_ops_w_tiled = value != 0;
   } else if (std::strcmp(name, "mlp_fused") == 0) {
     CHECK_ARG(value == 0 || value == 1, "mlp_fused must be 0 or 1");
     g_mlp_fused = value != 0;
@@ -1086,21 +1128,6 @@ int ppd_set_tuning(const char* name, int32_t value) {
   }
   gemm_tc_set_tuning(pair, stages, sched);
   ++g_tuning_epoch;
-  return PPD_OK;
-}
-
-int ppd_op_gemm_timeline(uint64_t* out, int32_t max_ctas) {
-  CHECK_ARG(out && max_ctas > 0, "bad timeline args");
-  const int n = gemm_tc_read_timeline(reinterpret_cast<unsigned long long*>(out), max_ctas);
-  if (n < 0) return fail(PPD_ERR_CUDA, "timeline read");
-  return n;
-}
-
-int ppd_op_tile_matrix(const void* src, void* dst, int32_t N, int32_t K, void* stream) {
-  CHECK_ARG(src && dst && N > 0 && K > 0, "bad tile args");
-  CHECK_ARG(N % 128 == 0 && K % 64 == 0, "tiled layout needs N % 128 == 0 and K % 64 == 0");
-  CU(launch_tile_matrix(static_cast<const bf16*>(src), static_cast<bf16*>(dst), (uint64_t)N, (uint64_t)K,
-                        static_cast<cudaStream_t>(stream)));
   return PPD_OK;
 }
 

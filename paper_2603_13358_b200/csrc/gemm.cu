@@ -14,7 +14,6 @@ namespace ppdk {
 struct GemmContext {
   cublasHandle_t handle = nullptr;
   bool tc = true;
-  bool w_tiled = false;
 };
 
 GemmContext* gemm_create() {
@@ -35,7 +34,6 @@ void gemm_destroy(GemmContext* c) {
 }
 
 bool gemm_uses_tcgen05(const GemmContext* c) { return c && c->tc; }
-void gemm_set_weights_tiled(GemmContext* c, bool tiled) { c->w_tiled = tiled && c->tc; }
 
 cudaError_t gemm_run_cublas(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N,
                             int K, bool out_f32, cudaStream_t s) {
@@ -52,7 +50,7 @@ cudaError_t gemm_run_cublas(GemmContext* c, const __nv_bfloat16* A, const __nv_b
 cudaError_t gemm_run(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N, int K,
                      bool out_f32, cudaStream_t s) {
   if (!c->tc) return gemm_run_cublas(c, A, B, C, M, N, K, out_f32, s);
-  return gemm_tc_run(A, B, C, M, N, K, out_f32, 1, 0, s, c->w_tiled);
+  return gemm_tc_run(A, B, C, M, N, K, out_f32, 1, 0, s);
 }
 
 cudaError_t gemm_run_split(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, float* C, int M, int N,
@@ -62,13 +60,13 @@ cudaError_t gemm_run_split(GemmContext* c, const __nv_bfloat16* A, const __nv_bf
     parts->stride = (size_t)M * N;
     return gemm_run_cublas(c, A, B, C, M, N, K, true, s);
   }
-  return gemm_tc_run_parts(A, B, C, M, N, K, max_slices, (size_t)M * N, parts, s, c->w_tiled);
+  return gemm_tc_run_parts(A, B, C, M, N, K, max_slices, (size_t)M * N, parts, s);
 }
 
 cudaError_t gemm_run_silu(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, __nv_bfloat16* m,
                           float* scratch, int M, int N, int K, cudaStream_t s) {
   if (M == 0) return cudaSuccess;
-  if (c->tc) return gemm_tc_run_silu(A, B, m, M, N, K, s, c->w_tiled);
+  if (c->tc) return gemm_tc_run_silu(A, B, m, M, N, K, s);
   cudaError_t e = gemm_run_cublas(c, A, B, scratch, M, N, K, true, s);
   if (e != cudaSuccess) return e;
   GemmParts one;

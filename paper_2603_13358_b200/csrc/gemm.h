@@ -13,9 +13,6 @@ struct GemmContext;
 GemmContext* gemm_create();
 void gemm_destroy(GemmContext* ctx);
 bool gemm_uses_tcgen05(const GemmContext* ctx);
-// the B (weight) operands of this context's model are stored k-block tiled
-// (tcgen05 path only; ops.cu phys_to_rc)
-void gemm_set_weights_tiled(GemmContext* ctx, bool tiled);
 // single-slice product (no K split)
 cudaError_t gemm_run(GemmContext* ctx, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N,
                      int K, bool out_f32, cudaStream_t s);

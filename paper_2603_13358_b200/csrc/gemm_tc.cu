@@ -50,15 +50,6 @@ PPD_DEV void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint6
       : "memory");
 }
 
-// one 16 KB k-block tile of a k-block-tiled weight (3-D map: 64 x 128 x tiles)
-PPD_DEV void tma_load_tile(void* smem, const CUtensorMap* map, int y, int tile, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(tile), "r"(smem_u32(bar))
-      : "memory");
-}
-
 PPD_DEV uint64_t sw128_kmajor_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);   // start address
@@ -121,13 +112,6 @@ PPD_DEV void tma_load_2d_pair(void* smem, const CUtensorMap* map, int x, int y, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster)
       : "memory");
 }
-PPD_DEV void tma_load_tile_pair(void* smem, const CUtensorMap* map, int y, int tile, uint32_t bar_cluster) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(smem)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(tile), "r"(bar_cluster)
-      : "memory");
-}
 PPD_DEV void mma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
@@ -159,20 +143,6 @@ PPD_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
 }
 
 }  // namespace
-
-// ---- timing probe (gemm_diag bit 2) ------------------------------------------
-constexpr int kMaxTsCtas = 512;
-__device__ unsigned long long g_gemm_ts[kMaxTsCtas][6];
-PPD_DEV unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-int gemm_tc_read_timeline(unsigned long long* out, int max_ctas) {
-  const int n = max_ctas < kMaxTsCtas ? max_ctas : kMaxTsCtas;
-  return cudaMemcpyFromSymbol(out, g_gemm_ts, (size_t)n * 6 * sizeof(unsigned long long)) == cudaSuccess ? n : -1;
-}
 
 // ---- work schedule shared by the producer, MMA and epilogue roles ----------
 // A segment is a contiguous k-block range [kb0, kb1) of one (weight tile,
@@ -249,19 +219,18 @@ struct Sched {
 // leader alone arms it with both CTAs' bytes); the leader's commits multicast
 // to the smem-slot and accumulator barriers of both CTAs; both epilogues
 // release an accumulator on the leader's barrier (8 warp arrivals).
-template <bool kPair, int kEpi, int kOcc>
+template <bool kPair, int kEpi, int kOcc, int kNSub>
 __global__ void __launch_bounds__(kThreads, kOcc)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                    GemmTcParams p) {
-  const unsigned long long t_entry = (p.diag & 4) ? globaltimer_ns() : 0ull;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kCta = kPair ? 2 : 1;
   const int S = p.stages;
   const int xrows = p.bn / kCta;  // token rows this CTA loads per stage and token sub-tile
-  const int n_sub = p.n_sub;      // token sub-tiles of bn rows per unit (one weight stage feeds all)
-  const int unit_t = p.bn * n_sub;
-  const int stage_bytes = kWBytes + n_sub * xrows * kBK * 2;  // multiples of 1 KB
+  // kNSub token sub-tiles of bn rows per unit (compile time): one weight stage feeds kNSub MMAs
+  const int unit_t = p.bn * kNSub;
+  const int stage_bytes = kWBytes + kNSub * xrows * kBK * 2;  // multiples of 1 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;      // [2]
@@ -274,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, kOcc)
   const bool leader = rank == 0;
   const int slot = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int n_slots = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int acc_cols = n_sub * p.bn_cols;  // TMEM columns of one accumulator set
+  const int acc_cols = kNSub * p.bn_cols;  // TMEM columns of one accumulator set
   const int n_acc = p.tmem_cols >= 2 * acc_cols ? 2 : 1;
 
   if (threadIdx.x == 0) {
@@ -304,12 +273,6 @@ __global__ void __launch_bounds__(kThreads, kOcc)
   if (kPair) cluster_sync_all();  // peer barriers initialised + TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // diag bit 2: per-CTA timeline (globaltimer ns) into g_gemm_ts[blockIdx.x][0..5]
-  unsigned long long* ts = (p.diag & 4) && blockIdx.x < kMaxTsCtas ? g_gemm_ts[blockIdx.x] : nullptr;
-  if (ts && threadIdx.x == 0) {
-    ts[0] = t_entry;
-    ts[1] = globaltimer_ns();
-  }
   pdl_trigger();  // the next kernel may launch; it waits for our completion itself
 
   const int rows = kBM * kCta;
@@ -317,8 +280,7 @@ __global__ void __launch_bounds__(kThreads, kOcc)
   const uint32_t acc_empty0 = kPair ? mapa_shared(smem_u32(acc_empty), 0) : smem_u32(acc_empty);
   const int w_row0 = (int)rank * kBM;
   const int x_row0 = (int)rank * xrows;
-  // diag bit 0: skip the activation loads (timing probe only)
-  const uint32_t tx_bytes = (uint32_t)(kCta * ((p.diag & 1) ? kWBytes : stage_bytes));
+  const uint32_t tx_bytes = (uint32_t)(kCta * stage_bytes);
 
   auto load = [&](void* dst, const CUtensorMap* map, int x, int y, int s) {
     if (kPair)
@@ -326,28 +288,9 @@ __global__ void __launch_bounds__(kThreads, kOcc)
     else
       tma_load_2d(dst, map, x, y, &full[s]);
   };
-  // sub-box `i` (of p.w_split) of the 128 x 64 weight box of k-block kb at
-  // weight row `row` (a multiple of 128): rows [i*128/ws, (i+1)*128/ws)
-  const int w_kbt = (p.K + kBK - 1) / kBK;
-  const int ws = p.w_split, ws_rows = kBM / ws;
-  auto load_w = [&](void* dst, int kb, int row, int s, int i) {
-    dst = static_cast<uint8_t*>(dst) + i * (kWBytes / ws);
-    if (p.w_tiled) {
-      const int tile = (row / kBM) * w_kbt + kb;
-      if (kPair)
-        tma_load_tile_pair(dst, &map_w, i * ws_rows, tile, full_bar0 + 8u * s);
-      else
-        tma_load_tile(dst, &map_w, i * ws_rows, tile, &full[s]);
-    } else {
-      load(dst, &map_w, kb * kBK, row + i * ws_rows, s);
-    }
-  };
 
   if (warp == 0) {
-    // The whole warp walks the schedule; lane 0 arms each stage's barrier,
-    // then lanes [0, ws) issue the weight sub-boxes and lanes [16, 16+n_sub)
-    // the activation boxes in parallel (several TMA boxes in flight per stage).
-    {
+    if (lane == 0) {
       Sched sc;
       sc.begin(p, rows, slot, n_slots);
       Seg sg;
@@ -356,9 +299,8 @@ __global__ void __launch_bounds__(kThreads, kOcc)
         Sched pre = sc;
         while (npre < S && pre.next(sg)) {
           for (int kb = sg.kb0; kb < sg.kb1 && npre < S; ++kb, ++npre) {
-            if (leader && lane == 0) mbar_arrive_expect_tx(&full[npre], tx_bytes);
-            __syncwarp();
-            if (lane < ws) load_w(smem + npre * stage_bytes, kb, sg.tw * rows + w_row0, npre, lane);
+            if (leader) mbar_arrive_expect_tx(&full[npre], tx_bytes);
+            load(smem + npre * stage_bytes, &map_w, kb * kBK, sg.tw * rows + w_row0, npre);
           }
         }
       }
@@ -375,12 +317,11 @@ __global__ void __launch_bounds__(kThreads, kOcc)
               else
                 mbar_wait(&empty[s], ((it / S) - 1) & 1);
             }
-            if (leader && lane == 0) mbar_arrive_expect_tx(&full[s], tx_bytes);
-            __syncwarp();
-            if (lane < ws) load_w(sw, kb, sg.tw * rows + w_row0, s, lane);
+            if (leader) mbar_arrive_expect_tx(&full[s], tx_bytes);
+            load(sw, &map_w, kb * kBK, sg.tw * rows + w_row0, s);
           }
-          const int jx = lane - 16;
-          if (jx >= 0 && jx < n_sub && !(p.diag & 1))
+#pragma unroll
+          for (int jx = 0; jx < kNSub; ++jx)
             load(sw + kWBytes + jx * xrows * (kBK * 2), &map_x, kb * kBK, sg.tt * unit_t + jx * p.bn + x_row0, s);
         }
       }
@@ -410,12 +351,12 @@ __global__ void __launch_bounds__(kThreads, kOcc)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * stage_bytes);
           const uint64_t da = sw128_kmajor_desc(sa);
-          if (ts && it == 0) ts[2] = globaltimer_ns();
-          for (int js = 0; js < n_sub; ++js) {
+#pragma unroll
+          for (int js = 0; js < kNSub; ++js) {
             const uint64_t db = sw128_kmajor_desc(sa + kWBytes + js * xrows * (kBK * 2));
             const uint32_t dj = d_tmem + (uint32_t)(js * p.bn_cols);
 #pragma unroll
-            for (int k = 0; k < kBK / 16 && !(p.diag & 2); ++k) {  // 32 B per UMMA_K inside the atom
+            for (int k = 0; k < kBK / 16; ++k) {  // 32 B per UMMA_K step inside the swizzle atom
               const uint32_t accum = (kb != sg.kb0) || (k != 0);
               if (kPair)
                 mma_bf16_pair(dj, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, accum);
@@ -433,7 +374,6 @@ __global__ void __launch_bounds__(kThreads, kOcc)
         else
           mma_commit(&acc_full[acc]);
       }
-      if (ts) ts[3] = globaltimer_ns();
     }
   } else if (warp >= 4) {
     pdl_wait();  // outputs are written only after the predecessor retired
@@ -449,8 +389,9 @@ __global__ void __launch_bounds__(kThreads, kOcc)
       tc_fence_after();
       float* out32 = reinterpret_cast<float*>(p.out) + (size_t)sg.slice * p.split_stride;
       __nv_bfloat16* out16 = reinterpret_cast<__nv_bfloat16*>(p.out);
-      int buf = 0;  // exchange buffer parity runs on across sub-tiles (double buffering)
-      for (int jsub = 0; jsub < n_sub; ++jsub) {
+      int buf = 0;  // SiLU exchange-buffer parity runs on across sub-tiles (double buffering)
+#pragma unroll
+      for (int jsub = 0; jsub < kNSub; ++jsub) {
       const int t0 = sg.tt * unit_t + jsub * p.bn;
       const uint32_t t_acc =
           tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * acc_cols + jsub * p.bn_cols);
@@ -492,27 +433,28 @@ __global__ void __launch_bounds__(kThreads, kOcc)
         tmem_ld32(t_acc + (uint32_t)c0, r);
         if (row < p.N) {
           const int nj = min(32, ncols - c0);
-          // one running pointer (not 32 precomputed addresses): keeps the
-          // epilogue's register footprint small enough for 2 CTAs per SM
           if (p.out_f32) {
             float* dst = out32 + (size_t)(t0 + c0) * p.ldo + row;
+            if (kOcc == 2) {  // one running pointer: fits the 128-register budget of 2 CTAs per SM
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              if (jj < nj) *dst = __uint_as_float(r[jj]);
-              dst += p.ldo;
+              for (int jj = 0; jj < 32; ++jj) {
+                if (jj < nj) *dst = __uint_as_float(r[jj]);
+                dst += p.ldo;
+              }
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < 32; ++jj)
+                if (jj < nj) dst[(size_t)jj * p.ldo] = __uint_as_float(r[jj]);
             }
           } else {
             __nv_bfloat16* dst = out16 + (size_t)(t0 + c0) * p.ldo + row;
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              if (jj < nj) *dst = __float2bfloat16_rn(__uint_as_float(r[jj]));
-              dst += p.ldo;
-            }
+            for (int jj = 0; jj < 32; ++jj)
+              if (jj < nj) dst[(size_t)jj * p.ldo] = __float2bfloat16_rn(__uint_as_float(r[jj]));
           }
         }
       }
       }  // token sub-tiles
-      if (ts && q == 0 && lane == 0) ts[4] = globaltimer_ns();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -526,7 +468,6 @@ __global__ void __launch_bounds__(kThreads, kOcc)
   tc_fence_before();
   __syncthreads();
   if (kPair) cluster_sync_all();  // the leader's MMAs may read the peer's smem until here
-  if (ts && threadIdx.x == 0) ts[5] = globaltimer_ns();
   if (warp == 2) {
     if (kPair)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(p.tmem_cols));
@@ -590,50 +531,11 @@ bool get_map(CUtensorMap* out, const void* ptr, int rows, int K, int box_rows) {
   return true;
 }
 
-// k-block tiled [N][K] weight: a 3-D view {64 k, 128 rows, tiles} whose box
-// {64, 128, 1} is one contiguous 16 KB tile; the 128 B swizzle lands it in smem
-// exactly like the 2-D box of the row-major layout.
-int g_w_promo = 2;  // L2 promotion of weight boxes: 0 none, 1 128 B, 2 256 B
-CUtensorMapL2promotion w_promo() {
-  return g_w_promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-         : g_w_promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-}
-
-bool get_map_tiled(CUtensorMap* out, const void* ptr, int N, int K, int ws) {
-  static std::mutex mu;
-  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  MapKey key{ptr, N, K, -1 - g_w_promo - 4 * ws};
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(key);
-  if (it != cache.end()) {
-    *out = it->second;
-    return true;
-  }
-  auto fn = encode_fn();
-  if (!fn) return false;
-  const cuuint64_t tiles = (cuuint64_t)(N / kBM) * (cuuint64_t)(K / kBK);
-  cuuint64_t dims[3] = {(cuuint64_t)kBK, (cuuint64_t)kBM, tiles};
-  cuuint64_t strides[2] = {(cuuint64_t)kBK * 2, (cuuint64_t)kWBytes};
-  cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)(kBM / ws), 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUtensorMap m;
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, w_promo(),
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return false;
-  if (cache.size() > 4096) cache.clear();
-  cache.emplace(key, m);
-  *out = m;
-  return true;
-}
-
 }  // namespace
 // Tuning knobs (ppd_set_tuning): pair = -1 auto / 0 single-CTA / 1 CTA pair;
 // stages = cap on the smem ring depth (0 = as many as fit); sched = -1 auto /
 // 0 uniform K split / 1 balanced partition.
 static int g_pair_mode = -1;
-static int g_stage_cap = 0;
-static int g_sched = -1;
 static bool g_multi_sub = true;  // T in (256, 512]: one unit covers both token sub-tiles
 // two co-resident single CTAs per SM: -1 auto (<= kOcc2MaxT tokens; measured
 // tools/gemm_knobs.py: +10-20% weight streaming at T = 64 / 128, neutral at
@@ -641,6 +543,8 @@ static bool g_multi_sub = true;  // T in (256, 512]: one unit covers both token 
 static int g_occ2 = -1;
 constexpr int kOcc2MaxT = 128;
 constexpr int kOcc2Smem = 113 * 1024;
+static int g_stage_cap = 0;
+static int g_sched = -1;
 
 
 
@@ -652,13 +556,6 @@ constexpr int kPairMinT = 48;
 constexpr double kPairMinTilesPerSm = 1.4;
 
 void gemm_tc_set_multi_sub(bool on) { g_multi_sub = on; }
-static int g_diag = 0;
-static int g_w_split = 1;
-void gemm_tc_set_diag(int diag, int w_promo) {
-  g_diag = diag;
-  g_w_promo = w_promo;
-}
-void gemm_tc_set_w_split(int ws) { g_w_split = ws; }
 void gemm_tc_set_occ2(int mode) { g_occ2 = mode; }
 
 void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched) {
@@ -675,21 +572,35 @@ struct Shape {
   int n_sub;   // token sub-tiles of bn rows per unit: a decode + append step of T <= 512 rows
                // streams each weight stage ONCE for all its tokens (2 MMAs of N = bn)
   int unit_t;  // token rows per unit = bn * n_sub
-  int occ;     // co-resident CTAs per SM: 2 = half the smem ring and one 256-column
-               // accumulator each, so one CTA's fill / epilogue tail (and the next
-               // kernel's PDL prologue) overlaps the other's weight streaming
+  int occ;     // co-resident CTAs per SM: 2 = half-depth ring and one <= 256-column
+               // accumulator each, so one CTA's fill / epilogue tail overlaps the
+               // other's weight streaming
 };
+
+// every kernel instantiation the launcher can pick
+#define PPD_GEMM_KERNELS(X)                                                            \
+  X(false, kEpiPlain, 1, 1) X(true, kEpiPlain, 1, 1) X(false, kEpiPlain, 1, 2)         \
+  X(true, kEpiPlain, 1, 2) X(false, kEpiSilu, 1, 1) X(true, kEpiSilu, 1, 1)            \
+  X(false, kEpiSilu, 1, 2) X(true, kEpiSilu, 1, 2) X(false, kEpiPlain, 2, 1) X(true, kEpiPlain, 2, 1)
+
+using GemmKernel = void (*)(const CUtensorMap, const CUtensorMap, GemmTcParams);
+GemmKernel pick_kernel(bool pair, int epi, int occ, int n_sub) {
+#define PPD_PICK(P, E, O, N) \
+  if (pair == P && epi == E && occ == O && n_sub == N) return gemm_tc_kernel<P, E, O, N>;
+  PPD_GEMM_KERNELS(PPD_PICK)
+#undef PPD_PICK
+  return nullptr;
+}
 
 void set_smem_attrs() {
   static bool done = false;
   if (done) return;
   const int bytes = 1024 + kSmemBudget + kBarBytes;
-  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiPlain, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiPlain, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiSilu, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiSilu, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(gemm_tc_kernel<false, kEpiPlain, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOcc2Smem);
-  cudaFuncSetAttribute(gemm_tc_kernel<true, kEpiPlain, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOcc2Smem);
+#define PPD_ATTR(P, E, O, N)                                                                \
+  cudaFuncSetAttribute(gemm_tc_kernel<P, E, O, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       O == 2 ? kOcc2Smem : bytes);
+  PPD_GEMM_KERNELS(PPD_ATTR)
+#undef PPD_ATTR
   done = true;
 }
 
@@ -701,7 +612,7 @@ int max_pair_slots(int smem, int occ) {
   if (it != cache.end()) return it->second;
   set_smem_attrs();
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(2 * 74);
+  cfg.gridDim = dim3(2 * 74 * occ);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
@@ -712,10 +623,7 @@ int max_pair_slots(int smem, int occ) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  cfg.gridDim = dim3(2 * 74 * occ);
-  const cudaError_t e = occ == 2 ? cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<true, kEpiPlain, 2>, &cfg)
-                                 : cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<true, kEpiPlain, 1>, &cfg);
-  if (e != cudaSuccess || n <= 0) {
+  if (cudaOccupancyMaxActiveClusters(&n, pick_kernel(true, kEpiPlain, occ, 1), &cfg) != cudaSuccess || n <= 0) {
     cudaGetLastError();
     n = 0;
   }
@@ -824,9 +732,8 @@ int gemm_tc_plan_splits(int T, int N, int K) {
 namespace {
 
 cudaError_t launch(const Shape& sh, const Plan& pl, const bf16* X, const bf16* W, void* out, int T, int N, int K,
-                   bool out_f32, size_t split_stride, cudaStream_t s, int epi = kEpiPlain, bool w_tiled = false) {
+                   bool out_f32, size_t split_stride, cudaStream_t s, int epi = kEpiPlain) {
   if (sh.stages < 2) return cudaErrorInvalidValue;  // ring does not fit
-  if (w_tiled && (N % kBM != 0 || K % kBK != 0)) return cudaErrorInvalidValue;
   GemmTcParams p{};
   p.out = out;
   p.T = T;
@@ -836,7 +743,6 @@ cudaError_t launch(const Shape& sh, const Plan& pl, const bf16* X, const bf16* W
   p.epi = epi;
   p.bn = sh.bn;
   p.n_sub = sh.n_sub;
-  p.diag = g_diag;
   p.out_f32 = out_f32 ? 1 : 0;
   p.splits = pl.balanced ? 1 : pl.splits;
   p.split_stride = split_stride ? split_stride : (size_t)T * N;
@@ -849,28 +755,20 @@ cudaError_t launch(const Shape& sh, const Plan& pl, const bf16* X, const bf16* W
   p.slots = pl.slots;
   p.total = pl.total;
   CUtensorMap mw, mx;
-  p.w_tiled = w_tiled ? 1 : 0;
-  p.w_split = g_w_split;
-  const bool ok_w = w_tiled ? get_map_tiled(&mw, W, N, K, p.w_split) : get_map(&mw, W, N, K, kBM / p.w_split);
-  if (!ok_w || !get_map(&mx, X, T, K, sh.pair ? sh.bn / 2 : sh.bn))
+  if (!get_map(&mw, W, N, K, kBM) || !get_map(&mx, X, T, K, sh.pair ? sh.bn / 2 : sh.bn))
     return cudaErrorInvalidValue;
   set_smem_attrs();
+  const GemmKernel kern = pick_kernel(sh.pair, epi, sh.occ, sh.n_sub);
+  if (!kern) return cudaErrorInvalidValue;
   if (sh.pair)
-    return launch_pdl_cluster(sh.occ == 2          ? gemm_tc_kernel<true, kEpiPlain, 2>
-                              : epi == kEpiSilu    ? gemm_tc_kernel<true, kEpiSilu, 1>
-                                                   : gemm_tc_kernel<true, kEpiPlain, 1>,
-                              dim3(2 * pl.slots), dim3(kThreads), (size_t)sh.smem, 2, s, mw,
-                              mx, p);
-  return launch_pdl(sh.occ == 2       ? gemm_tc_kernel<false, kEpiPlain, 2>
-                    : epi == kEpiSilu ? gemm_tc_kernel<false, kEpiSilu, 1>
-                                      : gemm_tc_kernel<false, kEpiPlain, 1>,
-                    dim3(pl.slots), dim3(kThreads), (size_t)sh.smem, s, mw, mx, p);
+    return launch_pdl_cluster(kern, dim3(2 * pl.slots), dim3(kThreads), (size_t)sh.smem, 2, s, mw, mx, p);
+  return launch_pdl(kern, dim3(pl.slots), dim3(kThreads), (size_t)sh.smem, s, mw, mx, p);
 }
 
 }  // namespace
 
 cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, int K, bool out_f32, int splits,
-                        size_t split_stride, cudaStream_t s, bool w_tiled) {
+                        size_t split_stride, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (K % 8 != 0) return cudaErrorInvalidValue;  // TMA row stride must be 16 B aligned
   if (splits < 1) splits = 1;
@@ -879,11 +777,11 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
   const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.unit_t - 1) / sh.unit_t);
   const int units = tiles * splits;
   const Plan pl{false, splits, units < sh.slots ? units : sh.slots, splits, 0};
-  return launch(sh, pl, X, W, out, T, N, K, out_f32, split_stride, s, kEpiPlain, w_tiled);
+  return launch(sh, pl, X, W, out, T, N, K, out_f32, split_stride, s);
 }
 
 cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, int N, int K, int max_slices,
-                              size_t split_stride, GemmParts* parts, cudaStream_t s, bool w_tiled) {
+                              size_t split_stride, GemmParts* parts, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (K % 8 != 0 || max_slices < 1) return cudaErrorInvalidValue;
   const Shape sh = shape_for(T, N);
@@ -898,17 +796,16 @@ cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, i
   g.n_tiles_t = (T + sh.unit_t - 1) / sh.unit_t;
   g.total = pl.balanced ? pl.total : 1;
   *parts = g;
-  return launch(sh, pl, X, W, out, T, N, K, true, g.stride, s, kEpiPlain, w_tiled);
+  return launch(sh, pl, X, W, out, T, N, K, true, g.stride, s);
 }
 
-cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N, int K, cudaStream_t s,
-                             bool w_tiled) {
+cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N, int K, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (K % 8 != 0 || N % kBM != 0) return cudaErrorInvalidValue;  // whole gate|up groups per 128-row slab
   const Shape sh = shape_for(T, N, kXchgBytes);
   const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.unit_t - 1) / sh.unit_t);
   const Plan pl{false, 1, tiles < sh.slots ? tiles : sh.slots, 1, 0};
-  return launch(sh, pl, X, W, m, T, N, K, false, 0, s, kEpiSilu, w_tiled);
+  return launch(sh, pl, X, W, m, T, N, K, false, 0, s, kEpiSilu);
 }
 
 }  // namespace ppdk

@@ -23,7 +23,7 @@ struct GemmParts {
   int kbt = 0;          // k-blocks per tile (0 = uniform split)
   int slots = 1;        // ranges (persistent CTAs / pairs)
   int rows = 128;       // weight rows (output columns) per tile
-  int bn = 256;         // token rows per tile (unit: all token sub-tiles of one weight stage)
+  int bn = 256;         // token rows per tile (a unit: all token sub-tiles of one weight stage)
   int n_tiles_t = 1;    // token tiles
   long long total = 1;  // tiles * kbt
 
@@ -47,41 +47,28 @@ struct GemmTcParams {
   long long total;      // tiles * k-blocks per tile (balanced)
   int epi;              // 0: write C (fp32 slices / bf16); 1: fused SiLU(gate)*up -> bf16 [T][N/2]
   int n_sub;            // token sub-tiles (of bn rows) per unit: every weight stage feeds n_sub MMAs
-  int diag;             // timing probes only: bit 0 skip activation loads, bit 1 skip MMAs
-  int w_split;          // TMA sub-boxes per 128-row weight box (issued lane-parallel)
-  int w_tiled;          // W stored k-block tiled (ops.cu phys_to_rc): one contiguous 16 KB run per TMA box
 };
 
 // out[T][N] (+ split slices) = X[T][K] . W[N][K]^T ; splits > 1 needs out_f32
-// w_tiled: W is stored k-block tiled (128-row x 64-col contiguous 16 KB tiles,
-// launch_fill_matrix / launch_tile_matrix); needs N % 128 == 0 and K % 64 == 0.
 cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, int K, bool out_f32, int splits,
-                        size_t split_stride, cudaStream_t s, bool w_tiled = false);
+                        size_t split_stride, cudaStream_t s);
 // fp32 output into partial slices chosen by the planner (uniform split or a
 // balanced partition), at most `max_slices` slices of split_stride floats.
 cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, int N, int K, int max_slices,
-                              size_t split_stride, GemmParts* parts, cudaStream_t s, bool w_tiled = false);
+                              size_t split_stride, GemmParts* parts, cudaStream_t s);
 // m[T][N/2] = rbf(silu(gate) * up) for the interleaved gate|up weight [N][K]
 // (64-row groups, launch_fill_gate_up): the MLP up-projection with SiLU fused
 // into the epilogue (no K split; no fp32 round trip through HBM).
-cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N, int K, cudaStream_t s,
-                             bool w_tiled = false);
+cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N, int K, cudaStream_t s);
 // pair_mode: -1 auto, 0 single-CTA kernel, 1 CTA-pair kernel; stage_cap 0 = no cap;
 // sched: -1 auto, 0 uniform K split, 1 balanced partition
 void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched);
 // T in (256, 512] token rows: one unit per weight tile covering 2 token
 // sub-tiles (default on) vs separate 256-row token tiles (A/B knob)
 void gemm_tc_set_multi_sub(bool on);
-// timing probes (results invalid when diag != 0) and the weight boxes' L2 promotion
-void gemm_tc_set_diag(int diag, int w_promo);
-// weight box split into 1/2/4/8 TMA sub-boxes issued by parallel lanes
-void gemm_tc_set_w_split(int ws);
 // two co-resident CTAs per SM (half-depth rings, one accumulator each):
 // -1 auto (small token counts), 0 off, 1 whenever the shape allows
 void gemm_tc_set_occ2(int mode);
-// per-CTA timeline of the last diag-4 launch: [cta][entry, setup, first data,
-// last MMA issued, last epilogue done, exit] (globaltimer ns); returns CTAs read
-int gemm_tc_read_timeline(unsigned long long* out, int max_ctas);
 // K-split count that fills the 148 SMs for this shape (1 when the tile grid already does)
 int gemm_tc_plan_splits(int T, int N, int K);
 

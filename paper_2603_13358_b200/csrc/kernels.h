@@ -50,6 +50,11 @@ cudaError_t launch_decode_attention(const void* kv_map, const AttnParams& p, int
 int make_kv_tensor_map(void* map_out /* CUtensorMap, 128 B */, const void* pool, uint64_t total_rows);
 cudaError_t launch_paged_attention(const void* kv_map, const AttnParams& p, int n_items,
                                    cudaStream_t stream);
+// K2 fused mixed step: n_pf tcgen05 prefill CTAs over n_pf_tiles = (prefill
+// items at pf_items) x n_kv_heads tiles + the balanced decode schedule of
+// n_vcta virtual CTAs (two per CTA), one launch
+cudaError_t launch_mixed_attention(const void* kv_map, const AttnParams& p, const AttnItem* pf_items, int n_pf,
+                                   int n_pf_tiles, int n_vcta, cudaStream_t stream);
 // tcgen05/TMEM prefill tiles (kind 1 items of 128/G tokens)
 cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p, int n_items, cudaStream_t stream);
 
@@ -57,15 +62,14 @@ cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p,
 cudaError_t launch_fill_random(bf16* dst, uint64_t n, uint64_t seed, int tensor, int layer,
                                cudaStream_t s);
 // fused QKV weight [Hq*Dh + 2*Hkv*Dh][d]: rows < qd from tensor WQ, then WK, then WV
-cudaError_t launch_fill_qkv(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer, int tiled, cudaStream_t s);
-// weight matrix [N][K], row-major (tiled = 0) or k-block tiled (ops.cu, kWTile*)
-cudaError_t launch_fill_matrix(bf16* dst, uint64_t N, uint64_t K, uint64_t seed, int tensor, int layer, int tiled,
+cudaError_t launch_fill_qkv(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer, cudaStream_t s);
+// weight matrix [N][K], row-major
+cudaError_t launch_fill_matrix(bf16* dst, uint64_t N, uint64_t K, uint64_t seed, int tensor, int layer,
                                cudaStream_t s);
-cudaError_t launch_tile_matrix(const bf16* src, bf16* dst, uint64_t N, uint64_t K, cudaStream_t s);
 cudaError_t launch_fill_bias(float* dst, int qd, int kd, uint64_t seed, int layer, cudaStream_t s);
 // gate/up weight [2F][d], interleaved in groups of 64 rows: rows [128j, 128j+64) = gate
 // rows [64j, 64j+64), rows [128j+64, 128j+128) = up rows [64j, 64j+64)
-cudaError_t launch_fill_gate_up(bf16* dst, int F, int d, uint64_t seed, int layer, int tiled, cudaStream_t s);
+cudaError_t launch_fill_gate_up(bf16* dst, int F, int d, uint64_t seed, int layer, cudaStream_t s);
 cudaError_t launch_fill_const(bf16* dst, uint64_t n, float v, cudaStream_t s);
 
 cudaError_t launch_embed(const int* tokens, const bf16* embed, bf16* x, int T, int d, cudaStream_t s);

@@ -45,46 +45,23 @@ cudaError_t launch_fill_random(bf16* dst, uint64_t n, uint64_t seed, int tensor,
   return cudaGetLastError();
 }
 
-// Weight matrices [N][K] are stored either row-major or K-BLOCK TILED
-// (tiled = 1): 128-row x 64-column tiles of 16 KB, each contiguous, ordered
-// (row tile, k-block) — so one GEMM TMA box is one contiguous 16 KB run of
-// HBM (kWTile* in kernels.h). Element (n, k) of a tiled matrix lives at
-//   ((n/128) * (K/64) + k/64) * 8192 + (n%128) * 64 + k%64.
-// The VALUE of element (n, k) never depends on the layout: it is the counter
-// hash of its logical index, exactly as oracle/model_oracle.c computes it.
-PPD_DEV void phys_to_rc(uint64_t i, uint64_t K, int tiled, uint64_t& r, uint64_t& c) {
-  if (!tiled) {
-    r = i / K;
-    c = i % K;
-    return;
-  }
-  const uint64_t tile = i >> 13, w = i & 8191, kbt = K >> 6;
-  r = (tile / kbt) * 128 + (w >> 6);
-  c = (tile % kbt) * 64 + (w & 63);
-}
-
-__global__ void fill_matrix_kernel(bf16* dst, uint64_t N, uint64_t K, uint64_t seed, int tensor, int layer,
-                                   int tiled) {
-  const uint64_t n = N * K;
+// weight matrix [N][K] (row-major): element (n, k) = counter hash of n*K + k
+__global__ void fill_matrix_kernel(bf16* dst, uint64_t n, uint64_t seed, int tensor, int layer) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t r, c;
-    phys_to_rc(i, K, tiled, r, c);
-    dst[i] = weight_value(seed, tensor, layer, r * K + c);
-  }
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = weight_value(seed, tensor, layer, i);
 }
-cudaError_t launch_fill_matrix(bf16* dst, uint64_t N, uint64_t K, uint64_t seed, int tensor, int layer, int tiled,
+cudaError_t launch_fill_matrix(bf16* dst, uint64_t N, uint64_t K, uint64_t seed, int tensor, int layer,
                                cudaStream_t s) {
-  fill_matrix_kernel<<<148 * 8, 256, 0, s>>>(dst, N, K, seed, tensor, layer, tiled);
+  fill_matrix_kernel<<<148 * 8, 256, 0, s>>>(dst, N * K, seed, tensor, layer);
   return cudaGetLastError();
 }
 
-__global__ void fill_qkv_kernel(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer, int tiled) {
+__global__ void fill_qkv_kernel(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer) {
   const uint64_t n = (uint64_t)(qd + 2 * kd) * d;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t r, c;
-    phys_to_rc(i, d, tiled, r, c);
+    uint64_t r = i / d, c = i % d;
     int tensor;
     uint64_t lr;
     if (r < (uint64_t)qd) { tensor = 1; lr = r; }
@@ -93,8 +70,8 @@ __global__ void fill_qkv_kernel(bf16* dst, int qd, int kd, int d, uint64_t seed,
     dst[i] = weight_value(seed, tensor, layer, lr * d + c);
   }
 }
-cudaError_t launch_fill_qkv(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer, int tiled, cudaStream_t s) {
-  fill_qkv_kernel<<<148 * 8, 256, 0, s>>>(dst, qd, kd, d, seed, layer, tiled);
+cudaError_t launch_fill_qkv(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer, cudaStream_t s) {
+  fill_qkv_kernel<<<148 * 8, 256, 0, s>>>(dst, qd, kd, d, seed, layer);
   return cudaGetLastError();
 }
 
@@ -113,35 +90,19 @@ cudaError_t launch_fill_bias(float* dst, int qd, int kd, uint64_t seed, int laye
   return cudaGetLastError();
 }
 
-__global__ void fill_gate_up_kernel(bf16* dst, int F, int d, uint64_t seed, int layer, int tiled) {
+__global__ void fill_gate_up_kernel(bf16* dst, int F, int d, uint64_t seed, int layer) {
   const uint64_t n = (uint64_t)2 * F * d;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t r, c;
-    phys_to_rc(i, d, tiled, r, c);
+    uint64_t r = i / d, c = i % d;
     uint64_t grp = r / 128, within = r % 128;
     int tensor = within < 64 ? 5 : 6;  // gate | up
     uint64_t lr = grp * 64 + (within & 63);
     dst[i] = weight_value(seed, tensor, layer, lr * d + c);
   }
 }
-cudaError_t launch_fill_gate_up(bf16* dst, int F, int d, uint64_t seed, int layer, int tiled, cudaStream_t s) {
-  fill_gate_up_kernel<<<148 * 8, 256, 0, s>>>(dst, F, d, seed, layer, tiled);
-  return cudaGetLastError();
-}
-
-// row-major [N][K] -> k-block tiled (the layout above); N % 128 == 0, K % 64 == 0
-__global__ void tile_matrix_kernel(const bf16* src, bf16* dst, uint64_t N, uint64_t K) {
-  const uint64_t n = N * K;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t r, c;
-    phys_to_rc(i, K, 1, r, c);
-    dst[i] = src[r * K + c];
-  }
-}
-cudaError_t launch_tile_matrix(const bf16* src, bf16* dst, uint64_t N, uint64_t K, cudaStream_t s) {
-  tile_matrix_kernel<<<148 * 8, 256, 0, s>>>(src, dst, N, K);
+cudaError_t launch_fill_gate_up(bf16* dst, int F, int d, uint64_t seed, int layer, cudaStream_t s) {
+  fill_gate_up_kernel<<<148 * 8, 256, 0, s>>>(dst, F, d, seed, layer);
   return cudaGetLastError();
 }
 

@@ -84,3 +84,24 @@ def test_mixed_decode_and_append_one_launch(gpu):
 def test_qwen_group_of_5(gpu):
     run_case(cfg_of(40, 8), [1, 1, 33], [300, 7, 90], seed=6)
     run_case(cfg_of(40, 8), [1], [5000], seed=7)
+
+
+def test_mixed_many_tiles_per_prefill_cta(gpu):
+    """K2 fused launch where the SM split gives each prefill CTA several tiles
+    (barriers re-armed per tile) next to a heavy decode batch."""
+    q_len = [1] * 64 + [512]
+    ctx = [2000 + 7 * i for i in range(64)] + [1500]
+    run_case(cfg_of(32, 8), q_len, ctx, seed=8)
+
+
+def test_mixed_fused_and_split_launches_agree(gpu):
+    """The one-launch mixed kernel and the two-launch path (attn_fused = 0)
+    both match the oracle on the same mixed batch."""
+    L = ppd.lib()
+    case = ([1, 1, 1, 96, 1, 40], [900, 33, 4000, 700, 1, 0])
+    run_case(cfg_of(32, 8), *case, seed=9)
+    ppd.check(L.ppd_set_tuning(b"attn_fused", 0))
+    try:
+        run_case(cfg_of(32, 8), *case, seed=9)
+    finally:
+        ppd.check(L.ppd_set_tuning(b"attn_fused", 1))

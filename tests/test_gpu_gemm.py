@@ -168,43 +168,3 @@ def test_gemm_silu_fused(gpu, pair_mode, M, N, K):
     assert torch.isfinite(got).all()
     tol = 2 ** -7 * ref.abs() + 1e-3 * np.sqrt(K) * ref.abs().max().item()
     assert ((got - ref).abs() <= tol).all()
-
-
-@pytest.mark.parametrize("M,N,K,splits", [
-    (200, 6144, 4096, 3),     # decode QKV, K-split
-    (328, 28672, 4096, 1),    # decode + 128-token append chunk, gate|up
-    (200, 4096, 14336, 4),    # down-proj
-    (1224, 6144, 4096, 1),    # several token tiles
-    (3, 2048, 512, 1),        # tiny model lm_head
-])
-def test_gemm_tc_tiled_weights_bit_exact(gpu, pair_mode, M, N, K, splits):
-    """The k-block tiled weight layout (the model's storage on the tcgen05
-    path, ppd_op_tile_matrix) gives the SAME bits as the row-major layout:
-    only the HBM address of each TMA box changes, not the smem image."""
-    import torch
-    L = ppd.lib()
-    g = torch.Generator(device="cuda").manual_seed(5)
-    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
-    B = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
-    Bt = torch.empty_like(B)
-    ppd.check(L.ppd_op_tile_matrix(B.data_ptr(), Bt.data_ptr(), N, K, None))
-    # the tiled image is a permutation of the row-major one
-    ref_t = B.view(N // 128, 128, K // 64, 64).permute(0, 2, 1, 3).contiguous().view(N, K)
-    assert torch.equal(Bt, ref_t)
-    C0 = torch.zeros(splits, M, N, device="cuda")
-    C1 = torch.zeros(splits, M, N, device="cuda")
-    ppd.check(L.ppd_op_gemm_tc(A.data_ptr(), B.data_ptr(), C0.data_ptr(), M, N, K, 1, splits, None))
-    ppd.check(L.ppd_set_tuning(b"ops_w_tiled", 1))
-    try:
-        ppd.check(L.ppd_op_gemm_tc(A.data_ptr(), Bt.data_ptr(), C1.data_ptr(), M, N, K, 1, splits, None))
-        m0 = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
-        m1 = torch.empty_like(m0)
-        ppd.check(L.ppd_set_tuning(b"ops_w_tiled", 0))
-        ppd.check(L.ppd_op_gemm_silu(A.data_ptr(), B.data_ptr(), m0.data_ptr(), M, N, K, None))
-        ppd.check(L.ppd_set_tuning(b"ops_w_tiled", 1))
-        ppd.check(L.ppd_op_gemm_silu(A.data_ptr(), Bt.data_ptr(), m1.data_ptr(), M, N, K, None))
-    finally:
-        ppd.check(L.ppd_set_tuning(b"ops_w_tiled", 0))
-    torch.cuda.synchronize()
-    assert torch.equal(C0, C1)
-    assert torch.equal(m0, m1)

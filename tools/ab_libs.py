@@ -44,8 +44,11 @@ def t_us(fn, iters=20):
 
 def main():
     libs = [load(s) for s in sys.argv[1:]]
-    T = 200
+    import os
+    T = int(os.environ.get("PPD_AB_T", "200"))
     shapes = [(6144, 4096, 3), (4096, 4096, 4), (28672, 4096, 1), (4096, 14336, 4), (128256, 4096, 1)]
+    if T > 512:  # prefill shapes: no K split
+        shapes = [(6144, 4096, 1), (4096, 4096, 1), (28672, 4096, 1), (4096, 14336, 1)]
     for N, K, sp in shapes:
         A = torch.randn(T, K, device="cuda").to(torch.bfloat16)
         B = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
@@ -59,6 +62,7 @@ def main():
         for i, (name, _) in enumerate(libs):
             out[f"lib{i}_us"] = round(float(np.median(res[name])), 2)
             out[f"lib{i}_TBs"] = round(N * K * 2 / np.median(res[name]) / 1e6, 2)
+            out[f"lib{i}_TFs"] = round(2 * T * N * K / np.median(res[name]) / 1e6, 1)
         print(json.dumps(out), flush=True)
 
 

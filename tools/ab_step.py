@@ -6,6 +6,9 @@ drift hits all of them alike; reports the median device ms per step of each.
   PPD_AB="base:;nofuse:mlp_fused=0;old:@old_build/<sha>/paper_2603_13358_b200/libppd_b200.so" \
       python tools/ab_step.py
 Each item is name:knob=v,...[@lib path]. One device (weights + KV pool) per build.
+PPD_AB_MIX="m:n[,m:n...]" adds prefill rows (m new tokens over n cached) to
+every step: the mixed decode + append / full prefill step of the
+interference sweep.
 """
 import contextlib
 import json
@@ -17,7 +20,8 @@ import numpy as np  # noqa: E402
 
 import paper_2603_13358_b200 as ppd  # noqa: E402
 
-DEFAULTS = {"gemm_pair": -1, "gemm_sched": -1, "gemm_stages": 0, "mlp_fused": 0, "diag_skip": 0}
+DEFAULTS = {"gemm_pair": -1, "gemm_sched": -1, "gemm_stages": 0, "mlp_fused": 0, "diag_skip": 0, "attn_fused": 1,
+            "gemm_occ2": -1, "gemm_multi_sub": 1}
 
 
 def parse(spec):
@@ -54,7 +58,15 @@ def main():
     cfg = ppd.llama8b_cfg()
     max_ctx = ctx0 + rounds * len(cfgs) * (steps + 2) + 16
     bps = (max_ctx + BT - 1) // BT
-    bts = np.arange(B * bps, dtype=np.int32).reshape(B, bps)
+    mix = [tuple(int(x) for x in it.split(":")) for it in filter(None, os.environ.get("PPD_AB_MIX", "").split(","))]
+    mbps = max([bps] + [(m + n + BT - 1) // BT for m, n in mix])
+    bts = np.zeros((B + len(mix), mbps), dtype=np.int32)
+    bts[:B, :bps] = np.arange(B * bps, dtype=np.int32).reshape(B, bps)
+    nxt = B * bps
+    for j, (m, n) in enumerate(mix):
+        k = (m + n + BT - 1) // BT
+        bts[B + j, :k] = np.arange(nxt, nxt + k)
+        nxt += k
     rng = np.random.default_rng(0)
     libs, devs = {}, {}
     for _, _, path in cfgs:
@@ -64,7 +76,7 @@ def main():
         with using(libs[path]):
             dev = ppd.Device(0, cfg, max_step_tokens=4096, max_step_seqs=256)
             dev.load_random_weights(1234)
-            dev.kv_pool_init(B * bps)
+            dev.kv_pool_init(nxt)
             ptr, nbytes = dev.kv_pool_ptr()
             ppd.check(libs[path].ppd_op_fill_random(ptr, nbytes // 2, 1234, 99, 0, None))
         devs[path] = dev
@@ -80,8 +92,11 @@ def main():
                         if L.ppd_set_tuning(k.encode(), v) != 0 and k in knobs:
                             raise SystemExit(f"{name}: knob {k} rejected: {L.ppd_last_error().decode()}")
                 for i in range(steps + 2):  # 2 warm-up steps: graph capture
-                    r = devs[path].step([1] * B, ctx, tok, bts)
-                    tok = r.tokens
+                    q = [1] * B + [m for m, _ in mix]
+                    c = list(ctx) + [n for _, n in mix]
+                    toks = np.concatenate([tok] + [rng.integers(0, cfg.vocab, m) for m, _ in mix]).astype(np.int32)
+                    r = devs[path].step(q, c, toks, bts, [1] * B + [0] * len(mix))
+                    tok = r.tokens[:B]
                     ctx += 1
                     if i >= 2:
                         res[name].append(r.ms)

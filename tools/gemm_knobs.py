@@ -1,6 +1,5 @@
 """Decode-GEMM sensitivity probe: weight-streaming TB/s of the fp32 forward
-path (ppd_op_gemm_parts, tiled weights rotating over > L2) under tuning knobs
-and timing-only diagnostics (gemm_diag: 1 skip activation loads, 2 skip MMAs).
+path (ppd_op_gemm_parts, weights rotating over > L2) under the tuning knobs.
   PPD_KN_T=200 python tools/gemm_knobs.py"""
 import ctypes
 import json
@@ -14,43 +13,20 @@ import paper_2603_13358_b200 as ppd  # noqa: E402
 from tools.gemm_rot import timed  # noqa: E402
 
 VARIANTS = [
-    {}, {"gemm_occ2": 0}, {"gemm_occ2": 1, "gemm_pair": 0}, {"gemm_occ2": 1, "gemm_pair": 0, "gemm_sched": 1},
-    {"gemm_occ2": 0, "gemm_pair": 0}, {"gemm_occ2": 0, "gemm_pair": 1},
+    {}, {"gemm_occ2": 0}, {"gemm_occ2": 1, "gemm_pair": 0}, {"gemm_multi_sub": 0},
+    {"gemm_pair": 0}, {"gemm_pair": 1}, {"gemm_sched": 0}, {"gemm_sched": 1},
 ]
-if os.environ.get("PPD_KN_WS"):
-    VARIANTS = [{}, {"gemm_wsplit": 2}, {"gemm_wsplit": 4}, {"gemm_wsplit": 8},
-    {"gemm_diag": 3}, {"gemm_wsplit": 2, "gemm_diag": 3}, {"gemm_wsplit": 4, "gemm_diag": 3},
-    {"gemm_wsplit": 8, "gemm_diag": 3},
-    {"gemm_pair": 0}, {"gemm_pair": 0, "gemm_wsplit": 4}, {"gemm_pair": 1, "gemm_wsplit": 4},
-    {"gemm_stages": 4, "gemm_wsplit": 4},
-]
-if os.environ.get("PPD_KN_OLD"):
-    VARIANTS = [
-        {}, {"gemm_stages": 3}, {"gemm_stages": 4}, {"gemm_stages": 5},
-        {"gemm_w_promo": 0}, {"gemm_w_promo": 1},
-        {"gemm_diag": 1}, {"gemm_diag": 2}, {"gemm_diag": 3},
-        {"gemm_pair": 0}, {"gemm_pair": 1}, {"gemm_pair": 0, "gemm_diag": 1}, {"gemm_pair": 0, "gemm_diag": 3},
-        {"gemm_sched": 0}, {"gemm_sched": 1},
-    ]
-DEFAULTS = {"gemm_occ2": -1, "gemm_stages": 0, "gemm_w_promo": 2, "gemm_diag": 0, "gemm_pair": -1, "gemm_sched": -1,
-            "gemm_wsplit": 1}
+DEFAULTS = {"gemm_occ2": -1, "gemm_stages": 0, "gemm_pair": -1, "gemm_sched": -1, "gemm_multi_sub": 1}
 
 
 def main():
     L = ppd.lib()
     ts = [int(x) for x in os.environ.get("PPD_KN_T", "200").split(",")]
     shapes = [(28672, 4096), (4096, 14336), (6144, 4096)]
-    ppd.check(L.ppd_set_tuning(b"ops_w_tiled", 1))
     for N, K in shapes:
         wbytes = N * K * 2
         ncopy = max(2, -(-400_000_000 // wbytes))
-        Ws = []
-        for _ in range(ncopy):
-            W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
-            Wt = torch.empty_like(W)
-            ppd.check(L.ppd_op_tile_matrix(W.data_ptr(), Wt.data_ptr(), N, K, None))
-            Ws.append(Wt)
-            del W
+        Ws = [(torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16) for _ in range(ncopy)]
         for T in ts:
             A = torch.randn(T, K, device="cuda").to(torch.bfloat16)
             C = torch.empty(8, T, N, device="cuda")

@@ -14,7 +14,8 @@ from tools.gemm_sweep import t_us  # noqa: E402
 
 def main():
     L = ppd.lib()
-    for T in (1024, 1536, 2048, 4096):
+    Ts = [int(x) for x in os.environ.get("PPD_PF_T", "1024,1224,2048,4096").split(",")]
+    for T in Ts:
         for N, K in ((6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)):
             A = torch.randn(T, K, device="cuda").to(torch.bfloat16)
             B = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)

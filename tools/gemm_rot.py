@@ -39,17 +39,10 @@ def main():
         wbytes = N * K * 2
         ncopy = max(2, -(-400_000_000 // wbytes))
         Ws = [(torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16) for _ in range(ncopy)]
-        tiled = os.environ.get("PPD_ROT_TILED", "0") == "1"
-        if tiled:  # the model's storage layout on the tcgen05 path
-            for W in Ws:
-                Wt = torch.empty_like(W)
-                ppd.check(L.ppd_op_tile_matrix(W.data_ptr(), Wt.data_ptr(), N, K, None))
-                W.copy_(Wt)
-        ppd.check(L.ppd_set_tuning(b"ops_w_tiled", 1 if tiled else 0))
         for T in ts:
             A = torch.randn(T, K, device="cuda").to(torch.bfloat16)
             C = torch.empty(8, T, N, device="cuda")
-            res = {"T": T, "N": N, "K": K, "tiled": tiled}
+            res = {"T": T, "N": N, "K": K}
             for name in modes:
                 pair, sched = MODES[name]
                 ppd.check(L.ppd_set_tuning(b"gemm_pair", pair))

@@ -14,7 +14,8 @@ for pair in filter(None, kv.split(",")):
     k, v = pair.split("=")
     lib.ppd_set_tuning.argtypes = [ctypes.c_char_p, i32]
     assert lib.ppd_set_tuning(k.encode(), int(v)) == 0
-T = 200
+import os
+T = int(os.environ.get("PPD_ONE_T", "200"))
 A = torch.randn(T, K, device="cuda").to(torch.bfloat16)
 B = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
 C = torch.empty(sp, T, N, device="cuda")
