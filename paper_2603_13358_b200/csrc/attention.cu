@@ -652,19 +652,25 @@ __global__ void __launch_bounds__(kThreads, 2)
 // ===========================================================================
 // K2: ONE launch for a mixed decode + (append-)prefill step.
 //
-// The first n_pf CTAs are tcgen05 prefill CTAs: warps 0-7 run the K3/K4 tile
-// (attention_tc_body.cuh) over tiles t = blockIdx.x, +n_pf, ... (tiles come
-// longest first), re-arming their mbarriers per tile; TMEM is allocated once.
-// Every other CTA runs TWO decode instances (warps 0-4 and 5-9, each its own
-// smem ring and named barriers) over the balanced decode schedule the host
-// cut for 2 x (gridDim.x - n_pf) virtual CTAs. HBM-bound decode streaming
-// and tensor-core-bound prefill tiles run concurrently on disjoint SMs of
-// the same launch, so the append prefill rides inside the decode step.
+// CTAs [0, n_pf) start on the prefill queue: the K3/K4 tcgen05 tile of
+// attention_tc_body.cuh on warps 0-7 (TMEM allocated on entering the mode,
+// mbarriers re-armed per tile), tiles pulled longest first with an atomic.
+// Every other CTA runs TWO decode instances (warps 0-4 and 5-9, own smem
+// ring and named barriers) over its two virtual CTAs of the balanced decode
+// schedule (static: the host cut it for 2 x (gridDim.x - n_pf) instances, so
+// the memory pipe streams without queue round trips), then joins the prefill
+// queue. HBM-bound decode streaming and tensor-core-bound prefill tiles run
+// concurrently on disjoint SMs; what prefill work is left when decode ends is
+// shared by every SM. Queue head + done counter live in p.mix_ctr[0..1]; the
+// last CTA out resets them for the next launch.
 // ===========================================================================
 namespace {
 constexpr int kMixThreads = 2 * kThreads;  // 320
 constexpr int kDecSmemInst = (kDecSmem - 1024 + 1023) / 1024 * 1024;
 constexpr int kMixSmem = pftc::kSmem > 1024 + 2 * kDecSmemInst ? pftc::kSmem : 1024 + 2 * kDecSmemInst;
+constexpr int kMixBarAll = 1;   // all 320 threads: mode switch
+constexpr int kMixBarPf = 2;    // prefill warps 0-7
+constexpr int kMixBarDec = 3;   // decode instance i: 3 + i (160 threads), consumers 5 + i (128)
 }  // namespace
 
 __global__ void __launch_bounds__(kMixThreads, 1)
@@ -672,38 +678,52 @@ __global__ void __launch_bounds__(kMixThreads, 1)
                            int n_pf, int n_pf_tiles, int n_vcta) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ int s_next;
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if ((int)blockIdx.x < n_pf) {
-    if (warp >= 8) return;  // the prefill role uses 8 warps (named barrier 1, 256 threads)
-    const pftc::Smem S(smem);
-    if (threadIdx.x == 0) pftc::init_barriers(S, false);
-    if (warp == 2) tc::alloc(S.tmem_slot, pftc::kTmemCols);
-    tc::fence_before();
-    named_barrier_sync(1, pftc::kThreads);
-    tc::fence_after();
-    const uint32_t tmem = *S.tmem_slot;
-    for (int t = blockIdx.x; t < n_pf_tiles; t += n_pf) {
-      if (t != (int)blockIdx.x) {  // previous tile fully retired (its epilogue waited on o_done)
-        tc::fence_before();
-        named_barrier_sync(1, pftc::kThreads);
-        if (threadIdx.x == 0) pftc::init_barriers(S, true);
-        named_barrier_sync(1, pftc::kThreads);
-        tc::fence_after();
-      }
-      const AttnItem it = pf_items[t / p.n_kv_heads];
-      pftc::tile(&kv_map, p, S, it, t % p.n_kv_heads, tmem, warp, lane, t + n_pf >= n_pf_tiles);
-    }
-    tc::fence_before();
-    named_barrier_sync(1, pftc::kThreads);
-    if (warp == 2) tc::dealloc(tmem, pftc::kTmemCols);
-    return;
+  if ((int)blockIdx.x >= n_pf) {
+    // ---------------- decode: two static virtual CTAs, then help with prefill
+    const int inst = threadIdx.x / kThreads;
+    const int lt = threadIdx.x - inst * kThreads;
+    const int v = ((int)blockIdx.x - n_pf) * 2 + inst;
+    if (v < n_vcta)
+      decode_body(&kv_map, p, smem + inst * kDecSmemInst, v, lt >> 5, lt & 31, kMixBarDec + inst,
+                  kMixBarDec + 2 + inst);
+    named_barrier_sync(kMixBarAll, kMixThreads);  // both instances retired: smem free
   }
-  const int inst = threadIdx.x / kThreads;
-  const int vcta = ((int)blockIdx.x - n_pf) * 2 + inst;
-  if (vcta >= n_vcta) return;
-  const int lt = threadIdx.x - inst * kThreads;
-  decode_body(&kv_map, p, smem + inst * kDecSmemInst, vcta, lt >> 5, lt & 31, 2 + inst, 4 + inst);
+  if (warp < 8) {
+    // ---------------- prefill queue (warps 0-7)
+    const pftc::Smem S(smem);
+    bool first = true;
+    for (;;) {
+      if (threadIdx.x == 0) s_next = atomicAdd(p.mix_ctr, 1);
+      tc::fence_before();
+      named_barrier_sync(kMixBarPf, pftc::kThreads);  // previous tile retired; next index published
+      tc::fence_after();
+      const int t = s_next;
+      if (t >= n_pf_tiles) break;
+      if (first && warp == 2) tc::alloc(S.tmem_slot, pftc::kTmemCols);
+      if (threadIdx.x == 0) pftc::init_barriers(S, !first);
+      tc::fence_before();
+      named_barrier_sync(kMixBarPf, pftc::kThreads);
+      tc::fence_after();
+      first = false;
+      const uint32_t tmem = *S.tmem_slot;
+      const AttnItem it = pf_items[t / p.n_kv_heads];
+      pftc::tile(&kv_map, p, S, it, t % p.n_kv_heads, tmem, warp, lane, false);
+    }
+    if (!first && warp == 2) tc::dealloc(*S.tmem_slot, pftc::kTmemCols);
+    // last CTA out resets the queue for the next launch (next layer / step)
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(p.mix_ctr + 1, 1) == (int)gridDim.x - 1) {
+        p.mix_ctr[0] = 0;
+        p.mix_ctr[1] = 0;
+        __threadfence();
+      }
+    }
+  }
+  pdl_trigger();
 }
 
 cudaError_t launch_mixed_attention(const void* kv_map, const AttnParams& p, const AttnItem* pf_items, int n_pf,
@@ -713,7 +733,7 @@ cudaError_t launch_mixed_attention(const void* kv_map, const AttnParams& p, cons
     cudaFuncSetAttribute(mixed_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMixSmem);
     attr = true;
   }
-  if (p.group > kDecMaxG || n_pf <= 0 || n_pf > n_pf_tiles) return cudaErrorInvalidValue;
+  if (p.group > kDecMaxG || n_pf <= 0 || n_pf > n_pf_tiles || !p.mix_ctr) return cudaErrorInvalidValue;
   const int grid = n_pf + (n_vcta + 1) / 2;
   return launch_pdl(mixed_attention_kernel, dim3(grid), dim3(kMixThreads), kMixSmem, stream,
                     *reinterpret_cast<const CUtensorMap*>(kv_map), p, pf_items, n_pf, n_pf_tiles, n_vcta);

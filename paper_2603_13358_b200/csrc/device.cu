@@ -291,27 +291,24 @@ void balance_decode(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_he
   items.insert(items.end(), rest.begin(), rest.end());
 }
 
-// K2 split of the 148 SMs for a mixed decode + prefill step (one launch,
-// mixed_attention_kernel): n_pf SMs run the prefill tiles, the rest two
-// decode instances each. Cost model (B200 measurements of the standalone
-// kernels): decode streams its K/V at min(5.6 TB/s, 44 GB/s per SM); a prefill
-// tile costs ~3 us per 128-key block on one SM (QK^T + PV at ~400 TF/s chip
-// wide). Picks n_pf minimising the later finisher; tiles are dealt round robin
-// longest first. Returns 0 (no fusion) when either side is empty.
+// K2 (mixed_attention_kernel) SM split: n_pf CTAs start on the prefill queue,
+// the decode schedule is cut for the other 148 - n_pf SMs (two instances
+// each) and those join the prefill queue when their decode work is done.
+// Cost model (B200, tools/ab_step.py PPD_AB_MIX sweeps of attn_pf_ctas):
+// decode streams min(5.6 TB/s, 44 GB/s per SM); a tile inside this launch
+// costs ~4 us + 6 us per 128-key block on one SM; prefill work left at the
+// end of decode is shared by all 148 SMs.
 int plan_mixed_split(double dec_bytes, const std::vector<double>& tile_cost) {
   const int n_tiles = (int)tile_cost.size();
   if (dec_bytes <= 0 || n_tiles == 0) return 0;
+  double pf = 0;
+  for (double c : tile_cost) pf += c;
   int best = 1;
   double best_t = 1e30;
   for (int n_pf = 1; n_pf <= std::min(n_tiles, 146); ++n_pf) {
-    double t_pf = 0;
-    for (int c = 0; c < n_pf; ++c) {
-      double t = 0;
-      for (int i = c; i < n_tiles; i += n_pf) t += tile_cost[i];
-      t_pf = std::max(t_pf, t);
-    }
-    const double bw = std::min(5.6e12, (148 - n_pf) * 44e9);
-    const double t = std::max(t_pf, dec_bytes / bw);
+    const double t_dec = dec_bytes / std::min(5.6e12, (148 - n_pf) * 44e9);
+    const double rest = std::max(0.0, pf - n_pf * t_dec);
+    const double t = t_dec + rest / 148 + (rest > 0 ? tile_cost[0] : 0.0);  // + one tile of tail
     if (t < best_t * 0.999) {
       best_t = t;
       best = n_pf;
@@ -321,6 +318,7 @@ int plan_mixed_split(double dec_bytes, const std::vector<double>& tile_cost) {
 }
 
 bool g_attn_fused = true;  // tuning "attn_fused": K2 one-launch mixed attention
+int g_attn_pf_ctas = 0;    // tuning "attn_pf_ctas": force the K2 prefill CTA count (0 = cost model)
 
 // The attention work of one step: decode items (balanced schedule), prefill
 // tiles (longest first) and, for a mixed step, the K2 SM split n_pf.
@@ -339,12 +337,12 @@ void plan_attention(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_he
     for (size_t i = n_dec; i < items.size(); ++i) {
       const AttnItem& it = items[i];
       const double blocks = (ctx[it.seq] + it.q_tok0 + it.n_q + 127) / 128;
-      for (int h = 0; h < n_kv_heads; ++h) cost.push_back(3.0e-6 * blocks);
+      for (int h = 0; h < n_kv_heads; ++h) cost.push_back(4.0e-6 + 6.0e-6 * blocks);
     }
     double dec_bytes = 0;
     for (int s = 0; s < n; ++s)
       if (q_len[s] == 1) dec_bytes += (double)(ctx[s] + 1) * n_kv_heads * 2 * 128 * 2;
-    n_pf = plan_mixed_split(dec_bytes, cost);
+    n_pf = g_attn_pf_ctas > 0 ? std::min<int>(g_attn_pf_ctas, (int)cost.size()) : plan_mixed_split(dec_bytes, cost);
   }
   balance_decode(n, q_len, ctx, n_kv_heads, items, n_ws, n_dec, seg_start, n_pf > 0 ? 2 * (148 - n_pf) : 296);
   if (seg_start.empty()) n_pf = 0;
@@ -473,7 +471,7 @@ int pack_batch(ppd_dev* d, const ppd_batch* b, StepLayout& L, std::vector<AttnIt
 int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf16* out,
                   const int* d_qstart, const int* d_ctx, const int* d_bt, int maxb,
                   const AttnItem* d_items, int n_dec, int n_items, const int* d_seg, int n_cta, int n_pf, int layer,
-                  float* ws_o, float* ws_ml, int* counters, cudaStream_t s) {
+                  float* ws_o, float* ws_ml, int* counters, int* mix_ctr, cudaStream_t s) {
   AttnParams p{};
   p.seg_start = d_seg;
   p.items = d_items;
@@ -492,6 +490,7 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   p.ws_o = ws_o;
   p.ws_ml = ws_ml;
   p.counters = counters;
+  p.mix_ctr = mix_ctr;
   // K2: a mixed step is ONE launch (prefill CTAs + decode CTAs)
   if (n_pf > 0) {
     CU(launch_mixed_attention(kv_map, p, d_items + n_dec, n_pf, (n_items - n_dec) * c.n_kv_heads, n_cta, s));
@@ -582,7 +581,8 @@ int forward(ppd_dev* d, const StepLayout& L) {
                             l, d->bt, s));
     PROF(0, false);
     int rc = (g_diag_skip & 2) ? 0 : run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items,
-                           at<int>(m, L.off_seg), L.n_cta, L.n_pf, l, d->ws_o, d->ws_ml, d->counters, s);
+                           at<int>(m, L.off_seg), L.n_cta, L.n_pf, l, d->ws_o, d->ws_ml, d->counters,
+                           d->counters + (size_t)d->max_S * c.n_kv_heads, s);
     if (rc) return rc;
     PROF(0, true);
     PROF(1, false);
@@ -629,8 +629,9 @@ int alloc_workspaces(ppd_dev* d) {
   CU(cudaMalloc(&d->gu32, Tp * 2 * c.d_ff * 4));
   CU(cudaMalloc(&d->down32, Tp * c.d_model * 4));
   CU(cudaMalloc(&d->logits, S * c.vocab * 4));
-  CU(cudaMalloc(&d->counters, S * c.n_kv_heads * 4));
-  CU(cudaMemset(d->counters, 0, S * c.n_kv_heads * 4));
+  // split-merge counters [S][Hkv] + the K2 queue heads / done counter [4]
+  CU(cudaMalloc(&d->counters, (S * c.n_kv_heads + 4) * 4));
+  CU(cudaMemset(d->counters, 0, (S * c.n_kv_heads + 4) * 4));
   CU(cudaMallocHost(&d->h_tokens_out, S * 4));
   CU(cudaMalloc(&d->d_tokens_out, S * 4));
   // RoPE cos/sin table, built in double on the host (same recipe as the oracle)
@@ -1025,8 +1026,8 @@ int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_poo
   CU(cudaMalloc(&dm, bytes));
   CU(cudaMalloc(&ws_o, (size_t)std::max(n_ws, 1) * cfg->n_kv_heads * G * 128 * 4));
   CU(cudaMalloc(&ws_ml, (size_t)std::max(n_ws, 1) * cfg->n_kv_heads * G * 2 * 4));
-  CU(cudaMalloc(&ctr, (size_t)n_seqs * cfg->n_kv_heads * 4));
-  CU(cudaMemset(ctr, 0, (size_t)n_seqs * cfg->n_kv_heads * 4));
+  CU(cudaMalloc(&ctr, ((size_t)n_seqs * cfg->n_kv_heads + 4) * 4));
+  CU(cudaMemset(ctr, 0, ((size_t)n_seqs * cfg->n_kv_heads + 4) * 4));
   int* d_qs = reinterpret_cast<int*>(dm);
   int* d_ctx = d_qs + n_seqs + 1;
   int* d_bt = d_ctx + n_seqs;
@@ -1038,7 +1039,8 @@ int ppd_op_attention(const ppd_model_cfg* cfg, const void* q, const void* kv_poo
   int* d_seg = reinterpret_cast<int*>(d_items + items.size());
   if (!seg_start.empty()) CU(cudaMemcpy(d_seg, seg_start.data(), seg_start.size() * 4, cudaMemcpyHostToDevice));
   rc = run_attention(*cfg, map, static_cast<const bf16*>(q), static_cast<bf16*>(out), d_qs, d_ctx,
-                     d_bt, max_blocks, d_items, n_dec, (int)items.size(), d_seg, n_cta, n_pf, layer, ws_o, ws_ml, ctr, s);
+                     d_bt, max_blocks, d_items, n_dec, (int)items.size(), d_seg, n_cta, n_pf, layer, ws_o, ws_ml, ctr,
+                     ctr + (size_t)n_seqs * cfg->n_kv_heads, s);
   cudaStreamSynchronize(s);
   cudaFree(dm);
   cudaFree(ws_o);
@@ -1111,6 +1113,9 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "diag_skip") == 0) {
     CHECK_ARG(value >= 0 && value <= 7, "diag_skip must be in [0, 7]");
     g_diag_skip = value;
+  } else if (std::strcmp(name, "attn_pf_ctas") == 0) {
+    CHECK_ARG(value >= 0 && value <= 146, "attn_pf_ctas must be in [0, 146]");
+    g_attn_pf_ctas = value;
   } else if (std::strcmp(name, "attn_fused") == 0) {
     CHECK_ARG(value == 0 || value == 1, "attn_fused must be 0 or 1");
     g_attn_fused = value != 0;

@@ -41,6 +41,7 @@ struct AttnParams {
   int* counters;             // [n_seqs][Hkv], zero-initialised, self-resetting
   // balanced decode schedule: CTA c owns decode segments [seg_start[c], seg_start[c+1])
   const int* seg_start;
+  int* mix_ctr;              // K2 queue heads + done counter [3], zero-initialised, self-resetting
 };
 
 // Persistent decode attention over balanced key segments (kv head in item.pad[0]).
@@ -50,9 +51,10 @@ cudaError_t launch_decode_attention(const void* kv_map, const AttnParams& p, int
 int make_kv_tensor_map(void* map_out /* CUtensorMap, 128 B */, const void* pool, uint64_t total_rows);
 cudaError_t launch_paged_attention(const void* kv_map, const AttnParams& p, int n_items,
                                    cudaStream_t stream);
-// K2 fused mixed step: n_pf tcgen05 prefill CTAs over n_pf_tiles = (prefill
-// items at pf_items) x n_kv_heads tiles + the balanced decode schedule of
-// n_vcta virtual CTAs (two per CTA), one launch
+// K2 fused mixed step, one persistent launch of 148 CTAs pulling from two
+// queues: n_pf_tiles = (prefill items at pf_items) x n_kv_heads tcgen05 tiles
+// (n_pf CTAs start there) and the balanced decode schedule's n_vcta virtual
+// CTAs (two decode instances per CTA)
 cudaError_t launch_mixed_attention(const void* kv_map, const AttnParams& p, const AttnItem* pf_items, int n_pf,
                                    int n_pf_tiles, int n_vcta, cudaStream_t stream);
 // tcgen05/TMEM prefill tiles (kind 1 items of 128/G tokens)
