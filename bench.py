@@ -139,7 +139,7 @@ def engine_ttft(gpus, layout: str, quick: bool = False):
     if layout in ("1P_1D", "1R"):
         # BASELINE configs[2]: 4 turns, +2048 tokens of context per turn (1536 in, 512 out)
         wl = {"id": "cfg3", "turn1": [1536, 512], "turn2plus": [1536, 512], "num_turns": 4,
-              "qps": 1.0, "duration_s": 4.0 if quick else 8.0}
+              "qps": 1.0, "duration_s": 4.0 if quick else 12.0}
     else:
         wl = {"id": "cfg4", "turn1": [2048, 128], "turn2plus": [1024, 128], "num_turns": 3,
               "qps": 8.0, "duration_s": 4.0 if quick else 8.0}
@@ -166,6 +166,43 @@ def engine_ttft(gpus, layout: str, quick: bool = False):
     if p0 and p1:
         out["ttft_t2_p50_reduction"] = 1.0 - p1 / p0
     return out
+
+
+def qwen_long_decode(local_rank, B=16, ctx0=16384, K=5, W=3):
+    """BASELINE configs[4]'s model on one GPU: Qwen2.5-32B-shape (GQA 40/8,
+    QKV bias, random-init bf16, 65.5 GB of weights) decoding B sequences at a
+    16k-token context (the 'large' router class). KV filled with random bf16
+    (the step reads every byte regardless). Device time, CUDA events."""
+    import paper_2603_13358_b200 as ppd
+    cfg = ppd.qwen32b_cfg()
+    BT = 16
+    bps = (ctx0 + W + K + BT) // BT + 1
+    dev = ppd.Device(local_rank, cfg, max_step_tokens=256, max_step_seqs=max(B, 8))
+    try:
+        dev.load_random_weights(SEED)
+        dev.kv_pool_init(B * bps)
+        ptr, nbytes = dev.kv_pool_ptr()
+        ppd.check(ppd.lib().ppd_op_fill_random(ptr, nbytes // 2, SEED, 99, 0, None))
+        bts = np.arange(B * bps, dtype=np.int32).reshape(B, bps)
+        ctx = np.full(B, ctx0, dtype=np.int32)
+        tok = np.random.default_rng(SEED).integers(0, cfg.vocab, B).astype(np.int32)
+        ms = []
+        for i in range(W + K):
+            r = dev.step([1] * B, ctx, tok, bts)
+            tok = r.tokens
+            ctx += 1
+            if i >= W:
+                ms.append(r.ms)
+        t = float(np.mean(ms))
+        kv_bytes = float(np.sum(ctx - 1)) * 262144
+        w_bytes = 65.5e9
+        pk, _ = peaks()
+        return {"model": "qwen2.5-32b-shape (random init, QKV bias, GQA 40/8)", "batch": B, "ctx": ctx0,
+                "tpot_ms": t, "tok_s": B / (t * 1e-3), "step_bytes": kv_bytes + w_bytes,
+                "step_hbm_gbs": (kv_bytes + w_bytes) / (t * 1e-3) / 1e9,
+                "step_hbm_frac": (kv_bytes + w_bytes) / (t * 1e-3) / 1e9 / pk["hbm_gbs"], "steps": K}
+    finally:
+        dev.close()
 
 
 def cpu_threads():
@@ -297,6 +334,9 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()  # rank 0 drives all GPUs for the engine runs
         return
+    qwen = None
+    if not args.no_qwen and not args.quick:
+        qwen = qwen_long_decode(local_rank)
     ttft = None
     if not args.no_engine:
         from paper_2603_13358_b200 import dist as D
@@ -352,6 +392,7 @@ def run_ours(args, rank, world, local_rank):
         "tpot_ms": dev_ms_max / K,
         "interference": inter,
         "ttft_pd_vs_ppd": ttft,
+        "qwen32b_long_decode": qwen,
         "roofline": {
             "kernel": "decode_attention_kernel (K1, balanced persistent paged decode attention)",
             "bound": "hbm",
@@ -433,6 +474,7 @@ def main():
     ap.add_argument("--fill-kv", default="prefill", choices=["prefill", "random"])
     ap.add_argument("--no-engine", action="store_true")
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--no-qwen", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
