@@ -128,7 +128,7 @@ def cpu_port_decode(batch: int, ctx: int, layers_full: int, n_rep: int = 1):
     return batch / t_full, sample, t_sum
 
 
-def engine_ttft(gpus, layout: str, quick: bool = False):
+def engine_ttft(gpus, layout: str, quick: bool = False, qps: float = None):
     """Turn-2+ TTFT / TPOT, PD (x=0) vs PPD (x=1), through the host C++ engine
     on the DEVICE clock: every prefill chunk, decode iteration and P->D KV hop
     runs on the GPUs listed (node i -> gpus[i]); each node's clock advances by
@@ -139,7 +139,7 @@ def engine_ttft(gpus, layout: str, quick: bool = False):
     if layout in ("1P_1D", "1R"):
         # BASELINE configs[2]: 4 turns, +2048 tokens of context per turn (1536 in, 512 out)
         wl = {"id": "cfg3", "turn1": [1536, 512], "turn2plus": [1536, 512], "num_turns": 4,
-              "qps": 1.0, "duration_s": 4.0 if quick else 12.0}
+              "qps": qps or 1.0, "duration_s": 4.0 if quick else 12.0}
     else:
         wl = {"id": "cfg4", "turn1": [2048, 128], "turn2plus": [1024, 128], "num_turns": 3,
               "qps": 8.0, "duration_s": 4.0 if quick else 8.0}
@@ -341,7 +341,9 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_engine:
         from paper_2603_13358_b200 import dist as D
         if world == 1:
-            ttft = [engine_ttft([local_rank, local_rank], "1P_1D", quick=args.quick)]
+            # configs[2] at two loads of the SURVEY §8d C3 QPS sweep
+            ttft = [engine_ttft([local_rank, local_rank], "1P_1D", quick=args.quick, qps=q)
+                    for q in ((1.0,) if args.quick else (1.0, 2.0))]
         else:
             ttft = [engine_ttft(D.layout_gpus(lay, world), lay, quick=args.quick) for lay in D.node_layouts(world)]
 
