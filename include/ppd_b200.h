@@ -170,6 +170,9 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
  *                  CTAs per SM with half-depth rings
  *   "attn_fused"   1 (default): a mixed decode + prefill step runs its
  *                  attention as ONE launch (K2); 0: decode and prefill launches
+ *   "attn_pf_ctas" K2 prefill CTA count (0 = cost model, default)
+ *   "attn_pf_persist" 1 (default): pure prefill steps run a persistent
+ *                  tcgen05 kernel over an atomic tile queue; 0: one CTA per tile
  * Unknown names -> PPD_ERR_INVALID. Every change makes devices re-capture
  * their step graphs with the newly selected kernels. */
 int ppd_set_tuning(const char* name, int32_t value);

@@ -691,38 +691,9 @@ __global__ void __launch_bounds__(kMixThreads, 1)
                   kMixBarDec + 2 + inst);
     named_barrier_sync(kMixBarAll, kMixThreads);  // both instances retired: smem free
   }
-  if (warp < 8) {
-    // ---------------- prefill queue (warps 0-7)
-    const pftc::Smem S(smem);
-    bool first = true;
-    for (;;) {
-      if (threadIdx.x == 0) s_next = atomicAdd(p.mix_ctr, 1);
-      tc::fence_before();
-      named_barrier_sync(kMixBarPf, pftc::kThreads);  // previous tile retired; next index published
-      tc::fence_after();
-      const int t = s_next;
-      if (t >= n_pf_tiles) break;
-      if (first && warp == 2) tc::alloc(S.tmem_slot, pftc::kTmemCols);
-      if (threadIdx.x == 0) pftc::init_barriers(S, !first);
-      tc::fence_before();
-      named_barrier_sync(kMixBarPf, pftc::kThreads);
-      tc::fence_after();
-      first = false;
-      const uint32_t tmem = *S.tmem_slot;
-      const AttnItem it = pf_items[t / p.n_kv_heads];
-      pftc::tile(&kv_map, p, S, it, t % p.n_kv_heads, tmem, warp, lane, false);
-    }
-    if (!first && warp == 2) tc::dealloc(*S.tmem_slot, pftc::kTmemCols);
-    // last CTA out resets the queue for the next launch (next layer / step)
-    if (threadIdx.x == 0) {
-      __threadfence();
-      if (atomicAdd(p.mix_ctr + 1, 1) == (int)gridDim.x - 1) {
-        p.mix_ctr[0] = 0;
-        p.mix_ctr[1] = 0;
-        __threadfence();
-      }
-    }
-  }
+  if (warp < 8)  // ---------------- prefill queue (warps 0-7)
+    pftc::tile_queue(&kv_map, p, smem, pf_items, n_pf_tiles, warp, lane, kMixBarPf, p.mix_ctr, p.mix_ctr + 1,
+                     gridDim.x, &s_next);
   pdl_trigger();
 }
 

@@ -42,6 +42,37 @@ __global__ void __launch_bounds__(pftc::kThreads, 1)
   if (warp == 2) tc::dealloc(tmem, pftc::kTmemCols);
 }
 
+// Pure prefill steps: min(148, tiles) persistent CTAs pull the tiles (longest
+// first) from an atomic queue, so a chunk's 2-3 waves of uneven causal tiles
+// leave no idle SMs at the tail.
+__global__ void __launch_bounds__(pftc::kThreads, 1)
+    prefill_attention_persistent_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p,
+                                        const AttnItem* items, int n_tiles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ int s_next;
+  pdl_wait();
+  pftc::tile_queue(&kv_map, p, smem, items, n_tiles, threadIdx.x >> 5, threadIdx.x & 31, 1, p.mix_ctr,
+                   p.mix_ctr + 1, gridDim.x, &s_next);
+  pdl_trigger();
+}
+
+cudaError_t launch_prefill_attention_persistent(const void* kv_map, const AttnParams& p, const AttnItem* items,
+                                                int n_items, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(prefill_attention_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         pftc::kSmem);
+    attr = true;
+  }
+  const int n_tiles = n_items * p.n_kv_heads;
+  if (n_tiles == 0) return cudaSuccess;
+  if (!p.mix_ctr) return cudaErrorInvalidValue;
+  const int grid = n_tiles < 148 ? n_tiles : 148;
+  return launch_pdl(prefill_attention_persistent_kernel, dim3(grid), dim3(pftc::kThreads), pftc::kSmem, stream,
+                    *reinterpret_cast<const CUtensorMap*>(kv_map), p, items, n_tiles);
+}
+
 cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p, int n_items, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {

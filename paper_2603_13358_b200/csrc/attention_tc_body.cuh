@@ -288,5 +288,42 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
   }
 }
 
+// Persistent prefill role: warps 0..7 of the calling CTA pull tiles t from the
+// atomic queue q (tiles are items[t / Hkv] x kv head t % Hkv, longest first),
+// allocating TMEM on the first tile and re-arming the mbarriers per tile.
+// bar: a named barrier id for the 256 prefill threads. `done` (CTA count)
+// resets the queue once every CTA of the launch has left it.
+PPD_DEV void tile_queue(const CUtensorMap* kv_map, const AttnParams& p, uint8_t* smem, const AttnItem* items,
+                        int n_tiles, int warp, int lane, int bar, int* q, int* done, int n_ctas, int* s_next) {
+  const Smem S(smem);
+  const int tid = warp * 32 + lane;
+  bool first = true;
+  for (;;) {
+    if (tid == 0) *s_next = atomicAdd(q, 1);
+    tc::fence_before();
+    named_barrier_sync(bar, kThreads);  // previous tile retired; next index published
+    tc::fence_after();
+    const int t = *s_next;
+    if (t >= n_tiles) break;
+    if (first && warp == 2) tc::alloc(S.tmem_slot, kTmemCols);
+    if (tid == 0) init_barriers(S, !first);
+    tc::fence_before();
+    named_barrier_sync(bar, kThreads);
+    tc::fence_after();
+    first = false;
+    const AttnItem it = items[t / p.n_kv_heads];
+    tile(kv_map, p, S, it, t % p.n_kv_heads, *S.tmem_slot, warp, lane, false);
+  }
+  if (!first && warp == 2) tc::dealloc(*S.tmem_slot, kTmemCols);
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1) == n_ctas - 1) {  // last CTA out resets the queue for the next launch
+      *q = 0;
+      *done = 0;
+      __threadfence();
+    }
+  }
+}
+
 }  // namespace pftc
 }  // namespace ppdk

@@ -318,7 +318,8 @@ int plan_mixed_split(double dec_bytes, const std::vector<double>& tile_cost) {
 }
 
 bool g_attn_fused = true;  // tuning "attn_fused": K2 one-launch mixed attention
-int g_attn_pf_ctas = 0;    // tuning "attn_pf_ctas": force the K2 prefill CTA count (0 = cost model)
+int g_attn_pf_ctas = 0;          // tuning "attn_pf_ctas": force the K2 prefill CTA count (0 = cost model)
+bool g_attn_pf_persist = true;  // tuning "attn_pf_persist": persistent tile queue for pure prefill steps
 
 // The attention work of one step: decode items (balanced schedule), prefill
 // tiles (longest first) and, for a mixed step, the K2 SM split n_pf.
@@ -328,6 +329,12 @@ void plan_attention(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_he
   seg_start.clear();
   n_pf = 0;
   if (!decode_persistent_enabled(G)) return;
+  if (attention_tc_enabled() && g_attn_pf_persist && n_dec == 0 && !items.empty()) {
+    // pure prefill step: longest tiles first for the persistent tile queue
+    std::stable_sort(items.begin(), items.end(), [&](const AttnItem& a, const AttnItem& b) {
+      return ctx[a.seq] + a.q_tok0 + a.n_q > ctx[b.seq] + b.q_tok0 + b.n_q;
+    });
+  }
   if (attention_tc_enabled() && g_attn_fused && n_dec > 0 && (int)items.size() > n_dec) {
     // longest prefill tiles first (round-robin dealing in mixed_attention_kernel)
     std::stable_sort(items.begin() + n_dec, items.end(), [&](const AttnItem& a, const AttnItem& b) {
@@ -505,7 +512,10 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   if (n_items > n_dec) {
     if (attention_tc_enabled()) {
       p.items = d_items + n_dec;
-      CU(launch_prefill_attention_tc(kv_map, p, n_items - n_dec, s));
+      if (n_dec == 0 && g_attn_pf_persist)
+        CU(launch_prefill_attention_persistent(kv_map, p, d_items, n_items, s));
+      else
+        CU(launch_prefill_attention_tc(kv_map, p, n_items - n_dec, s));
     } else if (n_cta > 0) {
       p.items = d_items + n_dec;
       CU(launch_paged_attention(kv_map, p, n_items - n_dec, s));
@@ -1116,6 +1126,9 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "attn_pf_ctas") == 0) {
     CHECK_ARG(value >= 0 && value <= 146, "attn_pf_ctas must be in [0, 146]");
     g_attn_pf_ctas = value;
+  } else if (std::strcmp(name, "attn_pf_persist") == 0) {
+    CHECK_ARG(value == 0 || value == 1, "attn_pf_persist must be 0 or 1");
+    g_attn_pf_persist = value != 0;
   } else if (std::strcmp(name, "attn_fused") == 0) {
     CHECK_ARG(value == 0 || value == 1, "attn_fused must be 0 or 1");
     g_attn_fused = value != 0;

@@ -57,6 +57,10 @@ cudaError_t launch_paged_attention(const void* kv_map, const AttnParams& p, int 
 // CTAs (two decode instances per CTA)
 cudaError_t launch_mixed_attention(const void* kv_map, const AttnParams& p, const AttnItem* pf_items, int n_pf,
                                    int n_pf_tiles, int n_vcta, cudaStream_t stream);
+// persistent tcgen05 prefill: min(148, tiles) CTAs over an atomic tile queue
+// (items longest first; queue head / done counter in p.mix_ctr)
+cudaError_t launch_prefill_attention_persistent(const void* kv_map, const AttnParams& p, const AttnItem* items,
+                                                int n_items, cudaStream_t stream);
 // tcgen05/TMEM prefill tiles (kind 1 items of 128/G tokens)
 cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p, int n_items, cudaStream_t stream);
 

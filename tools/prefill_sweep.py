@@ -14,6 +14,9 @@ import paper_2603_13358_b200 as ppd  # noqa: E402
 
 
 def main():
+    for kv in filter(None, os.environ.get("PPD_PF_KNOBS", "").split(",")):
+        k, v = kv.split("=")
+        ppd.check(ppd.lib().ppd_set_tuning(k.encode(), int(v)))
     cfg = ppd.llama8b_cfg()
     dev = ppd.Device(0, cfg, max_step_tokens=8192, max_step_seqs=8)
     dev.load_random_weights(1)
@@ -43,7 +46,8 @@ def main():
                "gemm_ms": st["gemm_ms"] / 3,
                "attn_tflops": attn_flop / (st["attn_ms"] * 1e-3) / 1e12 if st["attn_ms"] else None,
                "gemm_tflops": lin / (st["gemm_ms"] * 1e-3) / 1e12 if st["gemm_ms"] else None,
-               "tc_attention": os.environ.get("PPD_ATTN_TC", "1") != "0"}
+               "tc_attention": os.environ.get("PPD_ATTN_TC", "1") != "0",
+               "knobs": os.environ.get("PPD_PF_KNOBS", "")}
         out.append(res)
         print(json.dumps(res), flush=True)
     dev.close()
