@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 // K2: ONE launch for a mixed decode + (append-)prefill step.
 //
 // CTAs [0, n_pf) start on the prefill queue: the K3/K4 tcgen05 tile of
-// attention_tc_body.cuh on warps 0-7 (TMEM allocated on entering the mode,
+// attention_tc_body.cuh on all 12 warps (TMEM allocated on entering the mode,
 // mbarriers re-armed per tile), tiles pulled longest first with an atomic.
 // Every other CTA runs TWO decode instances (warps 0-4 and 5-9, own smem
 // ring and named barriers) over its two virtual CTAs of the balanced decode
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 // last CTA out resets them for the next launch.
 // ===========================================================================
 namespace {
-constexpr int kMixThreads = 2 * kThreads;  // 320
+constexpr int kMixThreads = pftc::kThreads;  // 384: the prefill role's 12 warps (decode uses 10)
 constexpr int kDecSmemInst = (kDecSmem - 1024 + 1023) / 1024 * 1024;
 constexpr int kMixSmem = pftc::kSmem > 1024 + 2 * kDecSmemInst ? pftc::kSmem : 1024 + 2 * kDecSmemInst;
 constexpr int kMixBarAll = 1;   // all 320 threads: mode switch
@@ -686,13 +686,13 @@ __global__ void __launch_bounds__(kMixThreads, 1)
     const int inst = threadIdx.x / kThreads;
     const int lt = threadIdx.x - inst * kThreads;
     const int v = ((int)blockIdx.x - n_pf) * 2 + inst;
-    if (v < n_vcta)
+    if (inst < 2 && v < n_vcta)
       decode_body(&kv_map, p, smem + inst * kDecSmemInst, v, lt >> 5, lt & 31, kMixBarDec + inst,
                   kMixBarDec + 2 + inst);
     named_barrier_sync(kMixBarAll, kMixThreads);  // both instances retired: smem free
   }
-  if (warp < 8)  // ---------------- prefill queue (warps 0-7)
-    pftc::tile_queue(&kv_map, p, smem, pf_items, n_pf_tiles, warp, lane, kMixBarPf, p.mix_ctr, p.mix_ctr + 1,
+  // ---------------- prefill queue (all 12 warps)
+  pftc::tile_queue(&kv_map, p, smem, pf_items, n_pf_tiles, warp, lane, kMixBarPf, p.mix_ctr, p.mix_ctr + 1,
                      gridDim.x, &s_next);
   pdl_trigger();
 }

@@ -12,7 +12,8 @@
 namespace ppdk {
 namespace pftc {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;              // warps 0-3: K TMA / MMA / TMEM alloc / V TMA; 4-11: softmax
+constexpr int kSoftmaxWarps = 8;           // two threads per query row (64 key columns each)
 constexpr int kBT = 16;
 constexpr int kDh = 128;
 constexpr int kKeys = 128;                  // keys per block
@@ -20,7 +21,8 @@ constexpr int kTile = 32768;                // 128 x 128 bf16
 constexpr int kKStages = 3;                 // K ring: released as soon as S_j retires
 constexpr int kVStages = 2;                 // V ring: released after PV_j
 constexpr int kSmem = 1024 + kTile /*Q*/ + (kKStages + kVStages) * kTile + kTile /*P*/ + 256;
-constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kTmemCols = 512;        // S0 | S1 | O | row-half exchange (cols 384..)
+constexpr uint32_t kXchgCol = 384;
 constexpr float kRescaleThreshold = 8.0f;   // log2 domain
 constexpr int kNumBars = 15;
 
@@ -75,14 +77,14 @@ PPD_DEV void init_barriers(const Smem& S, bool reinit) {
     mbar_init(&S.v_empty[i], 1);
   }
   for (int i = 0; i < 2; ++i) mbar_init(&S.s_full[i], 1);
-  mbar_init(S.p_ready, 4);
+  mbar_init(S.p_ready, kSoftmaxWarps);
   mbar_init(S.o_done, 1);
-  mbar_init(S.q_ready, 4);
+  mbar_init(S.q_ready, kSoftmaxWarps);
   fence_barrier_init();
 }
 
 // One 128-row tile (128/G query tokens x the G query heads of kv head `kvh`)
-// of prefill item `it`, run by warps 0..7 of the calling CTA. Barriers are
+// of prefill item `it`, run by warps 0..11 of the calling CTA. Barriers are
 // freshly initialised; `tmem` holds kTmemCols columns (S0 | S1 | O).
 PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S, const AttnItem& it, int kvh,
                   uint32_t tmem, int warp, int lane, bool trigger_pdl) {
@@ -172,16 +174,23 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       }
     }
   } else if (warp >= 4) {
-    const int r = warp * 32 + lane - 128;  // query row == TMEM lane
+    // Softmax: 8 warps, two threads per query row. Warp w handles TMEM lane
+    // quarter w & 3 (row r) and key / O columns [64h, 64h + 64), h = (w - 4) / 4.
+    // The two halves of a row agree on its running max through free TMEM
+    // columns (one tcgen05.st / ld each way per block) and a 64-thread named
+    // barrier per lane quarter; l is kept per half and summed in the epilogue.
     const int q4 = warp & 3;
+    const int h = (warp - 4) >> 2;
+    const int r = q4 * 32 + lane;  // query row == TMEM lane
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
-    // ---- Q row -> shared (K-major, 128 B swizzle, two 64-dim atoms)
+    const int pair_bar = 8 + q4;
+    // ---- Q row half -> shared (K-major, 128 B swizzle: atom h holds dims [64h, 64h + 64))
     {
       const uint4* src = nullptr;
       if (r < rows)
         src = reinterpret_cast<const uint4*>(p.q + ((size_t)(q_base + it.q_tok0 + r / G) * p.n_q_heads + kvh * G + r % G) * kDh);
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
+      for (int c = 8 * h; c < 8 * h + 8; ++c) {
         const uint4 v = src ? src[c] : make_uint4(0, 0, 0, 0);
         *reinterpret_cast<uint4*>(q_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
       }
@@ -195,25 +204,52 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc::fence_after();
-      // one warp per SM sub-partition runs this: keep every reduction chain
-      // short (8 independent partial max / sum accumulators) and the four
-      // TMEM loads in flight together
-      uint32_t raw[kKeys];
-#pragma unroll
-      for (int c0 = 0; c0 < kKeys; c0 += 32) tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + c0, raw + c0);
+      uint32_t raw[64];
+      tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + 64 * h, raw);
+      tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + 64 * h + 32, raw + 32);
       tc::wait_ld();
-      float sv[kKeys];
-      const int key0 = j * kKeys;
+      float sv[64];
+      const int key0 = j * kKeys + 64 * h;
       float mxp[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) mxp[i] = -INFINITY;
+      if (key0 + 63 <= pos) {  // no causal mask inside this half block
 #pragma unroll
-      for (int c = 0; c < kKeys; ++c) {
-        sv[c] = (key0 + c <= pos) ? __uint_as_float(raw[c]) * sl2 : -INFINITY;
-        mxp[c & 7] = fmaxf(mxp[c & 7], sv[c]);
+        for (int c = 0; c < 64; ++c) {
+          sv[c] = __uint_as_float(raw[c]) * sl2;
+          mxp[c & 7] = fmaxf(mxp[c & 7], sv[c]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          sv[c] = (key0 + c <= pos) ? __uint_as_float(raw[c]) * sl2 : -INFINITY;
+          mxp[c & 7] = fmaxf(mxp[c & 7], sv[c]);
+        }
       }
-      const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+      const float mh = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
                              fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+      // exchange the half maxima: column kXchgCol + 2 * (j & 1) + h (parity-double-buffered)
+      {
+        uint32_t v = __float_as_uint(mh);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(
+                         tmem + lane_base + kXchgCol + 2 * (j & 1) + h),
+                     "r"(v)
+                     : "memory");
+        tc::wait_st();
+      }
+      tc::fence_before();
+      named_barrier_sync(pair_bar, 64);
+      tc::fence_after();
+      float mo;
+      {
+        uint32_t v;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                     : "=r"(v)
+                     : "r"(tmem + lane_base + kXchgCol + 2 * (j & 1) + (1 - h)));
+        tc::wait_ld();
+        mo = __uint_as_float(v);
+      }
+      const float mx = fmaxf(mh, mo);  // identical in both halves
       float alpha = 1.f;
       bool rescale = false;
       if (m == -INFINITY) {
@@ -226,28 +262,29 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       const float base = m == -INFINITY ? 0.f : m;
       // exp2 on two pipes: even keys on the SFU (ex2.approx), odd keys by a
       // degree-3 polynomial on the FMA pipe (max rel. error 8.6e-5 << bf16 ulp)
-      float rsp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[kKeys / 2];
+      float rsp[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < kKeys; c += 2) {
+      for (int c = 0; c < 64; c += 2) {
         const float p0 = ex2_sfu(sv[c] - base), p1 = ex2_poly(sv[c + 1] - base);
-        rsp[(c >> 1) & 7] += p0 + p1;
+        rsp[(c >> 1) & 3] += p0 + p1;
         pk[c >> 1] = pack2(p0, p1);
       }
-      const float rs = ((rsp[0] + rsp[1]) + (rsp[2] + rsp[3])) + ((rsp[4] + rsp[5]) + (rsp[6] + rsp[7]));
+      const float rs = (rsp[0] + rsp[1]) + (rsp[2] + rsp[3]);
       // P_{j-1} and O must have been consumed by PV_{j-1} before we overwrite / rescale
       if (j >= 1) {
         mbar_wait(o_done, (j - 1) & 1);
         tc::fence_after();
       }
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const uint4 v = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+      for (int cc = 0; cc < 8; ++cc) {
+        const int c = 8 * h + cc;  // 16-byte chunk of the row (atom h)
+        const uint4 v = make_uint4(pk[cc * 4], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
         *reinterpret_cast<uint4*>(p_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
       }
       if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
 #pragma unroll
-        for (int c0 = 0; c0 < kDh; c0 += 32) {
+        for (int c0 = 64 * h; c0 < 64 * h + 64; c0 += 32) {
           uint32_t o[32];
           tc::ld32x32(t_o + lane_base + c0, o);
           tc::wait_ld();
@@ -263,15 +300,34 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       __syncwarp();
       if (lane == 0) mbar_arrive(p_ready);
     }
-    // ---- epilogue: O / l -> bf16
+    // ---- epilogue: O / (l_0 + l_1) -> bf16, each half its 64 columns
     if (trigger_pdl) pdl_trigger();
+    {
+      uint32_t v = __float_as_uint(l);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + lane_base + kXchgCol + 4 + h),
+                   "r"(v)
+                   : "memory");
+      tc::wait_st();
+    }
+    tc::fence_before();
+    named_barrier_sync(pair_bar, 64);
+    tc::fence_after();
+    float lo;
+    {
+      uint32_t v;
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                   : "=r"(v)
+                   : "r"(tmem + lane_base + kXchgCol + 4 + (1 - h)));
+      tc::wait_ld();
+      lo = __uint_as_float(v);
+    }
     mbar_wait(o_done, (nblk - 1) & 1);
     tc::fence_after();
-    const float inv = 1.f / l;
+    const float inv = 1.f / (h == 0 ? l + lo : lo + l);  // same summation order in both halves
     bf16* dst = r < rows ? p.out + ((size_t)(q_base + it.q_tok0 + r / G) * p.n_q_heads + kvh * G + r % G) * kDh
                          : nullptr;
 #pragma unroll
-    for (int c0 = 0; c0 < kDh; c0 += 32) {
+    for (int c0 = 64 * h; c0 < 64 * h + 64; c0 += 32) {
       uint32_t o[32];
       tc::ld32x32(t_o + lane_base + c0, o);
       tc::wait_ld();
@@ -288,10 +344,10 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
   }
 }
 
-// Persistent prefill role: warps 0..7 of the calling CTA pull tiles t from the
+// Persistent prefill role: warps 0..11 of the calling CTA pull tiles t from the
 // atomic queue q (tiles are items[t / Hkv] x kv head t % Hkv, longest first),
 // allocating TMEM on the first tile and re-arming the mbarriers per tile.
-// bar: a named barrier id for the 256 prefill threads. `done` (CTA count)
+// bar: a named barrier id for the kThreads prefill threads. `done` (CTA count)
 // resets the queue once every CTA of the launch has left it.
 PPD_DEV void tile_queue(const CUtensorMap* kv_map, const AttnParams& p, uint8_t* smem, const AttnItem* items,
                         int n_tiles, int warp, int lane, int bar, int* q, int* done, int n_ctas, int* s_next) {
