@@ -208,6 +208,8 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + 64 * h, raw);
       tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + 64 * h + 32, raw + 32);
       tc::wait_ld();
+      // raw (unscaled) scores; the scale folds into the exponent's FFMA below
+      // (sl2 > 0: the max commutes with it)
       float sv[64];
       const int key0 = j * kKeys + 64 * h;
       float mxp[8];
@@ -216,18 +218,18 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       if (key0 + 63 <= pos) {  // no causal mask inside this half block
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
-          sv[c] = __uint_as_float(raw[c]) * sl2;
+          sv[c] = __uint_as_float(raw[c]);
           mxp[c & 7] = fmaxf(mxp[c & 7], sv[c]);
         }
       } else {
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
-          sv[c] = (key0 + c <= pos) ? __uint_as_float(raw[c]) * sl2 : -INFINITY;
+          sv[c] = (key0 + c <= pos) ? __uint_as_float(raw[c]) : -INFINITY;
           mxp[c & 7] = fmaxf(mxp[c & 7], sv[c]);
         }
       }
       const float mh = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
-                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7]))) * sl2;
       // exchange the half maxima: column kXchgCol + 2 * (j & 1) + h (parity-double-buffered)
       {
         uint32_t v = __float_as_uint(mh);
@@ -266,7 +268,7 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       uint32_t pk[32];
 #pragma unroll
       for (int c = 0; c < 64; c += 2) {
-        const float p0 = ex2_sfu(sv[c] - base), p1 = ex2_poly(sv[c + 1] - base);
+        const float p0 = ex2_sfu(fmaf(sv[c], sl2, -base)), p1 = ex2_poly(fmaf(sv[c + 1], sl2, -base));
         rsp[(c >> 1) & 3] += p0 + p1;
         pk[c >> 1] = pack2(p0, p1);
       }
