@@ -150,7 +150,7 @@ def engine_ttft(gpus, layout: str, quick: bool = False, qps: float = None):
     for x in (0.0, 1.0):
         job = {"cluster": layout, "x": x, "clock": "device", "seed": 3, "workload": wl,
                "device": {"model": "llama8b", "weight_seed": SEED, "token_seed": 3, "gpus": gpus,
-                          "kv_blocks_per_node": 8192, "prefill_chunk": 2048, "record_tokens": False}}
+                          "kv_blocks_per_node": 0, "prefill_chunk": 2048, "record_tokens": False}}
         t0 = time.perf_counter()
         r = E.run(job)
         agg = r["aggregate"]
@@ -334,18 +334,26 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()  # rank 0 drives all GPUs for the engine runs
         return
+    def guarded(fn, *a, **k):
+        # a failing side measurement is reported in the line, never kills it
+        try:
+            return fn(*a, **k)
+        except Exception as e:  # noqa: BLE001
+            return {"error": f"{type(e).__name__}: {e}"}
+
     qwen = None
     if not args.no_qwen and not args.quick:
-        qwen = qwen_long_decode(local_rank)
+        qwen = guarded(qwen_long_decode, local_rank)
     ttft = None
     if not args.no_engine:
         from paper_2603_13358_b200 import dist as D
         if world == 1:
             # configs[2] at two loads of the SURVEY §8d C3 QPS sweep
-            ttft = [engine_ttft([local_rank, local_rank], "1P_1D", quick=args.quick, qps=q)
+            ttft = [guarded(engine_ttft, [local_rank, local_rank], "1P_1D", quick=args.quick, qps=q)
                     for q in ((1.0,) if args.quick else (1.0, 2.0))]
         else:
-            ttft = [engine_ttft(D.layout_gpus(lay, world), lay, quick=args.quick) for lay in D.node_layouts(world)]
+            ttft = [guarded(engine_ttft, D.layout_gpus(lay, world), lay, quick=args.quick)
+                    for lay in D.node_layouts(world)]
 
     pk, pk_kind = peaks()
     traffic = None  # dram read+write per launch of the same kernel/config, from the committed ncu capture

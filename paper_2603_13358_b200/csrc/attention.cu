@@ -665,7 +665,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 // last CTA out resets them for the next launch.
 // ===========================================================================
 namespace {
-constexpr int kMixThreads = pftc::kThreads;  // 384: the prefill role's 12 warps (decode uses 10)
+constexpr int kMixSW = 8;  // softmax warps of the prefill role (2 threads per query row)
+constexpr int kMixThreads = pftc::threads_for(kMixSW);  // 384: the prefill role's 12 warps (decode uses 10)
 constexpr int kDecSmemInst = (kDecSmem - 1024 + 1023) / 1024 * 1024;
 constexpr int kMixSmem = pftc::kSmem > 1024 + 2 * kDecSmemInst ? pftc::kSmem : 1024 + 2 * kDecSmemInst;
 constexpr int kMixBarAll = 1;   // all 320 threads: mode switch
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(kMixThreads, 1)
     named_barrier_sync(kMixBarAll, kMixThreads);  // both instances retired: smem free
   }
   // ---------------- prefill queue (all 12 warps)
-  pftc::tile_queue(&kv_map, p, smem, pf_items, n_pf_tiles, warp, lane, kMixBarPf, p.mix_ctr, p.mix_ctr + 1,
+  pftc::tile_queue<kMixSW>(&kv_map, p, smem, pf_items, n_pf_tiles, warp, lane, kMixBarPf, p.mix_ctr, p.mix_ctr + 1,
                      gridDim.x, &s_next);
   pdl_trigger();
 }

@@ -21,7 +21,10 @@
 
 namespace ppdk {
 
-__global__ void __launch_bounds__(pftc::kThreads, 1)
+constexpr int kSW = 16;  // softmax warps of the standalone kernels: 4 threads per query row
+constexpr int kPfThreads = pftc::threads_for(kSW);
+
+__global__ void __launch_bounds__(kPfThreads, 1)
     prefill_attention_tc_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -30,13 +33,13 @@ __global__ void __launch_bounds__(pftc::kThreads, 1)
   const AttnItem it = p.items[blockIdx.x];
   if (it.kind != 1) return;  // decode rows are served by the decode kernels
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) pftc::init_barriers(S, false);
+  if (threadIdx.x == 0) pftc::init_barriers<kSW>(S, false);
   if (warp == 2) tc::alloc(S.tmem_slot, pftc::kTmemCols);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *S.tmem_slot;
-  pftc::tile(&kv_map, p, S, it, blockIdx.y, tmem, warp, lane, true);
+  pftc::tile<kSW>(&kv_map, p, S, it, blockIdx.y, tmem, warp, lane, true);
   tc::fence_before();
   __syncthreads();
   if (warp == 2) tc::dealloc(tmem, pftc::kTmemCols);
@@ -45,14 +48,14 @@ __global__ void __launch_bounds__(pftc::kThreads, 1)
 // Pure prefill steps: min(148, tiles) persistent CTAs pull the tiles (longest
 // first) from an atomic queue, so a chunk's 2-3 waves of uneven causal tiles
 // leave no idle SMs at the tail.
-__global__ void __launch_bounds__(pftc::kThreads, 1)
+__global__ void __launch_bounds__(kPfThreads, 1)
     prefill_attention_persistent_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p,
                                         const AttnItem* items, int n_tiles) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ int s_next;
   pdl_wait();
-  pftc::tile_queue(&kv_map, p, smem, items, n_tiles, threadIdx.x >> 5, threadIdx.x & 31, 1, p.mix_ctr,
+  pftc::tile_queue<kSW>(&kv_map, p, smem, items, n_tiles, threadIdx.x >> 5, threadIdx.x & 31, 1, p.mix_ctr,
                    p.mix_ctr + 1, gridDim.x, &s_next);
   pdl_trigger();
 }
@@ -69,7 +72,7 @@ cudaError_t launch_prefill_attention_persistent(const void* kv_map, const AttnPa
   if (n_tiles == 0) return cudaSuccess;
   if (!p.mix_ctr) return cudaErrorInvalidValue;
   const int grid = n_tiles < 148 ? n_tiles : 148;
-  return launch_pdl(prefill_attention_persistent_kernel, dim3(grid), dim3(pftc::kThreads), pftc::kSmem, stream,
+  return launch_pdl(prefill_attention_persistent_kernel, dim3(grid), dim3(kPfThreads), pftc::kSmem, stream,
                     *reinterpret_cast<const CUtensorMap*>(kv_map), p, items, n_tiles);
 }
 
@@ -81,7 +84,7 @@ cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p,
   }
   if (n_items == 0) return cudaSuccess;
   dim3 grid(n_items, p.n_kv_heads);
-  return launch_pdl(prefill_attention_tc_kernel, grid, dim3(pftc::kThreads), pftc::kSmem, stream,
+  return launch_pdl(prefill_attention_tc_kernel, grid, dim3(kPfThreads), pftc::kSmem, stream,
                     *reinterpret_cast<const CUtensorMap*>(kv_map), p);
 }
 

@@ -12,15 +12,17 @@
 namespace ppdk {
 namespace pftc {
 
-constexpr int kThreads = 384;              // warps 0-3: K TMA / MMA / TMEM alloc / V TMA; 4-11: softmax
-constexpr int kSoftmaxWarps = 8;           // two threads per query row (64 key columns each)
+// warps 0-3: K TMA / MMA / TMEM alloc / V TMA; warps 4.. : kSW softmax warps,
+// kSW / 4 threads per query row (8: 64 key columns each, 16: 32 each)
+constexpr int threads_for(int kSW) { return 128 + 32 * kSW; }
 constexpr int kBT = 16;
 constexpr int kDh = 128;
 constexpr int kKeys = 128;                  // keys per block
 constexpr int kTile = 32768;                // 128 x 128 bf16
-constexpr int kKStages = 3;                 // K ring: released as soon as S_j retires
+constexpr int kKStages = 2;                 // K ring: released as soon as S_j retires
 constexpr int kVStages = 2;                 // V ring: released after PV_j
-constexpr int kSmem = 1024 + kTile /*Q*/ + (kKStages + kVStages) * kTile + kTile /*P*/ + 256;
+// P is double-buffered: softmax_j writes P_j while PV_{j-1} still reads P_{j-1}
+constexpr int kSmem = 1024 + kTile /*Q*/ + (kKStages + kVStages) * kTile + 2 * kTile /*P*/ + 256;
 constexpr uint32_t kTmemCols = 512;        // S0 | S1 | O | row-half exchange (cols 384..)
 constexpr uint32_t kXchgCol = 384;
 constexpr float kRescaleThreshold = 8.0f;   // log2 domain
@@ -31,13 +33,16 @@ PPD_DEV float ex2_sfu(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x = 2^floor(x) * p(frac(x)), p a minimax cubic on [0, 1) with p(0) = 1
+// 2^x = 2^n * p(x - n), n = round(x), p a minimax cubic on [-1/2, 1/2] with
+// p(0) = 1 (max rel. error 1.0e-4 << bf16 ulp). Rounding by the 1.5 * 2^23
+// magic add and the exponent insert by an integer add keep it entirely on the
+// FMA / ALU pipes (FRND / F2I would share the SFU-class pipe with MUFU.EX2).
 PPD_DEV float ex2_poly(float x) {
   x = fmaxf(x, -126.f);  // -inf (masked keys) -> ~0
-  const float fi = floorf(x);
-  const float f = x - fi;
-  const float p = fmaf(fmaf(fmaf(0.07706209f, f, 0.22765041f), f, 0.69511558f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float2int_rn(fi) << 23));
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  const float p = fmaf(fmaf(fmaf(0.05500893f, f, 0.24221098f), f, 0.69328293f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 // shared-memory carve-up of one prefill CTA (smem 1024-byte aligned)
@@ -49,21 +54,22 @@ struct Smem {
     q_s = smem;
     k_s = smem + kTile;              // [kKStages]
     v_s = k_s + kKStages * kTile;    // [kVStages]
-    p_s = v_s + kVStages * kTile;
-    bars = reinterpret_cast<uint64_t*>(p_s + kTile);
-    k_full = bars;        // [3]
-    k_empty = bars + 3;   // [3]
-    v_full = bars + 6;    // [2]
-    v_empty = bars + 8;   // [2]
-    s_full = bars + 10;   // [2]
-    p_ready = bars + 12;
-    o_done = bars + 13;
+    p_s = v_s + kVStages * kTile;    // [2]
+    bars = reinterpret_cast<uint64_t*>(p_s + 2 * kTile);
+    k_full = bars;        // [2]
+    k_empty = bars + 2;   // [2]
+    v_full = bars + 4;    // [2]
+    v_empty = bars + 6;   // [2]
+    s_full = bars + 8;    // [2]
+    p_ready = bars + 10;  // [2]: softmax_j arrives on p_ready[j & 1]
+    o_done = bars + 12;   // [2]: PV_j commits to o_done[j & 1]
     q_ready = bars + 14;
     tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
   }
 };
 
 // one thread: (re)initialise the tile's mbarriers
+template <int kSW>
 PPD_DEV void init_barriers(const Smem& S, bool reinit) {
   if (reinit)
     for (int i = 0; i < kNumBars; ++i)
@@ -77,15 +83,56 @@ PPD_DEV void init_barriers(const Smem& S, bool reinit) {
     mbar_init(&S.v_empty[i], 1);
   }
   for (int i = 0; i < 2; ++i) mbar_init(&S.s_full[i], 1);
-  mbar_init(S.p_ready, kSoftmaxWarps);
-  mbar_init(S.o_done, 1);
-  mbar_init(S.q_ready, kSoftmaxWarps);
+  for (int i = 0; i < 2; ++i) mbar_init(&S.p_ready[i], kSW);
+  for (int i = 0; i < 2; ++i) mbar_init(&S.o_done[i], 1);
+  mbar_init(S.q_ready, kSW);
   fence_barrier_init();
+}
+
+// NH consecutive 32-bit TMEM columns of this thread's lane -> max / sum (fixed order)
+template <int NH>
+PPD_DEV void ld_cols(uint32_t taddr, float* v) {
+  if constexpr (NH == 2) {
+    uint32_t a, b;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(taddr));
+    tc::wait_ld();
+    v[0] = __uint_as_float(a);
+    v[1] = __uint_as_float(b);
+  } else {
+    uint32_t a, b, c, d;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(taddr));
+    tc::wait_ld();
+    v[0] = __uint_as_float(a);
+    v[1] = __uint_as_float(b);
+    v[2] = __uint_as_float(c);
+    v[3] = __uint_as_float(d);
+  }
+}
+template <int NH>
+PPD_DEV float xchg_max(uint32_t taddr) {
+  float v[NH];
+  ld_cols<NH>(taddr, v);
+  float m = v[0];
+#pragma unroll
+  for (int i = 1; i < NH; ++i) m = fmaxf(m, v[i]);
+  return m;
+}
+template <int NH>
+PPD_DEV float xchg_sum(uint32_t taddr) {
+  float v[NH];
+  ld_cols<NH>(taddr, v);
+  float s = v[0];
+#pragma unroll
+  for (int i = 1; i < NH; ++i) s += v[i];
+  return s;
 }
 
 // One 128-row tile (128/G query tokens x the G query heads of kv head `kvh`)
 // of prefill item `it`, run by warps 0..11 of the calling CTA. Barriers are
 // freshly initialised; `tmem` holds kTmemCols columns (S0 | S1 | O).
+template <int kSW>
 PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S, const AttnItem& it, int kvh,
                   uint32_t tmem, int warp, int lane, bool trigger_pdl) {
   uint8_t* q_s = S.q_s;
@@ -158,39 +205,42 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
         }
         if (j >= 1) {
           const int jj = j - 1, st = jj % kVStages;
-          mbar_wait(p_ready, jj & 1);
+          mbar_wait(&p_ready[jj & 1], (jj >> 1) & 1);
           mbar_wait(&v_full[st], (jj / kVStages) & 1);
           tc::fence_after();
           const uint32_t va = smem_u32(v_s + st * kTile);
+          const uint32_t pj = pa + (uint32_t)((jj & 1) * kTile);
 #pragma unroll
           for (int kk = 0; kk < kKeys / 16; ++kk) {
             const uint32_t poff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-            tc::mma_bf16_ss(t_o, tc::desc_kmajor_sw128(pa + poff), tc::desc_mnmajor_sw128(va + kk * 2048, kTile / 2),
+            tc::mma_bf16_ss(t_o, tc::desc_kmajor_sw128(pj + poff), tc::desc_mnmajor_sw128(va + kk * 2048, kTile / 2),
                             id_o, (jj > 0) || (kk > 0));
           }
-          tc::commit(o_done);
+          tc::commit(&o_done[jj & 1]);
           tc::commit(&v_empty[st]);
         }
       }
     }
   } else if (warp >= 4) {
-    // Softmax: 8 warps, two threads per query row. Warp w handles TMEM lane
-    // quarter w & 3 (row r) and key / O columns [64h, 64h + 64), h = (w - 4) / 4.
-    // The two halves of a row agree on its running max through free TMEM
-    // columns (one tcgen05.st / ld each way per block) and a 64-thread named
-    // barrier per lane quarter; l is kept per half and summed in the epilogue.
+    // Softmax: kSW warps, NH = kSW / 4 threads per query row. Warp w handles
+    // TMEM lane quarter w & 3 (row r) and key / O columns [CPT h, CPT (h+1)),
+    // h = (w - 4) / 4. The parts of a row agree on its running max through
+    // free TMEM columns (one tcgen05.st + one tcgen05.ld per block) and a
+    // (32 NH)-thread named barrier per lane quarter; l is kept per part and
+    // summed (fixed order) in the epilogue.
+    constexpr int NH = kSW / 4, CPT = kKeys / NH;
     const int q4 = warp & 3;
     const int h = (warp - 4) >> 2;
     const int r = q4 * 32 + lane;  // query row == TMEM lane
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
     const int pair_bar = 8 + q4;
-    // ---- Q row half -> shared (K-major, 128 B swizzle: atom h holds dims [64h, 64h + 64))
+    // ---- Q row part -> shared (K-major, 128 B swizzle: atom c >> 3 holds dims [64 (c>>3), +64))
     {
       const uint4* src = nullptr;
       if (r < rows)
         src = reinterpret_cast<const uint4*>(p.q + ((size_t)(q_base + it.q_tok0 + r / G) * p.n_q_heads + kvh * G + r % G) * kDh);
 #pragma unroll
-      for (int c = 8 * h; c < 8 * h + 8; ++c) {
+      for (int c = (16 / NH) * h; c < (16 / NH) * (h + 1); ++c) {
         const uint4 v = src ? src[c] : make_uint4(0, 0, 0, 0);
         *reinterpret_cast<uint4*>(q_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
       }
@@ -204,54 +254,45 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc::fence_after();
-      uint32_t raw[64];
-      tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + 64 * h, raw);
-      tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + 64 * h + 32, raw + 32);
+      uint32_t raw[CPT];
+#pragma unroll
+      for (int c0 = 0; c0 < CPT; c0 += 32) tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + CPT * h + c0, raw + c0);
       tc::wait_ld();
       // raw (unscaled) scores; the scale folds into the exponent's FFMA below
       // (sl2 > 0: the max commutes with it)
-      float sv[64];
-      const int key0 = j * kKeys + 64 * h;
+      float sv[CPT];
+      const int key0 = j * kKeys + CPT * h;
       float mxp[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) mxp[i] = -INFINITY;
-      if (key0 + 63 <= pos) {  // no causal mask inside this half block
+      if (key0 + CPT - 1 <= pos) {  // no causal mask inside this part of the block
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
+        for (int c = 0; c < CPT; ++c) {
           sv[c] = __uint_as_float(raw[c]);
           mxp[c & 7] = fmaxf(mxp[c & 7], sv[c]);
         }
       } else {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
+        for (int c = 0; c < CPT; ++c) {
           sv[c] = (key0 + c <= pos) ? __uint_as_float(raw[c]) : -INFINITY;
           mxp[c & 7] = fmaxf(mxp[c & 7], sv[c]);
         }
       }
       const float mh = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
                              fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7]))) * sl2;
-      // exchange the half maxima: column kXchgCol + 2 * (j & 1) + h (parity-double-buffered)
+      // exchange the part maxima: columns kXchgCol + NH * (j & 1) + [0, NH) (parity-double-buffered)
       {
         uint32_t v = __float_as_uint(mh);
         asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(
-                         tmem + lane_base + kXchgCol + 2 * (j & 1) + h),
+                         tmem + lane_base + kXchgCol + NH * (j & 1) + h),
                      "r"(v)
                      : "memory");
         tc::wait_st();
       }
       tc::fence_before();
-      named_barrier_sync(pair_bar, 64);
+      named_barrier_sync(pair_bar, 32 * NH);
       tc::fence_after();
-      float mo;
-      {
-        uint32_t v;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
-                     : "=r"(v)
-                     : "r"(tmem + lane_base + kXchgCol + 2 * (j & 1) + (1 - h)));
-        tc::wait_ld();
-        mo = __uint_as_float(v);
-      }
-      const float mx = fmaxf(mh, mo);  // identical in both halves
+      const float mx = xchg_max<NH>(tmem + lane_base + kXchgCol + NH * (j & 1));  // identical in every part
       float alpha = 1.f;
       bool rescale = false;
       if (m == -INFINITY) {
@@ -265,28 +306,32 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       // exp2 on two pipes: even keys on the SFU (ex2.approx), odd keys by a
       // degree-3 polynomial on the FMA pipe (max rel. error 8.6e-5 << bf16 ulp)
       float rsp[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[32];
+      uint32_t pk[CPT / 2];
 #pragma unroll
-      for (int c = 0; c < 64; c += 2) {
+      for (int c = 0; c < CPT; c += 2) {
         const float p0 = ex2_sfu(fmaf(sv[c], sl2, -base)), p1 = ex2_poly(fmaf(sv[c + 1], sl2, -base));
         rsp[(c >> 1) & 3] += p0 + p1;
         pk[c >> 1] = pack2(p0, p1);
       }
       const float rs = (rsp[0] + rsp[1]) + (rsp[2] + rsp[3]);
-      // P_{j-1} and O must have been consumed by PV_{j-1} before we overwrite / rescale
-      if (j >= 1) {
-        mbar_wait(o_done, (j - 1) & 1);
+      // P buffer j & 1 was last read by PV_{j-2}
+      if (j >= 2) {
+        mbar_wait(&o_done[j & 1], ((j - 2) >> 1) & 1);
         tc::fence_after();
       }
+      uint8_t* pbuf = p_s + (j & 1) * kTile;
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const int c = 8 * h + cc;  // 16-byte chunk of the row (atom h)
+      for (int cc = 0; cc < CPT / 8; ++cc) {
+        const int c = (CPT / 8) * h + cc;  // 16-byte chunk of the row
         const uint4 v = make_uint4(pk[cc * 4], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
-        *reinterpret_cast<uint4*>(p_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+        *reinterpret_cast<uint4*>(pbuf + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
       }
       if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
+        // O must hold PV_{j-1} before it is rescaled (rare: lazy threshold)
+        mbar_wait(&o_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc::fence_after();
 #pragma unroll
-        for (int c0 = 64 * h; c0 < 64 * h + 64; c0 += 32) {
+        for (int c0 = CPT * h; c0 < CPT * (h + 1); c0 += 32) {
           uint32_t o[32];
           tc::ld32x32(t_o + lane_base + c0, o);
           tc::wait_ld();
@@ -300,36 +345,28 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       fence_proxy_async();
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_ready);
+      if (lane == 0) mbar_arrive(&p_ready[j & 1]);
     }
-    // ---- epilogue: O / (l_0 + l_1) -> bf16, each half its 64 columns
+    // ---- epilogue: O / (l_0 + ... + l_{NH-1}) -> bf16, each part its CPT columns
     if (trigger_pdl) pdl_trigger();
     {
       uint32_t v = __float_as_uint(l);
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + lane_base + kXchgCol + 4 + h),
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + lane_base + kXchgCol + 2 * NH + h),
                    "r"(v)
                    : "memory");
       tc::wait_st();
     }
     tc::fence_before();
-    named_barrier_sync(pair_bar, 64);
+    named_barrier_sync(pair_bar, 32 * NH);
     tc::fence_after();
-    float lo;
-    {
-      uint32_t v;
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
-                   : "=r"(v)
-                   : "r"(tmem + lane_base + kXchgCol + 4 + (1 - h)));
-      tc::wait_ld();
-      lo = __uint_as_float(v);
-    }
-    mbar_wait(o_done, (nblk - 1) & 1);
+    const float lsum = xchg_sum<NH>(tmem + lane_base + kXchgCol + 2 * NH);  // same order in every part
+    mbar_wait(&o_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
     tc::fence_after();
-    const float inv = 1.f / (h == 0 ? l + lo : lo + l);  // same summation order in both halves
+    const float inv = 1.f / lsum;
     bf16* dst = r < rows ? p.out + ((size_t)(q_base + it.q_tok0 + r / G) * p.n_q_heads + kvh * G + r % G) * kDh
                          : nullptr;
 #pragma unroll
-    for (int c0 = 64 * h; c0 < 64 * h + 64; c0 += 32) {
+    for (int c0 = CPT * h; c0 < CPT * (h + 1); c0 += 32) {
       uint32_t o[32];
       tc::ld32x32(t_o + lane_base + c0, o);
       tc::wait_ld();
@@ -351,6 +388,7 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
 // allocating TMEM on the first tile and re-arming the mbarriers per tile.
 // bar: a named barrier id for the kThreads prefill threads. `done` (CTA count)
 // resets the queue once every CTA of the launch has left it.
+template <int kSW>
 PPD_DEV void tile_queue(const CUtensorMap* kv_map, const AttnParams& p, uint8_t* smem, const AttnItem* items,
                         int n_tiles, int warp, int lane, int bar, int* q, int* done, int n_ctas, int* s_next) {
   const Smem S(smem);
@@ -359,18 +397,18 @@ PPD_DEV void tile_queue(const CUtensorMap* kv_map, const AttnParams& p, uint8_t*
   for (;;) {
     if (tid == 0) *s_next = atomicAdd(q, 1);
     tc::fence_before();
-    named_barrier_sync(bar, kThreads);  // previous tile retired; next index published
+    named_barrier_sync(bar, threads_for(kSW));  // previous tile retired; next index published
     tc::fence_after();
     const int t = *s_next;
     if (t >= n_tiles) break;
     if (first && warp == 2) tc::alloc(S.tmem_slot, kTmemCols);
-    if (tid == 0) init_barriers(S, !first);
+    if (tid == 0) init_barriers<kSW>(S, !first);
     tc::fence_before();
-    named_barrier_sync(bar, kThreads);
+    named_barrier_sync(bar, threads_for(kSW));
     tc::fence_after();
     first = false;
     const AttnItem it = items[t / p.n_kv_heads];
-    tile(kv_map, p, S, it, t % p.n_kv_heads, *S.tmem_slot, warp, lane, false);
+    tile<kSW>(kv_map, p, S, it, t % p.n_kv_heads, *S.tmem_slot, warp, lane, false);
   }
   if (!first && warp == 2) tc::dealloc(*S.tmem_slot, kTmemCols);
   if (tid == 0) {
