@@ -1135,9 +1135,6 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "gemm_occ2") == 0) {
     CHECK_ARG(value >= -1 && value <= 1, "gemm_occ2 must be -1, 0 or 1");
     gemm_tc_set_occ2(value);
-  } else if (std::strcmp(name, "gemm_pf_sub2") == 0) {
-    CHECK_ARG(value == 0 || value == 1, "gemm_pf_sub2 must be 0 or 1");
-    gemm_tc_set_pf_sub2(value != 0);
   } else if (std::strcmp(name, "gemm_multi_sub") == 0) {
     CHECK_ARG(value == 0 || value == 1, "gemm_multi_sub must be 0 or 1");
     gemm_tc_set_multi_sub(value != 0);

@@ -537,7 +537,6 @@ bool get_map(CUtensorMap* out, const void* ptr, int rows, int K, int box_rows) {
 // 0 uniform K split / 1 balanced partition.
 static int g_pair_mode = -1;
 static bool g_multi_sub = true;  // T in (256, 512]: one unit covers both token sub-tiles
-static bool g_pf_sub2 = false;   // T > 512: 512-token units (A/B knob "gemm_pf_sub2")
 // two co-resident single CTAs per SM: -1 auto (<= kOcc2MaxT tokens; measured
 // tools/gemm_knobs.py: +10-20% weight streaming at T = 64 / 128, neutral at
 // T = 200, a loss with CTA pairs), 0 off, 1 whenever the shape allows
@@ -557,7 +556,6 @@ constexpr int kPairMinT = 48;
 constexpr double kPairMinTilesPerSm = 1.4;
 
 void gemm_tc_set_multi_sub(bool on) { g_multi_sub = on; }
-void gemm_tc_set_pf_sub2(bool on) { g_pf_sub2 = on; }
 void gemm_tc_set_occ2(int mode) { g_occ2 = mode; }
 
 void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched) {
@@ -641,11 +639,6 @@ Shape shape_for(int T, int N, int extra_smem = 0, bool force_single = false) {
   } else if (T <= 2 * kMaxBN && g_multi_sub) {
     sh.n_sub = 2;
     sh.bn = (((T + 1) / 2 + 15) / 16) * 16;
-  } else if (g_pf_sub2) {
-    // prefill: 512-token units (two 256-row sub-tiles per weight stage) halve
-    // the weight bytes each SM pulls from L2 per MMA; one accumulator set
-    sh.n_sub = 2;
-    sh.bn = kMaxBN;
   } else {
     sh.n_sub = 1;
     sh.bn = kMaxBN;

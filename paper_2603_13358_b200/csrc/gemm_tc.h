@@ -66,8 +66,6 @@ void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched);
 // T in (256, 512] token rows: one unit per weight tile covering 2 token
 // sub-tiles (default on) vs separate 256-row token tiles (A/B knob)
 void gemm_tc_set_multi_sub(bool on);
-// T > 512 token rows: 512-row units of two sub-tiles per weight stage (A/B knob)
-void gemm_tc_set_pf_sub2(bool on);
 // two co-resident CTAs per SM (half-depth rings, one accumulator each):
 // -1 auto (small token counts), 0 off, 1 whenever the shape allows
 void gemm_tc_set_occ2(int mode);

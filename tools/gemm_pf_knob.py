@@ -1,5 +1,5 @@
 """Prefill-shape GEMM A/B of tuning knobs in one process (alternating):
-  PPD_PK="gemm_pf_sub2" PPD_PK_T=1546,2058,4096 python tools/gemm_pf_knob.py"""
+  PPD_PK="gemm_multi_sub" PPD_PK_T=1546,2058,4096 python tools/gemm_pf_knob.py"""
 import json
 import os
 import sys
@@ -15,7 +15,7 @@ from tools.gemm_sweep import t_us  # noqa: E402
 
 def main():
     L = ppd.lib()
-    knob = os.environ.get("PPD_PK", "gemm_pf_sub2").encode()
+    knob = os.environ.get("PPD_PK", "gemm_multi_sub").encode()
     for T in (int(x) for x in os.environ.get("PPD_PK_T", "1546,2058,4096").split(",")):
         for N, K in ((6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)):
             A = torch.randn(T, K, device="cuda").to(torch.bfloat16)
