@@ -497,7 +497,8 @@ def main():
     if world > 1:
         import torch
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
+        import datetime
+        torch.distributed.init_process_group("nccl", timeout=datetime.timedelta(minutes=30))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch

@@ -336,9 +336,30 @@ __global__ void argmax_kernel(const float* logits, int V, int* out) {
   const float* row = logits + (size_t)blockIdx.x * V;
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  for (int v = threadIdx.x; v < V; v += blockDim.x) {
-    float x = row[v];
-    if (x > best || (x == best && v < bi)) { best = x; bi = v; }
+  auto take = [&](float x, int v) {
+    if (x > best || (x == best && v < bi)) {
+      best = x;
+      bi = v;
+    }
+  };
+  if ((V & 3) == 0) {
+    // 16-byte loads, two in flight per thread; a thread's indices only grow,
+    // so the strict '>' keeps the lowest index among its ties
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const int n4 = V >> 2;
+    int i = threadIdx.x;
+    for (; i + (int)blockDim.x < n4; i += 2 * blockDim.x) {
+      const float4 a = r4[i], b = r4[i + blockDim.x];
+      take(a.x, 4 * i); take(a.y, 4 * i + 1); take(a.z, 4 * i + 2); take(a.w, 4 * i + 3);
+      const int j = i + blockDim.x;
+      take(b.x, 4 * j); take(b.y, 4 * j + 1); take(b.z, 4 * j + 2); take(b.w, 4 * j + 3);
+    }
+    for (; i < n4; i += blockDim.x) {
+      const float4 a = r4[i];
+      take(a.x, 4 * i); take(a.y, 4 * i + 1); take(a.z, 4 * i + 2); take(a.w, 4 * i + 3);
+    }
+  } else {
+    for (int v = threadIdx.x; v < V; v += blockDim.x) take(row[v], v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
