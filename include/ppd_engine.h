@@ -19,6 +19,27 @@ int ppd_engine_run_json(const char* job_json, char** out_json);
 void ppd_engine_free(char* p);
 const char* ppd_engine_last_error(void);
 
+/* Routing gateway (reference proj/include/ppd/gateway.hpp).
+ * Replaces ppd::gateway::Gateway (gateway.hpp:72-108) for non-C++ callers:
+ * the same framed-JSON messages (register / heartbeat / route / stats,
+ * gateway.cpp:204-255), handled in process or over loopback TCP
+ * (serve_tcp, gateway.cpp:316-342). A backend may register with "gpu": i, and
+ * route replies then name decode_gpu / prefill_gpu. Status: 0 ok, -1 invalid
+ * argument (the reference's std::invalid_argument), -2 other failure. */
+typedef struct ppd_gateway ppd_gateway;
+/* policy_json: {"x": 0..1} (static) or {"policy": "dynamic", "table_json": "..."},
+ * optional "session_ttl_s" (3600), "backend_timeout_s" (30) */
+int ppd_gateway_create(const char* policy_json, ppd_gateway** out);
+/* one JSON payload in (no length prefix), reply payload out (free with
+ * ppd_engine_free); `now` in seconds, the caller's clock */
+int ppd_gateway_handle(ppd_gateway* gw, const char* payload, double now, char** reply);
+/* start the TCP server on 127.0.0.1:port (0 = ephemeral) on a background
+ * thread; *bound_port receives the port. One server per gateway. */
+int ppd_gateway_serve(ppd_gateway* gw, int port, int* bound_port);
+/* stop the server (joins its threads); no-op when not serving */
+int ppd_gateway_stop(ppd_gateway* gw);
+void ppd_gateway_destroy(ppd_gateway* gw);
+
 #ifdef __cplusplus
 }
 #endif

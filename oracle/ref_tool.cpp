@@ -17,6 +17,8 @@
 //   op=weight_sweep  sweep::weight_sweep                     (sweep.cpp:456-547)
 //   op=plan_default  SweepPlan::full_default + to_json/hash  (sweep.cpp:44-166)
 //   op=ingest_trace  workload::ingest_trace                  (workload.cpp:121-194)
+//   op=gateway       a script of BackendRegistry / Gateway::route /
+//                    handle_message / stats calls          (gateway.cpp:23-255)
 // One JSON object on stdin, one JSON object on stdout.
 #include <chrono>
 #include <cmath>
@@ -31,6 +33,7 @@
 #include <json.hpp>
 
 #include "ppd/costmodel.hpp"
+#include "ppd/gateway.hpp"
 #include "ppd/md5.hpp"
 #include "ppd/metrics.hpp"
 #include "ppd/routing.hpp"
@@ -232,6 +235,61 @@ json op_decide(const json& job) {
   return {{"decisions", out}};
 }
 
+json gateway_item(gateway::Gateway& gw, const json& it) {
+  const std::string what = it.at("do").get<std::string>();
+  const double now = it.value("now", 0.0);
+  try {
+    if (what == "add") {
+      const std::string role = it.at("role").get<std::string>();
+      return {{"id", gw.registry().add(role.empty() ? '?' : role[0], it.value("address", std::string()), now)}};
+    }
+    if (what == "heartbeat") return {{"ok", gw.registry().heartbeat(it.at("id").get<int>(), now)}};
+    if (what == "remove") return {{"removed", gw.registry().remove(it.at("id").get<int>())}};
+    if (what == "invalidate") return {{"invalidated", gw.sessions().invalidate_backend(it.at("id").get<int>())}};
+    if (what == "prune") return {{"removed", gw.registry().prune_dead(now, it.value("timeout", 30.0))}};
+    if (what == "find") {
+      auto e = gw.registry().find(it.at("id").get<int>());
+      if (!e) return {{"found", false}};
+      return {{"found", true}, {"role", std::string(1, e->role)}, {"address", e->address},
+              {"last_heartbeat", e->last_heartbeat}};
+    }
+    if (what == "route") {
+      gateway::RouteQuery q;
+      q.conv_first_message = it.at("conv").get<std::string>();
+      q.turn_index = it.at("turn").get<int>();
+      q.new_input_tokens = it.value("n_in", 0L);
+      q.cached_context_tokens = it.value("n_ctx", 0L);
+      q.target_output_tokens = it.value("n_out", 0L);
+      auto r = gw.route(q, now);
+      return {{"ok", r.ok}, {"error", r.error}, {"target", r.target}, {"prefill_backend", r.prefill_backend},
+              {"decode_backend", r.decode_backend}, {"x_used", r.x_used}, {"session_missing", r.session_missing},
+              {"table_miss", r.table_miss}};
+    }
+    if (what == "message") {
+      json r = json::parse(gw.handle_message(it.at("payload").get<std::string>(), now));
+      r.erase("decision_latency_p99_us");
+      return {{"reply", r.dump()}};
+    }
+    if (what == "stats") {
+      auto s = gw.stats();
+      return {{"queries", s.queries}, {"p_path", s.p_path}, {"d_local", s.d_local}, {"r_local", s.r_local},
+              {"errors", s.errors},   {"sessions", s.sessions}, {"backends", s.backends}};
+    }
+  } catch (const std::invalid_argument&) {
+    return {{"invalid_argument", true}};
+  }
+  throw std::invalid_argument("gateway script: unknown step " + what);
+}
+
+json op_gateway(const json& job) {
+  gateway::Gateway gw(policy_from(job));
+  gw.session_ttl_s = job.value("session_ttl_s", 3600.0);
+  gw.backend_timeout_s = job.value("backend_timeout_s", 30.0);
+  json out = json::array();
+  for (const auto& it : job.at("script")) out.push_back(gateway_item(gw, it));
+  return {{"results", out}};
+}
+
 json cell_json(const sweep::CellResult& c) { return json::parse(c.to_json()); }
 
 json winner_json(const metrics::WinnerDistribution& d) {
@@ -375,6 +433,7 @@ int main() {
     else if (op == "weight_sweep") out = op_weight_sweep(job);
     else if (op == "plan_default") out = op_plan_default();
     else if (op == "ingest_trace") out = op_ingest_trace(job);
+    else if (op == "gateway") out = op_gateway(job);
     else throw std::invalid_argument("unknown op " + op);
     std::cout << out.dump() << "\n";
     return 0;

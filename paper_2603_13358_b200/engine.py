@@ -49,3 +49,54 @@ def run(job: dict) -> dict:
 
 def records(result: dict) -> list:
     return [json.loads(x) for x in result["records_jsonl"].splitlines()[1:]]
+
+
+class Gateway:
+    """ctypes view of the routing gateway (ppd_gateway_* in include/ppd_engine.h;
+    reference proj/include/ppd/gateway.hpp). handle() is one wire message in
+    process; serve() starts the loopback TCP server (4-byte big-endian length +
+    JSON frames)."""
+
+    def __init__(self, policy: dict | None = None):
+        L = _lib()
+        L.ppd_gateway_create.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+        L.ppd_gateway_handle.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_double,
+                                         ctypes.POINTER(ctypes.c_void_p)]
+        L.ppd_gateway_serve.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.ppd_gateway_stop.argtypes = [ctypes.c_void_p]
+        L.ppd_gateway_destroy.argtypes = [ctypes.c_void_p]
+        self._L = L
+        self._h = ctypes.c_void_p()
+        self._check(L.ppd_gateway_create(json.dumps(policy or {}).encode(), ctypes.byref(self._h)))
+
+    def _check(self, rc):
+        if rc != 0:
+            msg = self._L.ppd_engine_last_error().decode()
+            raise ValueError(msg) if rc == -1 else EngineError(msg)
+
+    def handle(self, payload: str, now: float) -> str:
+        out = ctypes.c_void_p()
+        self._check(self._L.ppd_gateway_handle(self._h, payload.encode(), now, ctypes.byref(out)))
+        try:
+            return ctypes.string_at(out.value).decode()
+        finally:
+            self._L.ppd_engine_free(out)
+
+    def serve(self, port: int = 0) -> int:
+        bound = ctypes.c_int(0)
+        self._check(self._L.ppd_gateway_serve(self._h, port, ctypes.byref(bound)))
+        return bound.value
+
+    def stop(self):
+        self._check(self._L.ppd_gateway_stop(self._h))
+
+    def close(self):
+        if self._h:
+            self._L.ppd_gateway_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

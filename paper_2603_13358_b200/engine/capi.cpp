@@ -7,12 +7,14 @@
 #include <memory>
 #include <sstream>
 #include <string>
+#include <thread>
 
 #include <json.hpp>
 
 #include "../../include/ppd_engine.h"
 #include "ppd/costmodel.hpp"
 #include "ppd/engine.hpp"
+#include "ppd/gateway.hpp"
 #include "ppd/md5.hpp"
 #include "ppd/metrics.hpp"
 #include "ppd/routing.hpp"
@@ -325,6 +327,110 @@ std::string op_ingest_trace(const json& job) {
   return json{{"conversations", convs}}.dump();
 }
 
+// ---- gateway ----------------------------------------------
+// op=gateway: a script of registry / route / wire-message calls against one
+// in-process Gateway with an explicit clock; oracle/ref_tool.cpp runs the same
+// script through the reference gateway (parity test: tests/test_gateway.py).
+json gateway_item(gateway::Gateway& gw, const json& it) {
+  const std::string what = it.at("do").get<std::string>();
+  const double now = it.value("now", 0.0);
+  try {
+    if (what == "add") {
+      const std::string role = it.at("role").get<std::string>();
+      return {{"id", gw.registry().add(role.empty() ? '?' : role[0], it.value("address", std::string()), now,
+                                        it.value("gpu", -1))}};
+    }
+    if (what == "heartbeat") return {{"ok", gw.registry().heartbeat(it.at("id").get<int>(), now)}};
+    if (what == "remove") return {{"removed", gw.registry().remove(it.at("id").get<int>())}};
+    if (what == "invalidate") return {{"invalidated", gw.sessions().invalidate_backend(it.at("id").get<int>())}};
+    if (what == "prune") return {{"removed", gw.registry().prune_dead(now, it.value("timeout", 30.0))}};
+    if (what == "find") {
+      auto e = gw.registry().find(it.at("id").get<int>());
+      if (!e) return {{"found", false}};
+      return {{"found", true}, {"role", std::string(1, e->role)}, {"address", e->address},
+              {"last_heartbeat", e->last_heartbeat}};
+    }
+    if (what == "route") {
+      gateway::RouteQuery q;
+      q.conv_first_message = it.at("conv").get<std::string>();
+      q.turn_index = it.at("turn").get<int>();
+      q.new_input_tokens = it.value("n_in", 0L);
+      q.cached_context_tokens = it.value("n_ctx", 0L);
+      q.target_output_tokens = it.value("n_out", 0L);
+      const gateway::RouteReply r = gw.route(q, now);
+      json o = {{"ok", r.ok}, {"error", r.error}, {"target", r.target}, {"prefill_backend", r.prefill_backend},
+                {"decode_backend", r.decode_backend}, {"x_used", r.x_used}, {"session_missing", r.session_missing},
+                {"table_miss", r.table_miss}};
+      if (r.decode_gpu >= 0) o["decode_gpu"] = r.decode_gpu;
+      if (r.prefill_gpu >= 0) o["prefill_gpu"] = r.prefill_gpu;
+      return o;
+    }
+    if (what == "message") {
+      json r = json::parse(gw.handle_message(it.at("payload").get<std::string>(), now));
+      r.erase("decision_latency_p99_us");  // wall-clock measurement, not comparable
+      return {{"reply", r.dump()}};
+    }
+    if (what == "stats") {
+      const gateway::GatewayStats s = gw.stats();
+      return {{"queries", s.queries}, {"p_path", s.p_path}, {"d_local", s.d_local}, {"r_local", s.r_local},
+              {"errors", s.errors},   {"sessions", s.sessions}, {"backends", s.backends}};
+    }
+  } catch (const std::invalid_argument& e) {
+    return {{"invalid_argument", true}};
+  }
+  throw std::invalid_argument("gateway script: unknown step " + what);
+}
+
+std::string op_gateway(const json& job) {
+  gateway::Gateway gw(policy_from(job));
+  gw.session_ttl_s = job.value("session_ttl_s", 3600.0);
+  gw.backend_timeout_s = job.value("backend_timeout_s", 30.0);
+  json out = json::array();
+  for (const json& it : job.at("script")) out.push_back(gateway_item(gw, it));
+  const gateway::GatewayStats s = gw.stats();
+  return json{{"results", out}, {"decision_latency_p99_us", s.decision_latency_p99_us}}.dump();
+}
+
+// op=gateway_tcp: the gateway on a loopback socket, GPU workers registering and
+// heartbeating over the wire (WorkerAgent), then `messages` sent by a client in
+// `split`-byte pieces; replies returned in order.
+std::string op_gateway_tcp(const json& job) {
+  gateway::Gateway gw(policy_from(job));
+  std::atomic<bool> stop{false};
+  std::atomic<int> port{0};
+  int rc = 0;
+  std::thread srv([&] { rc = gateway::serve_tcp(gw, job.value("port", 0), stop, &port); });
+  for (int i = 0; i < 2000 && port.load() == 0 && rc == 0; ++i) std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  json out;
+  try {
+    if (port.load() == 0) throw std::runtime_error("gateway_tcp: server did not start");
+    std::vector<std::unique_ptr<gateway::WorkerAgent>> workers;
+    json ids = json::array();
+    for (const json& w : job.value("workers", json::array())) {
+      workers.push_back(std::make_unique<gateway::WorkerAgent>(
+          port.load(), w.at("role").get<std::string>().at(0), w.value("gpu", -1), w.value("address", std::string()),
+          job.value("heartbeat_s", 5.0)));
+      ids.push_back(workers.back()->id());
+    }
+    gateway::Connection c(port.load());
+    json replies = json::array();
+    const std::size_t split = job.value("split", std::size_t{0});
+    for (const json& m : job.value("messages", json::array())) replies.push_back(c.call(m.get<std::string>(), split));
+    std::this_thread::sleep_for(std::chrono::duration<double>(job.value("hold_s", 0.0)));
+    long beats = 0;
+    for (const auto& w : workers) beats += w->heartbeats();
+    workers.clear();
+    out = {{"port", port.load()}, {"worker_ids", ids}, {"replies", replies}, {"heartbeats", beats}};
+  } catch (...) {
+    stop.store(true);
+    srv.join();
+    throw;
+  }
+  stop.store(true);
+  srv.join();
+  return out.dump();
+}
+
 std::string run(const std::string& text) {
   const json job = json::parse(text);
   const std::string op = job.value("op", std::string("simulate"));
@@ -336,6 +442,8 @@ std::string run(const std::string& text) {
   if (op == "weight_sweep") return op_weight_sweep(job);
   if (op == "plan_default") return op_plan_default();
   if (op == "ingest_trace") return op_ingest_trace(job);
+  if (op == "gateway") return op_gateway(job);
+  if (op == "gateway_tcp") return op_gateway_tcp(job);
   auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
   sim::ClusterConfig cfg = sim::ClusterConfig::from_name(job.at("cluster").get<std::string>(), policy_from(job), calib);
   if (job.contains("max_decode_batch")) cfg.max_decode_batch = job["max_decode_batch"].get<int>();
@@ -380,6 +488,81 @@ int ppd_engine_run_json(const char* job_json, char** out_json) {
 }
 
 void ppd_engine_free(char* p) { std::free(p); }
+
+struct ppd_gateway {
+  gateway::Gateway gw;
+  std::atomic<bool> stop{false};
+  std::atomic<int> port{0};
+  std::thread server;
+  explicit ppd_gateway(routing::RoutingPolicy p) : gw(std::move(p)) {}
+};
+
+#define PPD_GW_GUARD(body)                          \
+  try {                                             \
+    body;                                           \
+    return 0;                                       \
+  } catch (const std::invalid_argument& e) {        \
+    g_err = e.what();                               \
+    return -1;                                      \
+  } catch (const std::exception& e) {               \
+    g_err = e.what();                               \
+    return -2;                                      \
+  }
+
+int ppd_gateway_create(const char* policy_json, ppd_gateway** out) {
+  PPD_GW_GUARD({
+    if (!out) throw std::invalid_argument("ppd_gateway_create: out is null");
+    const json j = json::parse(policy_json && *policy_json ? policy_json : "{}");
+    auto* g = new ppd_gateway(policy_from(j));
+    g->gw.session_ttl_s = j.value("session_ttl_s", 3600.0);
+    g->gw.backend_timeout_s = j.value("backend_timeout_s", 30.0);
+    *out = g;
+  })
+}
+
+int ppd_gateway_handle(ppd_gateway* gw, const char* payload, double now, char** reply) {
+  PPD_GW_GUARD({
+    if (!gw || !payload || !reply) throw std::invalid_argument("ppd_gateway_handle: null argument");
+    const std::string r = gw->gw.handle_message(payload, now);
+    char* buf = static_cast<char*>(std::malloc(r.size() + 1));
+    std::memcpy(buf, r.c_str(), r.size() + 1);
+    *reply = buf;
+  })
+}
+
+int ppd_gateway_serve(ppd_gateway* gw, int port, int* bound_port) {
+  PPD_GW_GUARD({
+    if (!gw) throw std::invalid_argument("ppd_gateway_serve: null gateway");
+    if (gw->server.joinable()) throw std::invalid_argument("ppd_gateway_serve: already serving");
+    if (port < 0 || port > 65535) throw std::invalid_argument("ppd_gateway_serve: bad port");
+    gw->stop.store(false);
+    gw->port.store(0);
+    std::atomic<int> rc{0};
+    gw->server = std::thread([gw, port, &rc] {
+      if (gateway::serve_tcp(gw->gw, port, gw->stop, &gw->port) < 0) rc.store(-1);
+    });
+    while (gw->port.load() == 0 && rc.load() == 0) std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    if (rc.load() < 0) {
+      gw->server.join();
+      throw std::runtime_error("ppd_gateway_serve: cannot bind 127.0.0.1:" + std::to_string(port));
+    }
+    if (bound_port) *bound_port = gw->port.load();
+  })
+}
+
+int ppd_gateway_stop(ppd_gateway* gw) {
+  PPD_GW_GUARD({
+    if (!gw) throw std::invalid_argument("ppd_gateway_stop: null gateway");
+    gw->stop.store(true);
+    if (gw->server.joinable()) gw->server.join();
+  })
+}
+
+void ppd_gateway_destroy(ppd_gateway* gw) {
+  if (!gw) return;
+  ppd_gateway_stop(gw);
+  delete gw;
+}
 const char* ppd_engine_last_error(void) { return g_err.c_str(); }
 
 }  // extern "C"
