@@ -6,14 +6,19 @@
 // of a prefill chunk. One CTA = 128 query rows (128/G tokens x the G query
 // heads of one kv head) of one sequence, causal over the paged history.
 //
-//   warp 0  TMA producer: per 128-key block, 8 paged 16-token blocks of K and V
-//           (2-D tensor map over the pool, 128 B swizzle) -> 2-stage ring
+//   warp 0  K TMA producer, warp 3 V TMA producer: per 128-key block, 8 paged
+//           16-token blocks (2-D tensor map over the pool, 128 B swizzle, 16
+//           boxes issued lane-parallel) -> 2-stage K and V rings
 //   warp 1  MMA issuer (one thread): S_j = Q K_j^T into TMEM (double-buffered),
-//           then O += P_{j-1} V_{j-1} (A = P from smem, B = V MN-major)
-//   warp 2  TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4-7  one thread per query row: online softmax on the S row read with
-//           tcgen05.ld, lazy O rescaling (only when the running max grows by
-//           more than 2^8), P (bf16) to smem, epilogue O / l -> bf16.
+//           then O += P_{j-1} V_{j-1} with A = P_{j-1} read from TMEM (written
+//           over S_{j-1}'s columns) and B = V (MN-major, shared memory)
+//   warp 2  TMEM allocator (512 columns: S0 | S1 | O | max exchange)
+//   warps 4.. kSW softmax warps, kSW / 4 threads per query row: online
+//           softmax on the S row part read with tcgen05.ld, running max
+//           agreed through TMEM + a named barrier, exp2 split between MUFU and
+//           an f32x2 polynomial, lazy O rescaling (only when the running max
+//           grows by more than 2^8), P (bf16) back to TMEM with tcgen05.st,
+//           epilogue O / l -> bf16.
 #include <cuda.h>
 
 #include "attention_tc_body.cuh"
@@ -21,7 +26,11 @@
 
 namespace ppdk {
 
-constexpr int kSW = 16;  // softmax warps of the standalone kernels: 4 threads per query row
+#ifndef PPD_PF_SW
+constexpr int kSW = 8;  // softmax warps of the standalone kernels: 2 threads per query row (16: 4, measured ~5% slower)
+#else
+constexpr int kSW = PPD_PF_SW;
+#endif
 constexpr int kPfThreads = pftc::threads_for(kSW);
 
 __global__ void __launch_bounds__(kPfThreads, 1)

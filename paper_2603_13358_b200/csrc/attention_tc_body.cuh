@@ -19,14 +19,38 @@ constexpr int kBT = 16;
 constexpr int kDh = 128;
 constexpr int kKeys = 128;                  // keys per block
 constexpr int kTile = 32768;                // 128 x 128 bf16
-constexpr int kKStages = 2;                 // K ring: released as soon as S_j retires
-constexpr int kVStages = 2;                 // V ring: released after PV_j
-// P is double-buffered: softmax_j writes P_j while PV_{j-1} still reads P_{j-1}
-constexpr int kSmem = 1024 + kTile /*Q*/ + (kKStages + kVStages) * kTile + 2 * kTile /*P*/ + 256;
+// P_j (bf16) is written back into S_j's own TMEM columns and PV_j takes its A
+// operand from TMEM (FA4-style aliasing): no shared-memory P buffers, no
+// st.shared / proxy fence per block. S_{j+2} reuses the columns only after
+// PV_j in the MMA pipe's issue order (tcgen05.mma from one thread executes in
+// order). kPInTmem = false keeps the double-buffered shared-memory P (A/B).
+#ifndef PPD_PF_P_SMEM
+constexpr bool kPInTmem = true;
+#else
+constexpr bool kPInTmem = false;
+#endif
+#ifndef PPD_PF_KSTAGES
+constexpr int kKStages = 2;  // K ring: released as soon as S_j retires
+#else
+constexpr int kKStages = PPD_PF_KSTAGES;
+#endif
+#ifndef PPD_PF_VSTAGES
+constexpr int kVStages = 2;  // V ring: released after PV_j
+#else
+constexpr int kVStages = PPD_PF_VSTAGES;
+#endif
+constexpr int kPBufs = kPInTmem ? 0 : 2;
+constexpr int kSmem = 1024 + kTile /*Q*/ + (kKStages + kVStages) * kTile + kPBufs * kTile /*P*/ + 256;
 constexpr uint32_t kTmemCols = 512;        // S0 | S1 | O | row-half exchange (cols 384..)
 constexpr uint32_t kXchgCol = 384;
 constexpr float kRescaleThreshold = 8.0f;   // log2 domain
-constexpr int kNumBars = 15;
+constexpr int kNumBars = 2 * (kKStages + kVStages) + 7;
+// one key pair in kPolyEvery goes to the FMA-pipe polynomial, the rest to MUFU.EX2
+#ifndef PPD_PF_POLY_EVERY
+constexpr int kPolyEvery = 8;
+#else
+constexpr int kPolyEvery = PPD_PF_POLY_EVERY;
+#endif
 
 PPD_DEV float ex2_sfu(float x) {
   float y;
@@ -37,12 +61,18 @@ PPD_DEV float ex2_sfu(float x) {
 // p(0) = 1 (max rel. error 1.0e-4 << bf16 ulp). Rounding by the 1.5 * 2^23
 // magic add and the exponent insert by an integer add keep it entirely on the
 // FMA / ALU pipes (FRND / F2I would share the SFU-class pipe with MUFU.EX2).
-PPD_DEV float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);  // -inf (masked keys) -> ~0
-  const float t = x + 12582912.0f;
-  const float f = x - (t - 12582912.0f);
-  const float p = fmaf(fmaf(fmaf(0.05500893f, f, 0.24221098f), f, 0.69328293f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+// Two lanes at a time: the float math issues as packed f32x2 FADD2 / FFMA2.
+PPD_DEV float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);  // -inf (masked keys) -> ~0
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
+  const float2 u = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));  // round(x), exact
+  const float2 f = __ffma2_rn(u, make_float2(-1.f, -1.f), x);                 // x - round(x), exact
+  float2 p = __ffma2_rn(make_float2(0.05500893f, 0.05500893f), f, make_float2(0.24221098f, 0.24221098f));
+  p = __ffma2_rn(p, f, make_float2(0.69328293f, 0.69328293f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 // shared-memory carve-up of one prefill CTA (smem 1024-byte aligned)
@@ -54,16 +84,16 @@ struct Smem {
     q_s = smem;
     k_s = smem + kTile;              // [kKStages]
     v_s = k_s + kKStages * kTile;    // [kVStages]
-    p_s = v_s + kVStages * kTile;    // [2]
-    bars = reinterpret_cast<uint64_t*>(p_s + 2 * kTile);
-    k_full = bars;        // [2]
-    k_empty = bars + 2;   // [2]
-    v_full = bars + 4;    // [2]
-    v_empty = bars + 6;   // [2]
-    s_full = bars + 8;    // [2]
-    p_ready = bars + 10;  // [2]: softmax_j arrives on p_ready[j & 1]
-    o_done = bars + 12;   // [2]: PV_j commits to o_done[j & 1]
-    q_ready = bars + 14;
+    p_s = v_s + kVStages * kTile;    // [kPBufs]
+    bars = reinterpret_cast<uint64_t*>(p_s + kPBufs * kTile);
+    k_full = bars;                  // [kKStages]
+    k_empty = k_full + kKStages;    // [kKStages]
+    v_full = k_empty + kKStages;    // [kVStages]
+    v_empty = v_full + kVStages;    // [kVStages]
+    s_full = v_empty + kVStages;    // [2]
+    p_ready = s_full + 2;           // [2]: softmax_j arrives on p_ready[j & 1]
+    o_done = p_ready + 2;           // [2]: PV_j commits to o_done[j & 1]
+    q_ready = o_done + 2;
     tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
   }
 };
@@ -209,12 +239,24 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
           mbar_wait(&v_full[st], (jj / kVStages) & 1);
           tc::fence_after();
           const uint32_t va = smem_u32(v_s + st * kTile);
-          const uint32_t pj = pa + (uint32_t)((jj & 1) * kTile);
+          if constexpr (kPInTmem) {
+            // part h of a row packed its CPT keys into columns [CPT h, CPT h + CPT / 2) of S_jj
+            constexpr int CPT = kKeys / (kSW / 4);
+            const uint32_t sj = tmem + (jj & 1) * kKeys;
 #pragma unroll
-          for (int kk = 0; kk < kKeys / 16; ++kk) {
-            const uint32_t poff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-            tc::mma_bf16_ss(t_o, tc::desc_kmajor_sw128(pj + poff), tc::desc_mnmajor_sw128(va + kk * 2048, kTile / 2),
-                            id_o, (jj > 0) || (kk > 0));
+            for (int kk = 0; kk < kKeys / 16; ++kk) {
+              const uint32_t col = (16 * kk / CPT) * CPT + ((16 * kk) % CPT) / 2;
+              tc::mma_bf16_ts(t_o, sj + col, tc::desc_mnmajor_sw128(va + kk * 2048, kTile / 2), id_o,
+                              (jj > 0) || (kk > 0));
+            }
+          } else {
+            const uint32_t pj = pa + (uint32_t)((jj & 1) * kTile);
+#pragma unroll
+            for (int kk = 0; kk < kKeys / 16; ++kk) {
+              const uint32_t poff = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+              tc::mma_bf16_ss(t_o, tc::desc_kmajor_sw128(pj + poff), tc::desc_mnmajor_sw128(va + kk * 2048, kTile / 2),
+                              id_o, (jj > 0) || (kk > 0));
+            }
           }
           tc::commit(&o_done[jj & 1]);
           tc::commit(&v_empty[st]);
@@ -303,28 +345,49 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
         rescale = true;
       }
       const float base = m == -INFINITY ? 0.f : m;
-      // exp2 on two pipes: even keys on the SFU (ex2.approx), odd keys by a
-      // degree-3 polynomial on the FMA pipe (max rel. error 8.6e-5 << bf16 ulp)
-      float rsp[4] = {0.f, 0.f, 0.f, 0.f};
+      // exp2 on two pipes: of every 2 kPolyEvery keys, the last two go to a
+      // degree-3 polynomial on the FMA pipe (max rel. error 8.6e-5 << bf16
+      // ulp), the rest to the SFU (ex2.approx); scale, polynomial and row
+      // sums as packed f32x2 ops
+      const float2 sl2v = make_float2(sl2, sl2), nbase = make_float2(-base, -base);
+      float2 rs_a = make_float2(0.f, 0.f), rs_b = make_float2(0.f, 0.f);
       uint32_t pk[CPT / 2];
 #pragma unroll
       for (int c = 0; c < CPT; c += 2) {
-        const float p0 = ex2_sfu(fmaf(sv[c], sl2, -base)), p1 = ex2_poly(fmaf(sv[c + 1], sl2, -base));
-        rsp[(c >> 1) & 3] += p0 + p1;
-        pk[c >> 1] = pack2(p0, p1);
+        const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nbase);
+        float2 e;
+        if ((c / 2) % kPolyEvery == kPolyEvery - 1) {
+          e = ex2_poly2(x);
+          rs_b = __fadd2_rn(rs_b, e);
+        } else {
+          e = make_float2(ex2_sfu(x.x), ex2_sfu(x.y));
+          rs_a = __fadd2_rn(rs_a, e);
+        }
+        pk[c >> 1] = pack2(e.x, e.y);
       }
-      const float rs = (rsp[0] + rsp[1]) + (rsp[2] + rsp[3]);
-      // P buffer j & 1 was last read by PV_{j-2}
-      if (j >= 2) {
-        mbar_wait(&o_done[j & 1], ((j - 2) >> 1) & 1);
-        tc::fence_after();
-      }
-      uint8_t* pbuf = p_s + (j & 1) * kTile;
+      const float rs = (rs_a.x + rs_a.y) + (rs_b.x + rs_b.y);
+      if constexpr (kPInTmem) {
+        // P_j over this part's own (already loaded) S_j columns; every part's
+        // S loads precede the max-exchange barrier above
+        const uint32_t pdst = tmem + lane_base + (j & 1) * kKeys + CPT * h;
+        if constexpr (CPT == 32) {
+          tc::st32x16(pdst, pk);
+        } else {
+          tc::st32x32(pdst, pk);
+        }
+      } else {
+        // P buffer j & 1 was last read by PV_{j-2}
+        if (j >= 2) {
+          mbar_wait(&o_done[j & 1], ((j - 2) >> 1) & 1);
+          tc::fence_after();
+        }
+        uint8_t* pbuf = p_s + (j & 1) * kTile;
 #pragma unroll
-      for (int cc = 0; cc < CPT / 8; ++cc) {
-        const int c = (CPT / 8) * h + cc;  // 16-byte chunk of the row
-        const uint4 v = make_uint4(pk[cc * 4], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
-        *reinterpret_cast<uint4*>(pbuf + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+        for (int cc = 0; cc < CPT / 8; ++cc) {
+          const int c = (CPT / 8) * h + cc;  // 16-byte chunk of the row
+          const uint4 v = make_uint4(pk[cc * 4], pk[cc * 4 + 1], pk[cc * 4 + 2], pk[cc * 4 + 3]);
+          *reinterpret_cast<uint4*>(pbuf + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+        }
       }
       if (j >= 1 && __any_sync(0xffffffffu, rescale)) {
         // O must hold PV_{j-1} before it is rescaled (rare: lazy threshold)
@@ -342,7 +405,11 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
         tc::wait_st();
       }
       l = l * alpha + rs;
-      fence_proxy_async();
+      if constexpr (kPInTmem) {
+        tc::wait_st();
+      } else {
+        fence_proxy_async();
+      }
       tc::fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_ready[j & 1]);

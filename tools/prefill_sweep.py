@@ -14,6 +14,8 @@ import paper_2603_13358_b200 as ppd  # noqa: E402
 
 
 def main():
+    if os.environ.get("PPD_LIB"):  # A/B another build of libppd_b200.so
+        ppd._lib = ppd.load_lib(os.environ["PPD_LIB"], strict=False)
     for kv in filter(None, os.environ.get("PPD_PF_KNOBS", "").split(",")):
         k, v = kv.split("=")
         ppd.check(ppd.lib().ppd_set_tuning(k.encode(), int(v)))
