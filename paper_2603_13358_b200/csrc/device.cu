@@ -54,10 +54,14 @@ constexpr int kMaxRope = 1 << 17;  // positions covered by the RoPE table
 // process-wide tuning (ppd_set_tuning); each change bumps the epoch so devices
 // re-capture their step graphs with the newly selected kernels
 int g_tuning_epoch = 0;
-// gate|up GEMM with the SiLU epilogue (else fp32 partials + silu_mul_kernel).
-// Off by default: step-level A/B (tools/ab_step.py, 48 steps per arm) shows
-// no gain over the balanced-partition GEMM + silu_mul_kernel (within 1%).
-bool g_mlp_fused = false;
+// gate|up GEMM with the SiLU epilogue writing bf16 m directly (else fp32
+// partials + silu_mul_kernel). 0 never, 1 always, 2 (default) for steps of at
+// least kMlpFusedMinRows token rows. Decode-size steps: no gain (within 1%,
+// tools/ab_step.py, 48 steps per arm; the K-split partition balances better).
+// Prefill-size steps: 8-16% faster steps (tools/ab_knobs.sh: the fp32 gate|up
+// round trip is 2 x T x 28672 x 4 B per layer, 0.94 GB at T = 4096).
+int g_mlp_fused = 2;
+constexpr int kMlpFusedMinRows = 512;
 // diagnostics only ("diag_skip" knob): skip kernel classes of the forward step
 // (1 small ops, 2 attention, 4 GEMMs) to time their marginal cost in the live
 // graph. Results are meaningless while set.
@@ -600,7 +604,7 @@ int forward(ppd_dev* d, const StepLayout& L) {
     PROF(1, true);
     if (!(g_diag_skip & 1)) CU(launch_add_rmsnorm(d->x, d->proj32, np_o, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
     PROF(1, false);
-    if (g_mlp_fused) {
+    if (g_mlp_fused == 1 || (g_mlp_fused == 2 && T >= kMlpFusedMinRows)) {
       if (!(g_diag_skip & 4)) CU(gemm_run_silu(d->gemm, d->h, w.wgu, d->m, d->gu32, T, 2 * F, d_model, s));
       PROF(1, true);
     } else {
@@ -1139,8 +1143,8 @@ int ppd_set_tuning(const char* name, int32_t value) {
     CHECK_ARG(value == 0 || value == 1, "gemm_multi_sub must be 0 or 1");
     gemm_tc_set_multi_sub(value != 0);
   } else if (std::strcmp(name, "mlp_fused") == 0) {
-    CHECK_ARG(value == 0 || value == 1, "mlp_fused must be 0 or 1");
-    g_mlp_fused = value != 0;
+    CHECK_ARG(value >= 0 && value <= 2, "mlp_fused must be 0, 1 or 2");
+    g_mlp_fused = value;
   } else {
     return fail(PPD_ERR_INVALID, std::string("unknown tuning knob: ") + name);
   }

@@ -79,7 +79,7 @@ def test_step_parity_under_gemm_variants(pair, knobs):
             ppd.check(L.ppd_set_tuning(k.encode(), v))
         test_prefill_decode_append_parity(pair)
     finally:
-        for k, v in (("gemm_pair", -1), ("gemm_sched", -1), ("mlp_fused", 0)):
+        for k, v in (("gemm_pair", -1), ("gemm_sched", -1), ("mlp_fused", 2)):
             ppd.check(L.ppd_set_tuning(k.encode(), v))
 
 
