@@ -61,6 +61,8 @@ int g_tuning_epoch = 0;
 // Prefill-size steps: 8-16% faster steps (tools/ab_knobs.sh: the fp32 gate|up
 // round trip is 2 x T x 28672 x 4 B per layer, 0.94 GB at T = 4096).
 int g_mlp_fused = 2;
+// workspaces sized for two K-partial slices of a max-size step (see alloc_workspaces)
+bool g_ws_two_slices = true;
 constexpr int kMlpFusedMinRows = 512;
 // diagnostics only ("diag_skip" knob): skip kernel classes of the forward step
 // (1 small ops, 2 attention, 4 GEMMs) to time their marginal cost in the live
@@ -635,8 +637,11 @@ int alloc_workspaces(ppd_dev* d) {
   CU(cudaMalloc(&d->attn, T * qd * 2));
   CU(cudaMalloc(&d->m, T * c.d_ff * 2));
   CU(cudaMalloc(&d->hl, S * c.d_model * 2));
-  // fp32 GEMM outputs also hold up to 8 K-split partial slices of a <=256-token step
-  const size_t Tp = std::max<size_t>(T, 8 * 256);
+  // fp32 GEMM outputs also hold up to 8 K-split partial slices of a <=256-token
+  // step and 2 of a full-size step: prefill-size o / down GEMMs (N = 4096 -> 32
+  // weight tiles x T/256 token tiles) need a balanced 2-way K split to fill
+  // the 148 SMs (1.3 waves of tiles otherwise at T = 1536)
+  const size_t Tp = std::max<size_t>(g_ws_two_slices ? 2 * T : T, 8 * 256);
   d->ws_rows = Tp;
   CU(cudaMalloc(&d->qkv32, Tp * (qd + 2 * kd) * 4));
   CU(cudaMalloc(&d->proj32, Tp * c.d_model * 4));
@@ -1142,6 +1147,9 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "gemm_multi_sub") == 0) {
     CHECK_ARG(value == 0 || value == 1, "gemm_multi_sub must be 0 or 1");
     gemm_tc_set_multi_sub(value != 0);
+  } else if (std::strcmp(name, "ws_two_slices") == 0) {  // takes effect for devices opened afterwards
+    CHECK_ARG(value == 0 || value == 1, "ws_two_slices must be 0 or 1");
+    g_ws_two_slices = value != 0;
   } else if (std::strcmp(name, "mlp_fused") == 0) {
     CHECK_ARG(value >= 0 && value <= 2, "mlp_fused must be 0, 1 or 2");
     g_mlp_fused = value;
