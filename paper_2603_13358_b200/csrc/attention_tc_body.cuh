@@ -40,11 +40,33 @@ constexpr int kVStages = 2;  // V ring: released after PV_j
 constexpr int kVStages = PPD_PF_VSTAGES;
 #endif
 constexpr int kPBufs = kPInTmem ? 0 : 2;
-constexpr int kSmem = 1024 + kTile /*Q*/ + (kKStages + kVStages) * kTile + kPBufs * kTile /*P*/ + 256;
-constexpr uint32_t kTmemCols = 512;        // S0 | S1 | O | row-half exchange (cols 384..)
+// the parts of a query row agree on the running max (and, at the end, the row
+// sum) through shared memory (one st.shared + a 32 NH-thread named barrier +
+// NH ld.shared); kXchgSmem = false uses free TMEM columns instead (A/B)
+#ifndef PPD_PF_XCHG_TMEM
+constexpr bool kXchgSmem = true;
+#else
+constexpr bool kXchgSmem = false;
+#endif
+constexpr int kXchgBytes = 3 * 128 * 4 * 4;  // [3 slots: max parity 0/1, row sum][128 rows][NH <= 4]
+constexpr int kSmem = 1024 + kTile /*Q*/ + (kKStages + kVStages) * kTile + kPBufs * kTile /*P*/ + 256 + kXchgBytes;
+constexpr uint32_t kTmemCols = 512;        // S0 | S1 | O | S2 (or the TMEM max exchange, cols 384..)
 constexpr uint32_t kXchgCol = 384;
 constexpr float kRescaleThreshold = 8.0f;   // log2 domain
-constexpr int kNumBars = 2 * (kKStages + kVStages) + 7;
+// S buffers in TMEM. Three (S0 | S1 | O | S2) when P lives in TMEM and the
+// max exchange in shared memory: S_j is then issued two blocks ahead of PV_j,
+// so softmax_{j+1}'s scores are ready when softmax_j ends (with two, S_{j+1}
+// can only follow PV_{j-1}, and softmax waits out PV + S every other block).
+constexpr int kSBufs = (kPInTmem && kXchgSmem) ? 3 : 2;
+// diagnostics builds only (-DPPD_PF_DIAG=n, results wrong): 1 softmax without
+// exponentials, 2 PV reduced to one K slice, 3 S reduced to one K slice
+#ifndef PPD_PF_DIAG
+constexpr int kDiag = 0;
+#else
+constexpr int kDiag = PPD_PF_DIAG;
+#endif
+PPD_DEV constexpr uint32_t s_col(int b) { return b < 2 ? (uint32_t)b * kKeys : 3u * kKeys; }
+constexpr int kNumBars = 2 * (kKStages + kVStages) + 2 * kSBufs + 3;
 // one key pair in kPolyEvery goes to the FMA-pipe polynomial, the rest to MUFU.EX2
 #ifndef PPD_PF_POLY_EVERY
 constexpr int kPolyEvery = 8;
@@ -80,6 +102,7 @@ struct Smem {
   uint8_t *q_s, *k_s, *v_s, *p_s;
   uint64_t *bars, *k_full, *k_empty, *v_full, *v_empty, *s_full, *p_ready, *o_done, *q_ready;
   uint32_t* tmem_slot;
+  float* xchg;  // [3][128][NH]
   PPD_DEV explicit Smem(uint8_t* smem) {
     q_s = smem;
     k_s = smem + kTile;              // [kKStages]
@@ -90,11 +113,12 @@ struct Smem {
     k_empty = k_full + kKStages;    // [kKStages]
     v_full = k_empty + kKStages;    // [kVStages]
     v_empty = v_full + kVStages;    // [kVStages]
-    s_full = v_empty + kVStages;    // [2]
-    p_ready = s_full + 2;           // [2]: softmax_j arrives on p_ready[j & 1]
-    o_done = p_ready + 2;           // [2]: PV_j commits to o_done[j & 1]
+    s_full = v_empty + kVStages;    // [kSBufs]: S_j commits to s_full[j % kSBufs]
+    p_ready = s_full + kSBufs;      // [kSBufs]: softmax_j arrives on p_ready[j % kSBufs]
+    o_done = p_ready + kSBufs;      // [2]: PV_j commits to o_done[j & 1]
     q_ready = o_done + 2;
     tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
+    xchg = reinterpret_cast<float*>(p_s + kPBufs * kTile + 256);
   }
 };
 
@@ -112,8 +136,8 @@ PPD_DEV void init_barriers(const Smem& S, bool reinit) {
     mbar_init(&S.v_full[i], 1);
     mbar_init(&S.v_empty[i], 1);
   }
-  for (int i = 0; i < 2; ++i) mbar_init(&S.s_full[i], 1);
-  for (int i = 0; i < 2; ++i) mbar_init(&S.p_ready[i], kSW);
+  for (int i = 0; i < kSBufs; ++i) mbar_init(&S.s_full[i], 1);
+  for (int i = 0; i < kSBufs; ++i) mbar_init(&S.p_ready[i], kSW);
   for (int i = 0; i < 2; ++i) mbar_init(&S.o_done[i], 1);
   mbar_init(S.q_ready, kSW);
   fence_barrier_init();
@@ -218,7 +242,8 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       mbar_wait(q_ready, 0);
       tc::fence_after();
       const uint32_t qa = smem_u32(q_s), pa = smem_u32(p_s);
-      for (int j = 0; j <= nblk; ++j) {
+      constexpr int kAhead = kSBufs - 1;  // S_j is issued before PV_{j - kAhead}
+      for (int j = 0; j < nblk + kAhead; ++j) {
         if (j < nblk) {
           const int st = j % kKStages;
           mbar_wait(&k_full[st], (j / kKStages) & 1);
@@ -226,25 +251,27 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
           const uint32_t ka = smem_u32(k_s + st * kTile);
 #pragma unroll
           for (int kk = 0; kk < kDh / 16; ++kk) {
+            if (kDiag == 3 && kk > 0) break;  // diagnostics: one K=16 slice of S only
             const uint32_t off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-            tc::mma_bf16_ss(tmem + (j & 1) * kKeys, tc::desc_kmajor_sw128(qa + off), tc::desc_kmajor_sw128(ka + off),
-                            id_s, kk > 0);
+            tc::mma_bf16_ss(tmem + s_col(j % kSBufs), tc::desc_kmajor_sw128(qa + off),
+                            tc::desc_kmajor_sw128(ka + off), id_s, kk > 0);
           }
-          tc::commit(&s_full[j & 1]);
+          tc::commit(&s_full[j % kSBufs]);
           tc::commit(&k_empty[st]);  // K tile free once S_j retires
         }
-        if (j >= 1) {
-          const int jj = j - 1, st = jj % kVStages;
-          mbar_wait(&p_ready[jj & 1], (jj >> 1) & 1);
+        if (j >= kAhead) {
+          const int jj = j - kAhead, st = jj % kVStages;
+          mbar_wait(&p_ready[jj % kSBufs], (jj / kSBufs) & 1);
           mbar_wait(&v_full[st], (jj / kVStages) & 1);
           tc::fence_after();
           const uint32_t va = smem_u32(v_s + st * kTile);
           if constexpr (kPInTmem) {
             // part h of a row packed its CPT keys into columns [CPT h, CPT h + CPT / 2) of S_jj
             constexpr int CPT = kKeys / (kSW / 4);
-            const uint32_t sj = tmem + (jj & 1) * kKeys;
+            const uint32_t sj = tmem + s_col(jj % kSBufs);
 #pragma unroll
             for (int kk = 0; kk < kKeys / 16; ++kk) {
+              if (kDiag == 2 && kk > 0) break;  // diagnostics: one K=16 slice of PV only
               const uint32_t col = (16 * kk / CPT) * CPT + ((16 * kk) % CPT) / 2;
               tc::mma_bf16_ts(t_o, sj + col, tc::desc_mnmajor_sw128(va + kk * 2048, kTile / 2), id_o,
                               (jj > 0) || (kk > 0));
@@ -294,11 +321,12 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
     const float sl2 = p.scale_log2;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      const int sb = j % kSBufs;
+      mbar_wait(&s_full[sb], (j / kSBufs) & 1);
       tc::fence_after();
       uint32_t raw[CPT];
 #pragma unroll
-      for (int c0 = 0; c0 < CPT; c0 += 32) tc::ld32x32(tmem + lane_base + (j & 1) * kKeys + CPT * h + c0, raw + c0);
+      for (int c0 = 0; c0 < CPT; c0 += 32) tc::ld32x32(tmem + lane_base + s_col(sb) + CPT * h + c0, raw + c0);
       tc::wait_ld();
       // raw (unscaled) scores; the scale folds into the exponent's FFMA below
       // (sl2 > 0: the max commutes with it)
@@ -322,19 +350,28 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       }
       const float mh = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
                              fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7]))) * sl2;
-      // exchange the part maxima: columns kXchgCol + NH * (j & 1) + [0, NH) (parity-double-buffered)
-      {
+      // exchange the part maxima (parity-double-buffered slots: a part writes
+      // slot j & 1 only after every part passed block j-1's barrier)
+      float mx;
+      if constexpr (kXchgSmem) {
+        float* slot = S.xchg + ((j & 1) * 128 + r) * NH;
+        slot[h] = mh;
+        named_barrier_sync(pair_bar, 32 * NH);
+        mx = slot[0];
+#pragma unroll
+        for (int i = 1; i < NH; ++i) mx = fmaxf(mx, slot[i]);  // identical in every part
+      } else {
         uint32_t v = __float_as_uint(mh);
         asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(
                          tmem + lane_base + kXchgCol + NH * (j & 1) + h),
                      "r"(v)
                      : "memory");
         tc::wait_st();
+        tc::fence_before();
+        named_barrier_sync(pair_bar, 32 * NH);
+        tc::fence_after();
+        mx = xchg_max<NH>(tmem + lane_base + kXchgCol + NH * (j & 1));  // identical in every part
       }
-      tc::fence_before();
-      named_barrier_sync(pair_bar, 32 * NH);
-      tc::fence_after();
-      const float mx = xchg_max<NH>(tmem + lane_base + kXchgCol + NH * (j & 1));  // identical in every part
       float alpha = 1.f;
       bool rescale = false;
       if (m == -INFINITY) {
@@ -354,6 +391,10 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       uint32_t pk[CPT / 2];
 #pragma unroll
       for (int c = 0; c < CPT; c += 2) {
+        if (kDiag == 1) {  // diagnostics: no exponentials
+          pk[c >> 1] = __float_as_uint(sv[c]) ^ __float_as_uint(sv[c + 1]);
+          continue;
+        }
         const float2 x = __ffma2_rn(make_float2(sv[c], sv[c + 1]), sl2v, nbase);
         float2 e;
         if ((c / 2) % kPolyEvery == kPolyEvery - 1) {
@@ -369,7 +410,7 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       if constexpr (kPInTmem) {
         // P_j over this part's own (already loaded) S_j columns; every part's
         // S loads precede the max-exchange barrier above
-        const uint32_t pdst = tmem + lane_base + (j & 1) * kKeys + CPT * h;
+        const uint32_t pdst = tmem + lane_base + s_col(sb) + CPT * h;
         if constexpr (CPT == 32) {
           tc::st32x16(pdst, pk);
         } else {
@@ -412,21 +453,29 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_ready[j & 1]);
+      if (lane == 0) mbar_arrive(&p_ready[sb]);
     }
     // ---- epilogue: O / (l_0 + ... + l_{NH-1}) -> bf16, each part its CPT columns
     if (trigger_pdl) pdl_trigger();
-    {
+    float lsum;
+    if constexpr (kXchgSmem) {
+      float* slot = S.xchg + (2 * 128 + r) * NH;
+      slot[h] = l;
+      named_barrier_sync(pair_bar, 32 * NH);
+      lsum = slot[0];
+#pragma unroll
+      for (int i = 1; i < NH; ++i) lsum += slot[i];  // same order in every part
+    } else {
       uint32_t v = __float_as_uint(l);
       asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + lane_base + kXchgCol + 2 * NH + h),
                    "r"(v)
                    : "memory");
       tc::wait_st();
+      tc::fence_before();
+      named_barrier_sync(pair_bar, 32 * NH);
+      tc::fence_after();
+      lsum = xchg_sum<NH>(tmem + lane_base + kXchgCol + 2 * NH);  // same order in every part
     }
-    tc::fence_before();
-    named_barrier_sync(pair_bar, 32 * NH);
-    tc::fence_after();
-    const float lsum = xchg_sum<NH>(tmem + lane_base + kXchgCol + 2 * NH);  // same order in every part
     mbar_wait(&o_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
     tc::fence_after();
     const float inv = 1.f / lsum;
