@@ -35,9 +35,18 @@ __global__ void kv_copy_kernel(KvCopyParams p) {
     uint8_t* dst = reinterpret_cast<uint8_t*>(p.dst_pool) +
                    (((size_t)p.dst_blocks[b] * per_block * BT) + slice + t0) * row_bytes;
     const int n16 = (int)((t1 - t0) * row_bytes / 16);
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
-    for (int i = lane; i < n16; i += 32) d4[i] = __ldcs(s4 + i);
+    const uint4* __restrict__ s4 = reinterpret_cast<const uint4*>(src);
+    uint4* __restrict__ d4 = reinterpret_cast<uint4*>(dst);
+    int i = lane;
+    // a whole 16-token run (4 KB at head_dim 128) is 8 x 512 B: issue all loads first
+    for (; i + 7 * 32 < n16; i += 8 * 32) {
+      uint4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcs(s4 + i + k * 32);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) __stcs(d4 + i + k * 32, v[k]);
+    }
+    for (; i < n16; i += 32) __stcs(d4 + i, __ldcs(s4 + i));
   }
 }
 
