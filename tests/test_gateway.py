@@ -279,3 +279,31 @@ def test_gateway_c_abi_in_process_and_python_client():
     gw.stop()
     gw.stop()
     gw.close()
+
+
+def test_gateway_threadsanitizer(tmp_path):
+    """SURVEY §5 race detection: the gateway under concurrent TCP clients,
+    heartbeating workers and in-process admin calls, built with
+    -fsanitize=thread (tests/native/gateway_tsan.cpp)."""
+    import shutil
+    import subprocess
+    import pytest
+    if not shutil.which("g++"):
+        pytest.skip("g++ absent")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    eng = os.path.join(repo, "paper_2603_13358_b200", "engine")
+    json_inc = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+    if not os.path.isdir(json_inc):
+        pytest.skip("nlohmann json headers absent")
+    exe = str(tmp_path / "gateway_tsan")
+    srcs = [os.path.join(repo, "tests", "native", "gateway_tsan.cpp")] + [
+        os.path.join(eng, f) for f in ("gateway.cpp", "routing.cpp", "md5.cpp", "metrics.cpp", "util.cpp",
+                                       "workload.cpp", "costmodel.cpp")]
+    subprocess.run(["g++", "-std=c++20", "-O1", "-g", "-fsanitize=thread", "-pthread", "-I" + os.path.join(repo, "include"),
+                    "-I" + json_inc, *srcs, "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, TSAN_OPTIONS="halt_on_error=1 second_deadlock_stack=1"))
+    assert "ThreadSanitizer" not in r.stderr, r.stderr[-4000:]
+    assert r.returncode == 0, (r.stdout, r.stderr[-2000:])
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["bad"] == 0 and out["queries"] == 2400 and out["backends"] == 6
