@@ -408,8 +408,11 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       }
       const float rs = (rs_a.x + rs_a.y) + (rs_b.x + rs_b.y);
       if constexpr (kPInTmem) {
-        // P_j over this part's own (already loaded) S_j columns; every part's
-        // S loads precede the max-exchange barrier above
+        // consume PV_{j-2}'s o_done phase (long retired; keeps every mbarrier
+        // phase observed before its next arrival, as compute-sanitizer
+        // synccheck requires), then P_j over this part's own (already loaded)
+        // S_j columns; every part's S loads precede the max-exchange barrier above
+        if (j >= 2) mbar_wait(&o_done[j & 1], ((j - 2) >> 1) & 1);
         const uint32_t pdst = tmem + lane_base + s_col(sb) + CPT * h;
         if constexpr (CPT == 32) {
           tc::st32x16(pdst, pk);
@@ -476,6 +479,9 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       tc::fence_after();
       lsum = xchg_sum<NH>(tmem + lane_base + kXchgCol + 2 * NH);  // same order in every part
     }
+    // the final phase of both o_done slots is consumed before the barriers are
+    // re-armed for the next tile (PV_{nblk-2} retired before PV_{nblk-1})
+    if (nblk >= 2) mbar_wait(&o_done[(nblk - 2) & 1], ((nblk - 2) >> 1) & 1);
     mbar_wait(&o_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
     tc::fence_after();
     const float inv = 1.f / lsum;

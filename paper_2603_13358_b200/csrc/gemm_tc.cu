@@ -381,6 +381,11 @@ __global__ void __launch_bounds__(kThreads, kOcc)
     Sched sc;
     sc.begin(p, rows, slot, n_slots);
     Seg sg;
+    // SiLU exchange-buffer parity runs on across sub-tiles AND segments: warps
+    // 2-3 may start the next segment's first chunk while warps 0-1 still read
+    // the last chunk of this one (a per-segment reset raced there whenever a
+    // segment ended on buffer 0; found by compute-sanitizer memcheck timing)
+    int buf = 0;
     for (int j = 0; sc.next(sg); ++j) {
       const int acc = j % n_acc;
       const int use = j / n_acc;
@@ -389,7 +394,6 @@ __global__ void __launch_bounds__(kThreads, kOcc)
       tc_fence_after();
       float* out32 = reinterpret_cast<float*>(p.out) + (size_t)sg.slice * p.split_stride;
       __nv_bfloat16* out16 = reinterpret_cast<__nv_bfloat16*>(p.out);
-      int buf = 0;  // SiLU exchange-buffer parity runs on across sub-tiles (double buffering)
 #pragma unroll
       for (int jsub = 0; jsub < kNSub; ++jsub) {
       const int t0 = sg.tt * unit_t + jsub * p.bn;
