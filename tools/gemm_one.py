@@ -1,6 +1,7 @@
 """Launch one tcgen05 GEMM per (T, pair mode) for an ncu capture:
   PPD_ONE="T:N:K:splits:pair,..." python tools/gemm_one.py
-Each shape is launched 3 times (ncu -c/-s pick which)."""
+Each shape is launched 3 times (ncu -c/-s pick which); splits 0 = the fused
+SiLU gate|up GEMM."""
 import os
 import sys
 
@@ -18,9 +19,13 @@ def main():
         ppd.check(L.ppd_set_tuning(b"gemm_pair", pair))
         A = torch.randn(T, K, device="cuda").to(torch.bfloat16)
         B = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
-        C = torch.empty(sp, T, N, device="cuda")
+        C = torch.empty(max(sp, 1), T, N, device="cuda")
+        m = torch.empty(T, N // 2, device="cuda", dtype=torch.bfloat16)
         for _ in range(3):
-            ppd.check(L.ppd_op_gemm_tc(A.data_ptr(), B.data_ptr(), C.data_ptr(), T, N, K, 1, sp, None))
+            if sp == 0:  # fused SiLU gate|up epilogue (bf16 m out)
+                ppd.check(L.ppd_op_gemm_silu(A.data_ptr(), B.data_ptr(), m.data_ptr(), T, N, K, None))
+            else:
+                ppd.check(L.ppd_op_gemm_tc(A.data_ptr(), B.data_ptr(), C.data_ptr(), T, N, K, 1, sp, None))
         torch.cuda.synchronize()
         print(item, "ok", flush=True)
 
