@@ -166,3 +166,24 @@ def test_qwen_shape_bias_group5_parity(gpu):
     new = rng.integers(0, cfg.vocab, 30)
     compare(dev, model, pool, [1, 30], ctx, np.concatenate([tok[:1], new]), bts)
     dev.close()
+
+
+def test_prefill_size_step_fused_silu_auto(pair):
+    """A step of >= 512 token rows takes the default fused-SiLU gate|up GEMM
+    (device.cu kMlpFusedMinRows) and, for pure prefill, the persistent tcgen05
+    prefill attention: a 600-token full prefill + a 130-token append over it in
+    one later step, then decode, all against the oracle."""
+    cfg, dev, model, pool = pair
+    rng = np.random.default_rng(29)
+    bts = np.array([np.arange(16, 56), np.arange(56, 96)], dtype=np.int32)  # 40 blocks = 640 tokens each
+    a = rng.integers(0, cfg.vocab, 600)
+    tok, _ = compare(dev, model, pool, [600], [0], a, bts[:1])
+    b = rng.integers(0, cfg.vocab, 430)
+    tok_b, _ = compare(dev, model, pool, [430], [0], b, bts[1:])
+    # one 531-row step: A decodes while B appends 130 tokens over its 430
+    new = rng.integers(0, cfg.vocab, 130)
+    tok2, _ = compare(dev, model, pool, [1, 130], [600, 430], np.concatenate([tok, new]), bts)
+    ctx = np.array([601, 560])
+    for _ in range(2):
+        tok2, _ = compare(dev, model, pool, [1, 1], ctx, tok2, bts)
+        ctx += 1
