@@ -635,7 +635,13 @@ int max_pair_slots(int smem, int occ) {
   return n;
 }
 
-Shape shape_for(int T, int N, int extra_smem = 0, bool force_single = false) {
+// Auto mode for 257-512-row steps (two token sub-tiles per unit, one
+// accumulator set): the CTA pair also when K is long (down projection:
+// 41.7 vs 45.7 us at T=328), and never the balanced partition (uniform splits
+// measured 4-30% faster per shape, 4% on the mixed step; tools/gemm_rot.py,
+// tools/ab_step.py).
+constexpr int kSubPairMinK = 8192;
+Shape shape_for(int T, int N, int K, int extra_smem = 0, bool force_single = false) {
   Shape sh{};
   if (T <= kMaxBN) {
     sh.n_sub = 1;
@@ -649,7 +655,8 @@ Shape shape_for(int T, int N, int extra_smem = 0, bool force_single = false) {
   }
   sh.unit_t = sh.bn * sh.n_sub;
   const double tiles1 = double((N + kBM - 1) / kBM) * ((T + sh.unit_t - 1) / sh.unit_t);
-  const bool auto_pair = T >= kPairMinT && tiles1 >= kPairMinTilesPerSm * 148;
+  const bool auto_pair =
+      T >= kPairMinT && (tiles1 >= kPairMinTilesPerSm * 148 || (sh.n_sub > 1 && K >= kSubPairMinK));
   const bool want_occ2 = sh.n_sub == 1 && extra_smem == 0 && (g_occ2 == 1 || (g_occ2 < 0 && T <= kOcc2MaxT));
   sh.pair = !force_single && (g_pair_mode == 1 || (g_pair_mode < 0 && auto_pair && !want_occ2));
   sh.rows = sh.pair ? 2 * kBM : kBM;
@@ -664,7 +671,7 @@ Shape shape_for(int T, int N, int extra_smem = 0, bool force_single = false) {
   sh.slots = 148 * sh.occ;
   if (sh.pair) {
     sh.slots = max_pair_slots(sh.smem, sh.occ);
-    if (sh.slots <= 0) return shape_for(T, N, extra_smem, true);  // no co-resident pair fits: single-CTA kernel
+    if (sh.slots <= 0) return shape_for(T, N, K, extra_smem, true);  // no co-resident pair fits: single-CTA kernel
   }
   return sh;
 }
@@ -699,7 +706,7 @@ Plan plan_for(const Shape& sh, int T, int N, int K, int max_slices) {
       best = Plan{false, s, units < sh.slots ? units : sh.slots, s, 0};
     }
   }
-  if (g_sched != 0 && max_slices >= 2) {
+  if (g_sched != 0 && max_slices >= 2 && !(g_sched < 0 && sh.n_sub > 1)) {
     const long long total = (long long)tiles * kbt;
     const int slots = (int)(total < sh.slots ? total : sh.slots);
     const long long share = (total + slots - 1) / slots;
@@ -724,7 +731,7 @@ Plan plan_for(const Shape& sh, int T, int N, int K, int max_slices) {
 }  // namespace
 
 int gemm_tc_plan_splits(int T, int N, int K) {
-  const Shape sh = shape_for(T, N);
+  const Shape sh = shape_for(T, N, K);
   const int cap = 8 * 256 / (T > 0 ? T : 1);
   const int saved = g_sched;
   g_sched = 0;
@@ -777,7 +784,7 @@ cudaError_t gemm_tc_run(const bf16* X, const bf16* W, void* out, int T, int N, i
   if (K % 8 != 0) return cudaErrorInvalidValue;  // TMA row stride must be 16 B aligned
   if (splits < 1) splits = 1;
   if (splits > 1 && !out_f32) return cudaErrorInvalidValue;
-  const Shape sh = shape_for(T, N);
+  const Shape sh = shape_for(T, N, K);
   const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.unit_t - 1) / sh.unit_t);
   const int units = tiles * splits;
   const Plan pl{false, splits, units < sh.slots ? units : sh.slots, splits, 0};
@@ -788,7 +795,7 @@ cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, i
                               size_t split_stride, GemmParts* parts, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (K % 8 != 0 || max_slices < 1) return cudaErrorInvalidValue;
-  const Shape sh = shape_for(T, N);
+  const Shape sh = shape_for(T, N, K);
   const Plan pl = plan_for(sh, T, N, K, max_slices);
   GemmParts g;
   g.n = pl.n_slices;
@@ -806,7 +813,7 @@ cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, i
 cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N, int K, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (K % 8 != 0 || N % kBM != 0) return cudaErrorInvalidValue;  // whole gate|up groups per 128-row slab
-  const Shape sh = shape_for(T, N, kXchgBytes);
+  const Shape sh = shape_for(T, N, K, kXchgBytes);
   const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.unit_t - 1) / sh.unit_t);
   const Plan pl{false, 1, tiles < sh.slots ? tiles : sh.slots, 1, 0};
   return launch(sh, pl, X, W, m, T, N, K, false, 0, s, kEpiSilu);
