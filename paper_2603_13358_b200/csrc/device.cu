@@ -65,7 +65,7 @@ int g_mlp_fused = 2;
 bool g_ws_two_slices = true;
 constexpr int kMlpFusedMinRows = 512;
 // diagnostics only ("diag_skip" knob): skip kernel classes of the forward step
-// (1 small ops, 2 attention, 4 GEMMs) to time their marginal cost in the live
+// (1 small ops, 2 attention, 4 GEMMs; 8 rope_kv, 16 silu_mul, 32 add_rmsnorm) to time their marginal cost in the live
 // graph. Results are meaningless while set.
 int g_diag_skip = 0;
 constexpr int kAttnTargetCtas = 148 * 2 * 2;
@@ -587,12 +587,12 @@ int forward(ppd_dev* d, const StepLayout& L) {
     GemmParts np_qkv, np_o;
     const Layer& w = d->layers[l];
     // x += down(prev) ; h = norm(x)
-    if (!(g_diag_skip & 1)) CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, np_down, nullptr, d->ones, d->h, T, d_model,
+    if (!(g_diag_skip & (1 | 32))) CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, np_down, nullptr, d->ones, d->h, T, d_model,
                           c.rms_eps, s));
     PROF(1, false);
     if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->h, w.wqkv, d->qkv32, T, W, d_model, max_sl, &np_qkv, s));
     PROF(1, true);
-    if (!(g_diag_skip & 1)) CU(launch_rope_kv_write(d->qkv32, np_qkv, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
+    if (!(g_diag_skip & (1 | 8))) CU(launch_rope_kv_write(d->qkv32, np_qkv, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
                             d->rope_sin, d->q, d->kv, T, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers,
                             l, d->bt, s));
     PROF(0, false);
@@ -604,7 +604,7 @@ int forward(ppd_dev* d, const StepLayout& L) {
     PROF(1, false);
     if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->attn, w.wo, d->proj32, T, d_model, qd, max_sl, &np_o, s));
     PROF(1, true);
-    if (!(g_diag_skip & 1)) CU(launch_add_rmsnorm(d->x, d->proj32, np_o, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
+    if (!(g_diag_skip & (1 | 32))) CU(launch_add_rmsnorm(d->x, d->proj32, np_o, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
     PROF(1, false);
     if (g_mlp_fused == 1 || (g_mlp_fused == 2 && T >= kMlpFusedMinRows)) {
       if (!(g_diag_skip & 4)) CU(gemm_run_silu(d->gemm, d->h, w.wgu, d->m, d->gu32, T, 2 * F, d_model, s));
@@ -613,7 +613,7 @@ int forward(ppd_dev* d, const StepLayout& L) {
       GemmParts np_gu;
       if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->h, w.wgu, d->gu32, T, 2 * F, d_model, max_sl, &np_gu, s));
       PROF(1, true);
-      if (!(g_diag_skip & 1)) CU(launch_silu_mul(d->gu32, np_gu, d->m, T, F, s));
+      if (!(g_diag_skip & (1 | 16))) CU(launch_silu_mul(d->gu32, np_gu, d->m, T, F, s));
     }
     PROF(1, false);
     if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, max_sl, &np_down, s));
@@ -1130,7 +1130,7 @@ int ppd_set_tuning(const char* name, int32_t value) {
     CHECK_ARG(value >= 0 && value <= 16, "gemm_stages must be in [0, 16]");
     stages = value;
   } else if (std::strcmp(name, "diag_skip") == 0) {
-    CHECK_ARG(value >= 0 && value <= 7, "diag_skip must be in [0, 7]");
+    CHECK_ARG(value >= 0 && value <= 63, "diag_skip must be in [0, 63]");
     g_diag_skip = value;
   } else if (std::strcmp(name, "attn_pf_ctas") == 0) {
     CHECK_ARG(value >= 0 && value <= 146, "attn_pf_ctas must be in [0, 146]");
