@@ -59,7 +59,8 @@ constexpr float kRescaleThreshold = 8.0f;   // log2 domain
 // can only follow PV_{j-1}, and softmax waits out PV + S every other block).
 constexpr int kSBufs = (kPInTmem && kXchgSmem) ? 3 : 2;
 // diagnostics builds only (-DPPD_PF_DIAG=n, results wrong): 1 softmax without
-// exponentials, 2 PV reduced to one K slice, 3 S reduced to one K slice
+// exponentials, 2 PV reduced to one K slice, 3 S reduced to one K slice, 4 half
+// the S columns read from TMEM
 #ifndef PPD_PF_DIAG
 constexpr int kDiag = 0;
 #else
@@ -326,7 +327,14 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       tc::fence_after();
       uint32_t raw[CPT];
 #pragma unroll
-      for (int c0 = 0; c0 < CPT; c0 += 32) tc::ld32x32(tmem + lane_base + s_col(sb) + CPT * h + c0, raw + c0);
+      if (kDiag == 4) {  // diagnostics: one 32-column TMEM load, replicated (S read cost removed)
+        tc::ld32x32(tmem + lane_base + s_col(sb) + CPT * h, raw);
+#pragma unroll
+        for (int c = 32; c < CPT; ++c) raw[c] = raw[c - 32] ^ (uint32_t)c;
+      } else {
+#pragma unroll
+        for (int c0 = 0; c0 < CPT; c0 += 32) tc::ld32x32(tmem + lane_base + s_col(sb) + CPT * h + c0, raw + c0);
+      }
       tc::wait_ld();
       // raw (unscaled) scores; the scale folds into the exponent's FFMA below
       // (sl2 > 0: the max commutes with it)
