@@ -385,6 +385,14 @@ class DeviceCluster {
     // map outputs (only want rows produce tokens, in row order)
     step_out_.clear();
     for (std::size_t i = 0, k = 0; i < want.size(); ++i) step_out_.push_back(want[i] ? out[k++] : -1);
+    // a sampled id outside the vocabulary means non-finite logits: fail here,
+    // at the step that produced it, not when it is fed back a step later
+    for (std::size_t i = 0; i < want.size(); ++i)
+      if (want[i] && (step_out_[i] < 0 || step_out_[i] >= mcfg_.vocab))
+        throw std::runtime_error("device step produced token id " + std::to_string(step_out_[i]) + " on node " +
+                                 std::to_string(ni) + " (" + std::string(1, n.role) + ") row " + std::to_string(i) +
+                                 " of " + std::to_string(want.size()) + ": q_len " + std::to_string(q_len[i]) +
+                                 ", ctx " + std::to_string(ctx[i]) + ", step " + std::to_string(n.steps));
     n.steps += 1;
     n.device_ms += ms;
     n.decode_rows += long(n.running.size());

@@ -152,3 +152,20 @@ def test_device_clock_trace_replay(gpu):
     assert all(x["status"] == "completed" and x["output_tokens_emitted"] == want[(x["conv_id"], x["turn_index"])]
                for x in recs)
     assert all(x["route"] == "D_local" for x in recs if x["turn_index"] > 1)
+
+
+@pytest.mark.parametrize("cluster", ["2P_6D", "4P_4D"])
+@pytest.mark.parametrize("x", [0.0, 1.0])
+def test_device_eight_node_layouts(gpu, cluster, x):
+    """configs[3]-shaped multi-turn load on the 8-node layouts, all nodes on
+    one GPU (tiny model): every request completes with its target tokens and
+    the link carries the reference's delta rule."""
+    wl = {"id": "cfg4_tiny", "turn1": [64, 6], "turn2plus": [32, 6], "num_turns": 3, "qps": 24.0, "duration_s": 1.0}
+    job = {"cluster": cluster, "x": x, "clock": "device", "seed": 3, "workload": wl,
+           "device": {"model": "tiny", "weight_seed": 5, "token_seed": 9, "gpus": [0], "prefill_chunk": 64}}
+    r = E.run(job)
+    recs = E.records(r)
+    assert recs and all(x_["status"] == "completed" for x_ in recs)
+    assert all(x_["output_tokens_emitted"] == 6 for x_ in recs)
+    ref = E.run(dict(job, clock="virtual"))
+    assert len(E.records(ref)) == len(recs)
