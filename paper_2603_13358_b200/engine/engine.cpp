@@ -7,6 +7,8 @@
 //   kv_transfer_time             -> ppd_kv_copy of the missing tokens
 // The engine clock of a node advances by the CUDA-event duration of its own
 // step; nodes are independent GPUs (node i -> gpus[i % n]).
+#include <cstdlib>
+#include <fstream>
 #include <algorithm>
 #include <cmath>
 #include <deque>
@@ -388,11 +390,19 @@ class DeviceCluster {
     // a sampled id outside the vocabulary means non-finite logits: fail here,
     // at the step that produced it, not when it is fed back a step later
     for (std::size_t i = 0; i < want.size(); ++i)
-      if (want[i] && (step_out_[i] < 0 || step_out_[i] >= mcfg_.vocab))
+      if (want[i] && (step_out_[i] < 0 || step_out_[i] >= mcfg_.vocab)) {
+        if (const char* path = std::getenv("PPD_DUMP_BAD_STEP")) {  // replayable record of the failing step
+          std::ofstream f(path);
+          f << nlohmann::json{{"node", ni}, {"role", std::string(1, n.role)}, {"q_len", q_len}, {"ctx", ctx},
+                              {"tokens", toks}, {"block_tables", bt}, {"max_blocks", maxb}, {"want", want},
+                              {"out", step_out_}, {"step", n.steps}}
+                   .dump();
+        }
         throw std::runtime_error("device step produced token id " + std::to_string(step_out_[i]) + " on node " +
                                  std::to_string(ni) + " (" + std::string(1, n.role) + ") row " + std::to_string(i) +
                                  " of " + std::to_string(want.size()) + ": q_len " + std::to_string(q_len[i]) +
                                  ", ctx " + std::to_string(ctx[i]) + ", step " + std::to_string(n.steps));
+      }
     n.steps += 1;
     n.device_ms += ms;
     n.decode_rows += long(n.running.size());

@@ -15,6 +15,11 @@ from paper_2603_13358_b200 import engine as E  # noqa: E402
 
 
 def main():
+    import paper_2603_13358_b200 as ppd
+    os.environ.setdefault("PPD_DUMP_BAD_STEP", "gpurun_out/bad_step.json")
+    for kv in filter(None, os.environ.get("PPD_LAYOUT_KNOBS", "").split(",")):
+        k, v = kv.split("=")
+        ppd.check(ppd.lib().ppd_set_tuning(k.encode(), int(v)))
     qps = float(os.environ.get("PPD_LAYOUT_QPS", "8"))
     dur = float(os.environ.get("PPD_LAYOUT_DUR", "4"))
     wl = {"id": "cfg4", "turn1": [2048, 128], "turn2plus": [1024, 128], "num_turns": 3, "qps": qps,
@@ -27,7 +32,11 @@ def main():
                               "kv_blocks_per_node": int(os.environ.get("PPD_LAYOUT_KV", "2000")), "prefill_chunk": 2048,
                               "record_tokens": False}}
             t0 = time.perf_counter()
-            r = E.run(job)
+            try:
+                r = E.run(job)
+            except Exception as e:  # report and continue with the next run
+                print(json.dumps({"cluster": layout, "x": x, "error": str(e)}), flush=True)
+                continue
             a = r["aggregate"]
             ms = lambda v: None if v is None else round(v * 1e3, 2)
             out[f"x{int(x)}"] = {"ttft_t2_p50_ms": ms(a["ttft_t2_p50"]), "ttft_t2_p99_ms": ms(a["ttft_t2_p99"]),
@@ -35,8 +44,9 @@ def main():
                                  "link_transfers": r["link_transfers"], "link_gb": r["link_bytes"] / 1e9,
                                  "kv_transfer_gbs": r["device"]["kv_transfer"]["gbs"],
                                  "wall_s": round(time.perf_counter() - t0, 1)}
-        p50 = (out["x0"]["ttft_t2_p50_ms"], out["x1"]["ttft_t2_p50_ms"])
-        out["ttft_t2_p50_reduction"] = None if None in p50 else 1 - p50[1] / p50[0]
+        if "x0" in out and "x1" in out:
+            p50 = (out["x0"]["ttft_t2_p50_ms"], out["x1"]["ttft_t2_p50_ms"])
+            out["ttft_t2_p50_reduction"] = None if None in p50 else 1 - p50[1] / p50[0]
         print(json.dumps(out), flush=True)
 
 
