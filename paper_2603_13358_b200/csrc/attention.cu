@@ -700,10 +700,9 @@ __global__ void __launch_bounds__(kMixThreads, 1)
 
 cudaError_t launch_mixed_attention(const void* kv_map, const AttnParams& p, const AttnItem* pf_items, int n_pf,
                                    int n_pf_tiles, int n_vcta, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_devs = 0;
+  if (first_on_device(&attr_devs)) {
     cudaFuncSetAttribute(mixed_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMixSmem);
-    attr = true;
   }
   if (p.group > kDecMaxG || n_pf <= 0 || n_pf > n_pf_tiles || !p.mix_ctr) return cudaErrorInvalidValue;
   const int grid = n_pf + (n_vcta + 1) / 2;
@@ -713,10 +712,9 @@ cudaError_t launch_mixed_attention(const void* kv_map, const AttnParams& p, cons
 
 cudaError_t launch_decode_attention(const void* kv_map, const AttnParams& p, int n_cta, int group,
                                     cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_devs = 0;
+  if (first_on_device(&attr_devs)) {
     cudaFuncSetAttribute(decode_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
-    attr = true;
   }
   if (n_cta == 0) return cudaSuccess;
   if (group > kDecMaxG) return cudaErrorInvalidValue;
@@ -753,10 +751,9 @@ int make_kv_tensor_map(void* map_out, const void* pool, uint64_t total_rows) {
 
 cudaError_t launch_paged_attention(const void* kv_map, const AttnParams& p, int n_items,
                                    cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_devs = 0;
+  if (first_on_device(&attr_devs)) {
     cudaFuncSetAttribute(paged_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    attr = true;
   }
   if (n_items == 0) return cudaSuccess;
   dim3 grid(n_items, p.n_kv_heads);

@@ -71,11 +71,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 
 cudaError_t launch_prefill_attention_persistent(const void* kv_map, const AttnParams& p, const AttnItem* items,
                                                 int n_items, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_devs = 0;
+  if (first_on_device(&attr_devs)) {
     cudaFuncSetAttribute(prefill_attention_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          pftc::kSmem);
-    attr = true;
   }
   const int n_tiles = n_items * p.n_kv_heads;
   if (n_tiles == 0) return cudaSuccess;
@@ -86,10 +85,9 @@ cudaError_t launch_prefill_attention_persistent(const void* kv_map, const AttnPa
 }
 
 cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p, int n_items, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_devs = 0;
+  if (first_on_device(&attr_devs)) {
     cudaFuncSetAttribute(prefill_attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pftc::kSmem);
-    attr = true;
   }
   if (n_items == 0) return cudaSuccess;
   dim3 grid(n_items, p.n_kv_heads);

@@ -6,6 +6,18 @@
 
 #define PPD_DEV __device__ __forceinline__
 
+// Host: true the first time it is called for the current device with this
+// mask (function attributes such as the dynamic shared-memory limit belong to
+// the function's per-device context, so a process driving several GPUs, e.g.
+// the engine's disaggregated layouts, must set them on every device).
+inline bool first_on_device(unsigned long long* mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const unsigned long long bit = 1ull << dev;
+  if (__atomic_fetch_or(mask, bit, __ATOMIC_ACQ_REL) & bit) return false;
+  return true;
+}
+
 namespace ppdk {
 
 typedef __nv_bfloat16 bf16;

@@ -597,15 +597,14 @@ GemmKernel pick_kernel(bool pair, int epi, int occ, int n_sub) {
 }
 
 void set_smem_attrs() {
-  static bool done = false;
-  if (done) return;
+  static unsigned long long done_devs = 0;
+  if (!first_on_device(&done_devs)) return;
   const int bytes = 1024 + kSmemBudget + kBarBytes;
 #define PPD_ATTR(P, E, O, N)                                                                \
   cudaFuncSetAttribute(gemm_tc_kernel<P, E, O, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                        O == 2 ? kOcc2Smem : bytes);
   PPD_GEMM_KERNELS(PPD_ATTR)
 #undef PPD_ATTR
-  done = true;
 }
 
 int max_pair_slots(int smem, int occ) {
