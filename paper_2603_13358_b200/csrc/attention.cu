@@ -418,12 +418,18 @@ constexpr int kDecSmem = 1024 + kStages * kStageBytes + kConsumerWarps * kDecMax
 // over the segments of virtual CTA `vcta`, on `smem` (kDecSmemInst bytes,
 // 1024-aligned). bar_init (160 threads) / bar_cons (128 consumer threads) are
 // the instance's named barriers.
+// the instance's mbarriers: full[kStages] then empty[kStages]
+PPD_DEV uint64_t* decode_bars(uint8_t* smem) {
+  return reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes +
+                                     (kConsumerWarps * kDecMaxG * kDh + kConsumerWarps * kDecMaxG * 2) * 4);
+}
+
 PPD_DEV void decode_body(const CUtensorMap* kv_map, const AttnParams& p, uint8_t* smem, int vcta, int warp, int lane,
                          int bar_init, int bar_cons) {
   uint8_t* stage_base = smem;
   float* mo = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [warp][G][Dh]
   float* mml = mo + kConsumerWarps * kDecMaxG * kDh;                    // [warp][G][2]
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(mml + kConsumerWarps * kDecMaxG * 2);
+  uint64_t* full_bar = decode_bars(smem);
   uint64_t* empty_bar = full_bar + kStages;
   int* flag = reinterpret_cast<int*>(empty_bar + kStages);
 
@@ -691,6 +697,15 @@ __global__ void __launch_bounds__(kMixThreads, 1)
       decode_body(&kv_map, p, smem + inst * kDecSmemInst, v, lt >> 5, lt & 31, kMixBarDec + inst,
                   kMixBarDec + 2 + inst);
     named_barrier_sync(kMixBarAll, kMixThreads);  // both instances retired: smem free
+    // the prefill role reuses this smem for tiles and its own barriers: the
+    // decode instances' mbarrier objects are invalidated first (PTX: a
+    // location holding an mbarrier is repurposed only after mbarrier.inval)
+    if (threadIdx.x < 2 && ((int)blockIdx.x - n_pf) * 2 + (int)threadIdx.x < n_vcta) {
+      uint64_t* bars = decode_bars(smem + threadIdx.x * kDecSmemInst);
+      for (int i = 0; i < 2 * kStages; ++i)
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bars + i)) : "memory");
+    }
+    named_barrier_sync(kMixBarAll, kMixThreads);
   }
   // ---------------- prefill queue (all 12 warps)
   pftc::tile_queue<kMixSW>(&kv_map, p, smem, pf_items, n_pf_tiles, warp, lane, kMixBarPf, p.mix_ctr, p.mix_ctr + 1,
