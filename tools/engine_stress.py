@@ -1,3 +1,5 @@
+"""Device-engine stress with the tiny model: every (layout, routing x, prefill
+chunk, load) combination on GPU 0 must complete every request."""
 import sys, json, itertools
 sys.path.insert(0, '.')
 from paper_2603_13358_b200 import engine as E
