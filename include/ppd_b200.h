@@ -59,6 +59,10 @@ int ppd_kv_pool_init(ppd_dev* dev, int32_t block_tokens, int32_t num_blocks);
 /* bytes of one KV block (all layers, K and V, all kv heads) */
 int ppd_kv_block_bytes(const ppd_model_cfg* cfg, int32_t block_tokens, uint64_t* bytes);
 int ppd_kv_pool_ptr(ppd_dev* dev, void** ptr, uint64_t* bytes);
+/* Synchronous host <-> pool copies of a byte range (after the device's queued
+ * work): KV snapshot / restore, and how tests seed a cached context. */
+int ppd_kv_pool_write(ppd_dev* dev, uint64_t offset, const void* host, uint64_t bytes);
+int ppd_kv_pool_read(ppd_dev* dev, uint64_t offset, void* host, uint64_t bytes);
 
 /* One fused iteration over n_seqs sequences. Sequence s contributes q_len[s]
  * new tokens at positions ctx[s] .. ctx[s]+q_len[s]-1; their K/V are written
@@ -94,12 +98,33 @@ int ppd_prefill(ppd_dev* dev, int32_t kind, const int32_t* tokens, int32_t n_new
 
 /* Token-granular KV transfer of positions [start, start+n_tokens) of one
  * sequence from src's pool to dst's pool (the P->D hop, simulator.cpp:349-356).
- * Runs on dst's transfer stream over peer pointers (NVLink when src/dst are
- * different GPUs), fenced after src's compute stream; dst's next step waits on
- * it. *out_ms: device time of the copy. Bytes moved = n_tokens * kv bytes/token. */
+ * The copy kernel runs on dst's transfer stream and pulls over peer pointers
+ * (NVLink when src/dst are different GPUs), fenced after src's last submitted
+ * step. Bytes moved = n_tokens * kv bytes/token.
+ *
+ * ppd_kv_copy_submit is asynchronous: no host synchronisation, no allocation
+ * on the hot path (block tables travel through a preallocated pinned/device
+ * ring), and dst's compute stream is NOT blocked, so the hop overlaps dst's
+ * decode steps. Rows that read the copied tokens may be stepped only after
+ * ppd_kv_copy_wait(dst, ticket) returned (tickets of one dst are waited for
+ * in submission order, from any one thread; at most 64 in flight per dst).
+ * *out_ms: device time of the copy (CUDA events on the transfer stream).
+ * ppd_kv_copy = submit + wait (it first retires older tickets of dst). */
+int ppd_kv_copy_submit(ppd_dev* src, ppd_dev* dst, const int32_t* src_block_table,
+                       const int32_t* dst_block_table, int32_t n_blocks, int32_t start,
+                       int32_t n_tokens, uint64_t* ticket);
+int ppd_kv_copy_wait(ppd_dev* dst, uint64_t ticket, float* out_ms);
 int ppd_kv_copy(ppd_dev* src, ppd_dev* dst, const int32_t* src_block_table,
                 const int32_t* dst_block_table, int32_t n_blocks, int32_t start,
                 int32_t n_tokens, float* out_ms);
+/* NVLink roofline probe: GB/s of `bytes` moved src_gpu -> dst_gpu, best of
+ * `iters` (mode 0 copy engines / cudaMemcpyPeerAsync, mode 1 SM pull kernel
+ * on dst, the K7 access pattern). src_gpu == dst_gpu measures an HBM copy. */
+int ppd_p2p_bandwidth(int32_t src_gpu, int32_t dst_gpu, uint64_t bytes, int32_t iters, int32_t mode,
+                      double* gbs);
+/* Weights of one node: bytes resident and how many open devices share them
+ * (nodes on the same GPU with the same shape and seed share one copy). */
+int ppd_weights_info(ppd_dev* dev, uint64_t* bytes, int32_t* shared_by);
 
 /* ---- instrumentation (CUDA events on the compute stream, per kernel class) ----
  * With profiling on, every attention launch and every GEMM of a step is

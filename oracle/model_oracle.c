@@ -91,6 +91,13 @@ static uint16_t* gen_tensor(uint64_t seed, int tensor, int layer, size_t n) {
   return p;
 }
 
+/* n consecutive weights of one logical tensor (the fixture generator loads
+ * these into the HF reference models, tests/golden/make_hf_fixtures.py) */
+void mo_fill_tensor(uint64_t seed, int tensor, int layer, uint64_t n, uint16_t* out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)n; ++i) out[i] = mo_weight_bf16(seed, tensor, layer, (uint64_t)i);
+}
+
 static float* gen_bias(uint64_t seed, int tensor, int layer, size_t n) {
   float* p = (float*)malloc(n * sizeof(float));
   for (size_t i = 0; i < n; ++i) p[i] = mo_bf16_to_f32(mo_weight_bf16(seed, tensor, layer, i));
@@ -228,6 +235,7 @@ void mo_attention_paged(const mo_cfg* c, const uint16_t* q, const uint16_t* kv, 
           int blk = block_tables[(size_t)s * max_blocks + j / bt];
           const uint16_t* kr = kv + kv_index(c, bt, blk, layer, 0, hk, j % bt, 0);
           float acc = 0.f;
+#pragma omp simd reduction(+ : acc)
           for (int d = 0; d < Dh; ++d) acc += mo_bf16_to_f32(qr[d]) * mo_bf16_to_f32(kr[d]);
           sc[j] = acc * scale;
           if (sc[j] > mx) mx = sc[j];

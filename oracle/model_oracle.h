@@ -37,6 +37,8 @@ enum { MO_T_EMBED = 0, MO_T_WQ = 1, MO_T_WK = 2, MO_T_WV = 3, MO_T_WO = 4,
 
 uint16_t mo_weight_bf16(uint64_t seed, int tensor, int layer, uint64_t idx);
 uint16_t mo_f32_to_bf16(float f);
+/* out[i] = mo_weight_bf16(seed, tensor, layer, i), i < n (OpenMP) */
+void mo_fill_tensor(uint64_t seed, int tensor, int layer, uint64_t n, uint16_t* out);
 float mo_bf16_to_f32(uint16_t h);
 uint32_t mo_token_id(uint64_t seed, uint64_t conv_hash, int turn, int64_t pos, int vocab);
 

@@ -59,6 +59,7 @@ def lib():
         L.mo_step.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, i32, vp, vp, vp]
         L.mo_attention_paged.argtypes = [ctypes.POINTER(MoCfg), vp, vp, i32, i32, i32, vp, vp, vp, i32, vp]
         L.mo_rope_table.argtypes = [ctypes.c_float, i32, i32, vp, vp]
+        L.mo_fill_tensor.argtypes = [u64, i32, i32, u64, vp]
         _lib = L
     return _lib
 
@@ -86,6 +87,14 @@ def f32_to_bf16(a: np.ndarray) -> np.ndarray:
 
 def weight(seed: int, tensor: int, layer: int, idx: int) -> int:
     return lib().mo_weight_bf16(seed, tensor, layer, idx)
+
+
+def tensor_bf16(seed: int, tensor: int, layer: int, n: int) -> np.ndarray:
+    """The first n weights of one logical tensor (bf16 bits), the same values
+    the device fill kernels and mo_model_create produce."""
+    out = np.empty(n, dtype=np.uint16)
+    lib().mo_fill_tensor(seed, tensor, layer, n, _p(out))
+    return out
 
 
 class KvPool:

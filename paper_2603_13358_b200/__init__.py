@@ -120,12 +120,18 @@ def load_lib(path: str = LIB_PATH, strict: bool = True):
         "ppd_kv_pool_init": [vp, i32, i32],
         "ppd_kv_block_bytes": [P(ModelCfg), i32, P(u64)],
         "ppd_kv_pool_ptr": [vp, P(vp), P(u64)],
+        "ppd_kv_pool_write": [vp, u64, vp, u64],
+        "ppd_kv_pool_read": [vp, u64, vp, u64],
         "ppd_step": [vp, P(Batch), vp, P(ctypes.c_float)],
         "ppd_step_submit": [vp, P(Batch)],
         "ppd_step_wait": [vp, vp, P(ctypes.c_float)],
         "ppd_last_logits": [vp, vp, i64],
         "ppd_prefill": [vp, i32, vp, i32, i32, vp, i32, vp, P(ctypes.c_float)],
         "ppd_kv_copy": [vp, vp, vp, vp, i32, i32, i32, P(ctypes.c_float)],
+        "ppd_kv_copy_submit": [vp, vp, vp, vp, i32, i32, i32, P(u64)],
+        "ppd_kv_copy_wait": [vp, u64, P(ctypes.c_float)],
+        "ppd_p2p_bandwidth": [i32, i32, u64, i32, i32, P(ctypes.c_double)],
+        "ppd_weights_info": [vp, P(u64), P(i32)],
         "ppd_op_attention": [P(ModelCfg), vp, vp, i32, i32, i32, i32, vp, vp, vp, i32, vp, vp],
         "ppd_op_gemm": [vp, vp, vp, i32, i32, i32, i32, vp],
         "ppd_op_gemm_tc": [vp, vp, vp, i32, i32, i32, i32, i32, vp],
@@ -208,6 +214,22 @@ class Device:
         check(lib().ppd_kv_pool_ptr(self.h, ctypes.byref(p), ctypes.byref(n)))
         return p.value, n.value
 
+    def weights_info(self):
+        n, k = ctypes.c_uint64(), ctypes.c_int32()
+        check(lib().ppd_weights_info(self.h, ctypes.byref(n), ctypes.byref(k)))
+        return n.value, k.value
+
+    def kv_pool_write(self, host: np.ndarray, offset: int = 0):
+        host = np.ascontiguousarray(host)
+        check(lib().ppd_kv_pool_write(self.h, offset, _ptr(host), host.nbytes))
+
+    def kv_pool_read(self, n_bytes: int = None, offset: int = 0) -> np.ndarray:
+        if n_bytes is None:
+            n_bytes = self.kv_pool_ptr()[1] - offset
+        out = np.empty(n_bytes // 2, dtype=np.uint16)
+        check(lib().ppd_kv_pool_read(self.h, offset, _ptr(out), out.nbytes))
+        return out
+
     def _batch(self, q_len, ctx, tokens, block_tables, want_token=None):
         q_len, ctx, tokens = _i32(q_len), _i32(ctx), _i32(tokens)
         bt = _i32(block_tables)
@@ -274,6 +296,26 @@ def kv_copy(src: Device, dst: Device, src_blocks, dst_blocks, start: int, n_toke
     ms = ctypes.c_float()
     check(lib().ppd_kv_copy(src.h, dst.h, _ptr(sb), _ptr(db), len(sb), start, n_tokens, ctypes.byref(ms)))
     return ms.value
+
+
+def kv_copy_submit(src: Device, dst: Device, src_blocks, dst_blocks, start: int, n_tokens: int) -> int:
+    sb, db = _i32(src_blocks), _i32(dst_blocks)
+    assert len(sb) == len(db)
+    t = ctypes.c_uint64()
+    check(lib().ppd_kv_copy_submit(src.h, dst.h, _ptr(sb), _ptr(db), len(sb), start, n_tokens, ctypes.byref(t)))
+    return t.value
+
+
+def kv_copy_wait(dst: Device, ticket: int) -> float:
+    ms = ctypes.c_float()
+    check(lib().ppd_kv_copy_wait(dst.h, ticket, ctypes.byref(ms)))
+    return ms.value
+
+
+def p2p_bandwidth(src_gpu: int, dst_gpu: int, n_bytes: int = 1 << 30, iters: int = 5, mode: int = 0) -> float:
+    gbs = ctypes.c_double()
+    check(lib().ppd_p2p_bandwidth(src_gpu, dst_gpu, n_bytes, iters, mode, ctypes.byref(gbs)))
+    return gbs.value
 
 
 def kv_block_bytes(cfg: ModelCfg, block_tokens: int = 16) -> int:

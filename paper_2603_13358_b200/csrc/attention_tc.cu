@@ -79,7 +79,7 @@ cudaError_t launch_prefill_attention_persistent(const void* kv_map, const AttnPa
   const int n_tiles = n_items * p.n_kv_heads;
   if (n_tiles == 0) return cudaSuccess;
   if (!p.mix_ctr) return cudaErrorInvalidValue;
-  const int grid = n_tiles < 148 ? n_tiles : 148;
+  const int grid = n_tiles < device_sms() ? n_tiles : device_sms();
   return launch_pdl(prefill_attention_persistent_kernel, dim3(grid), dim3(kPfThreads), pftc::kSmem, stream,
                     *reinterpret_cast<const CUtensorMap*>(kv_map), p, items, n_tiles);
 }

@@ -18,6 +18,19 @@ inline bool first_on_device(unsigned long long* mask) {
   return true;
 }
 
+// Host: SM count of the current device (queried once per device; B200: 148).
+// Grids, persistent-kernel slots and schedule cuts are sized from it.
+inline int device_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  int n = __atomic_load_n(&cache[dev], __ATOMIC_ACQUIRE);
+  if (n > 0) return n;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  __atomic_store_n(&cache[dev], n, __ATOMIC_RELEASE);
+  return n;
+}
+
 namespace ppdk {
 
 typedef __nv_bfloat16 bf16;

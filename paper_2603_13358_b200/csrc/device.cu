@@ -16,13 +16,16 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <atomic>
 #include <map>
+#include <mutex>
 #include <tuple>
 #include <vector>
 
 #include "../../include/ppd_b200.h"
 #include "gemm.h"
 #include "gemm_tc.h"
+#include "common.cuh"
 #include "kernels.h"
 
 using namespace ppdk;
@@ -64,11 +67,6 @@ int g_mlp_fused = 2;
 // workspaces sized for two K-partial slices of a max-size step (see alloc_workspaces)
 bool g_ws_two_slices = true;
 constexpr int kMlpFusedMinRows = 512;
-// diagnostics only ("diag_skip" knob): skip kernel classes of the forward step
-// (1 small ops, 2 attention, 4 GEMMs; 8 rope_kv, 16 silu_mul, 32 add_rmsnorm) to time their marginal cost in the live
-// graph. Results are meaningless while set.
-int g_diag_skip = 0;
-constexpr int kAttnTargetCtas = 148 * 2 * 2;
 
 struct Layer {
   bf16 *wqkv, *wo, *wgu, *wdown;
@@ -92,6 +90,29 @@ int validate_cfg(const ppd_model_cfg* c) {
 
 }  // namespace
 
+// One in-flight P->D KV hop on the destination's transfer stream
+// (ppd_kv_copy_submit / ppd_kv_copy_wait): its timing events and the
+// preallocated block-table staging (pinned host + device), reused per ticket.
+struct CopySlot {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int32_t* h_bt = nullptr;  // pinned [2 * cap]
+  int32_t* d_bt = nullptr;  // device [2 * cap]
+  int cap = 0;              // blocks per table
+};
+constexpr int kCopySlots = 64;
+
+// Weights are read-only and a pure function of (shape, seed): nodes opened on
+// the same GPU with the same model share one resident copy (an 8-node layout
+// colocated on one B200 holds 16 GB of Llama-3-8B weights, not 128 GB).
+struct SharedWeights {
+  int gpu = 0;
+  ppd_model_cfg cfg{};
+  uint64_t seed = 0;
+  void* mem = nullptr;
+  size_t bytes = 0;
+  int refs = 0;
+};
+
 struct ppd_dev {
   int gpu = 0;
   ppd_model_cfg cfg{};
@@ -99,10 +120,8 @@ struct ppd_dev {
   size_t ws_rows = 0;  // token rows of fp32 GEMM-output workspace (holds K-partial slices)
   cudaStream_t compute = nullptr, xfer = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, xev0 = nullptr, xev1 = nullptr, compute_done = nullptr;
-  GemmContext* gemm = nullptr;
-  // weights
-  void* wmem = nullptr;
-  size_t wbytes = 0;
+  // weights (possibly shared with other nodes on this GPU)
+  SharedWeights* wshared = nullptr;
   bf16 *embed = nullptr, *lm_head = nullptr, *ones = nullptr;
   std::vector<Layer> layers;
   bool weights_ready = false;
@@ -138,6 +157,10 @@ struct ppd_dev {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> prof_marks;  // (kind 0 attn / 1 gemm, first event index)
   int ev_used = 0;
+  // KV hops INTO this device (it is the destination): ticket t uses slot t % kCopySlots
+  CopySlot copy[kCopySlots];
+  std::atomic<uint64_t> copy_head{0}, copy_done{0};
+  uint64_t peer_mask = 0;  // source GPUs peer access was enabled for
 };
 
 namespace {
@@ -182,8 +205,9 @@ void build_items(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads
     }
   }
   int want = 1;
-  if (n_decode > 0 && base_ctas < kAttnTargetCtas)
-    want = (int)((kAttnTargetCtas + base_ctas - 1) / std::max<long>(base_ctas, 1));
+  const long target_ctas = 4L * device_sms();
+  if (n_decode > 0 && base_ctas < target_ctas)
+    want = (int)((target_ctas + base_ctas - 1) / std::max<long>(base_ctas, 1));
   for (int s = 0; s < n; ++s) {
     if (q_len[s] <= 0) continue;
     if (q_len[s] == 1) {
@@ -238,7 +262,7 @@ bool decode_persistent_enabled(int group) {
 // the split workspace. Replaces the decode items of `items` (kept first) and
 // fills seg_start[n_cta + 1].
 void balance_decode(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads, std::vector<AttnItem>& items,
-                    int& n_ws, int& n_dec, std::vector<int>& seg_start, int kMaxCtas = 148 * 2) {
+                    int& n_ws, int& n_dec, std::vector<int>& seg_start, int kMaxCtas) {
   constexpr int kStageKeys = 64;
   long U = 0;
   for (int s = 0; s < n; ++s)
@@ -298,23 +322,23 @@ void balance_decode(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_he
 }
 
 // K2 (mixed_attention_kernel) SM split: n_pf CTAs start on the prefill queue,
-// the decode schedule is cut for the other 148 - n_pf SMs (two instances
+// the decode schedule is cut for the other sms - n_pf SMs (two instances
 // each) and those join the prefill queue when their decode work is done.
 // Cost model (B200, tools/ab_step.py PPD_AB_MIX sweeps of attn_pf_ctas):
 // decode streams min(5.6 TB/s, 44 GB/s per SM); a tile inside this launch
 // costs ~4 us + 6 us per 128-key block on one SM; prefill work left at the
-// end of decode is shared by all 148 SMs.
-int plan_mixed_split(double dec_bytes, const std::vector<double>& tile_cost) {
+// end of decode is shared by all SMs.
+int plan_mixed_split(double dec_bytes, const std::vector<double>& tile_cost, int sms) {
   const int n_tiles = (int)tile_cost.size();
   if (dec_bytes <= 0 || n_tiles == 0) return 0;
   double pf = 0;
   for (double c : tile_cost) pf += c;
   int best = 1;
   double best_t = 1e30;
-  for (int n_pf = 1; n_pf <= std::min(n_tiles, 146); ++n_pf) {
-    const double t_dec = dec_bytes / std::min(5.6e12, (148 - n_pf) * 44e9);
+  for (int n_pf = 1; n_pf <= std::min(n_tiles, sms - 2); ++n_pf) {
+    const double t_dec = dec_bytes / std::min(5.6e12, (sms - n_pf) * 44e9);
     const double rest = std::max(0.0, pf - n_pf * t_dec);
-    const double t = t_dec + rest / 148 + (rest > 0 ? tile_cost[0] : 0.0);  // + one tile of tail
+    const double t = t_dec + rest / sms + (rest > 0 ? tile_cost[0] : 0.0);  // + one tile of tail
     if (t < best_t * 0.999) {
       best_t = t;
       best = n_pf;
@@ -332,6 +356,7 @@ bool g_attn_pf_persist = true;  // tuning "attn_pf_persist": persistent tile que
 void plan_attention(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads, int G,
                     std::vector<AttnItem>& items, int& n_ws, int& n_dec, std::vector<int>& seg_start, int& n_pf) {
   build_items(n, q_len, ctx, n_kv_heads, G, items, n_ws, n_dec);
+  const int sms = device_sms();
   seg_start.clear();
   n_pf = 0;
   if (!decode_persistent_enabled(G)) return;
@@ -355,9 +380,9 @@ void plan_attention(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_he
     double dec_bytes = 0;
     for (int s = 0; s < n; ++s)
       if (q_len[s] == 1) dec_bytes += (double)(ctx[s] + 1) * n_kv_heads * 2 * 128 * 2;
-    n_pf = g_attn_pf_ctas > 0 ? std::min<int>(g_attn_pf_ctas, (int)cost.size()) : plan_mixed_split(dec_bytes, cost);
+    n_pf = g_attn_pf_ctas > 0 ? std::min<int>(g_attn_pf_ctas, (int)cost.size()) : plan_mixed_split(dec_bytes, cost, sms);
   }
-  balance_decode(n, q_len, ctx, n_kv_heads, items, n_ws, n_dec, seg_start, n_pf > 0 ? 2 * (148 - n_pf) : 296);
+  balance_decode(n, q_len, ctx, n_kv_heads, items, n_ws, n_dec, seg_start, n_pf > 0 ? 2 * (sms - n_pf) : 2 * sms);
   if (seg_start.empty()) n_pf = 0;
 }
 
@@ -536,10 +561,7 @@ void count_launches(ppd_dev* d, const StepLayout& L) {
   const long nl = d->cfg.n_layers;
   // own kernels per layer: add_rmsnorm x2, rope_kv, attention, silu_mul; + embed, final norm, argmax
   d->stats.own_launches += 5 * nl + 3;
-  if (gemm_uses_tcgen05(d->gemm))
-    d->stats.own_launches += 4 * nl + 1;
-  else
-    d->stats.lib_launches += 4 * nl + 1;
+  d->stats.own_launches += 4 * nl + 1;  // tcgen05 GEMMs
   d->stats.attn_launches += nl;
   d->stats.attn_bytes += L.attn_bytes * nl;
 }
@@ -587,42 +609,42 @@ int forward(ppd_dev* d, const StepLayout& L) {
     GemmParts np_qkv, np_o;
     const Layer& w = d->layers[l];
     // x += down(prev) ; h = norm(x)
-    if (!(g_diag_skip & (1 | 32))) CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, np_down, nullptr, d->ones, d->h, T, d_model,
+    CU(launch_add_rmsnorm(d->x, l == 0 ? nullptr : d->down32, np_down, nullptr, d->ones, d->h, T, d_model,
                           c.rms_eps, s));
     PROF(1, false);
-    if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->h, w.wqkv, d->qkv32, T, W, d_model, max_sl, &np_qkv, s));
+    CU(gemm_run_split(d->h, w.wqkv, d->qkv32, T, W, d_model, max_sl, &np_qkv, s));
     PROF(1, true);
-    if (!(g_diag_skip & (1 | 8))) CU(launch_rope_kv_write(d->qkv32, np_qkv, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
+    CU(launch_rope_kv_write(d->qkv32, np_qkv, w.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
                             d->rope_sin, d->q, d->kv, T, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers,
                             l, d->bt, s));
     PROF(0, false);
-    int rc = (g_diag_skip & 2) ? 0 : run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items,
+    int rc = run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items,
                            at<int>(m, L.off_seg), L.n_cta, L.n_pf, l, d->ws_o, d->ws_ml, d->counters,
                            d->counters + (size_t)d->max_S * c.n_kv_heads, s);
     if (rc) return rc;
     PROF(0, true);
     PROF(1, false);
-    if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->attn, w.wo, d->proj32, T, d_model, qd, max_sl, &np_o, s));
+    CU(gemm_run_split(d->attn, w.wo, d->proj32, T, d_model, qd, max_sl, &np_o, s));
     PROF(1, true);
-    if (!(g_diag_skip & (1 | 32))) CU(launch_add_rmsnorm(d->x, d->proj32, np_o, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
+    CU(launch_add_rmsnorm(d->x, d->proj32, np_o, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
     PROF(1, false);
     if (g_mlp_fused == 1 || (g_mlp_fused == 2 && T >= kMlpFusedMinRows)) {
-      if (!(g_diag_skip & 4)) CU(gemm_run_silu(d->gemm, d->h, w.wgu, d->m, d->gu32, T, 2 * F, d_model, s));
+      CU(gemm_run_silu(d->h, w.wgu, d->m, T, 2 * F, d_model, s));
       PROF(1, true);
     } else {
       GemmParts np_gu;
-      if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->h, w.wgu, d->gu32, T, 2 * F, d_model, max_sl, &np_gu, s));
+      CU(gemm_run_split(d->h, w.wgu, d->gu32, T, 2 * F, d_model, max_sl, &np_gu, s));
       PROF(1, true);
-      if (!(g_diag_skip & (1 | 16))) CU(launch_silu_mul(d->gu32, np_gu, d->m, T, F, s));
+      CU(launch_silu_mul(d->gu32, np_gu, d->m, T, F, s));
     }
     PROF(1, false);
-    if (!(g_diag_skip & 4)) CU(gemm_run_split(d->gemm, d->m, w.wdown, d->down32, T, d_model, F, max_sl, &np_down, s));
+    CU(gemm_run_split(d->m, w.wdown, d->down32, T, d_model, F, max_sl, &np_down, s));
     PROF(1, true);
   }
   count_launches(d, L);
   CU(launch_final_norm(d->x, d->down32, np_down, nullptr, outrows, L.n_out, d->ones, d->hl, T, d_model,
                        c.rms_eps, s));
-  CU(gemm_run(d->gemm, d->hl, d->lm_head, d->logits, L.n_out, c.vocab, d_model, true, s));
+  CU(gemm_run(d->hl, d->lm_head, d->logits, L.n_out, c.vocab, d_model, true, s));
   CU(launch_argmax(d->logits, L.n_out, c.vocab, d->d_tokens_out, s));
   return PPD_OK;
 }
@@ -671,15 +693,38 @@ int alloc_workspaces(ppd_dev* d) {
   return PPD_OK;
 }
 
+std::mutex g_weights_mu;
+std::vector<SharedWeights*> g_weights;
+
+bool same_cfg(const ppd_model_cfg& a, const ppd_model_cfg& b) { return std::memcmp(&a, &b, sizeof(a)) == 0; }
+
+void release_weights(ppd_dev* d) {
+  if (!d->wshared) return;
+  std::lock_guard<std::mutex> lk(g_weights_mu);
+  SharedWeights* w = d->wshared;
+  d->wshared = nullptr;
+  if (--w->refs > 0) return;
+  cudaFree(w->mem);
+  g_weights.erase(std::find(g_weights.begin(), g_weights.end(), w));
+  delete w;
+}
+
 void free_all(ppd_dev* d) {
-  void* dev_ptrs[] = {d->wmem, d->kv, d->x, d->h, d->q, d->attn, d->m, d->hl, d->qkv32, d->proj32,
+  release_weights(d);
+  for (CopySlot& c : d->copy) {
+    if (c.e0) cudaEventDestroy(c.e0);
+    if (c.e1) cudaEventDestroy(c.e1);
+    if (c.h_bt) cudaFreeHost(c.h_bt);
+    if (c.d_bt) cudaFree(c.d_bt);
+    c = CopySlot{};
+  }
+  void* dev_ptrs[] = {d->kv, d->x, d->h, d->q, d->attn, d->m, d->hl, d->qkv32, d->proj32,
                       d->gu32, d->down32, d->logits, d->ws_o, d->ws_ml, d->counters, d->d_meta,
                       d->d_tokens_out, d->rope_cos, d->rope_sin};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (d->h_meta) cudaFreeHost(d->h_meta);
   if (d->h_tokens_out) cudaFreeHost(d->h_tokens_out);
-  if (d->gemm) gemm_destroy(d->gemm);
   cudaEvent_t evs[] = {d->ev0, d->ev1, d->xev0, d->xev1, d->compute_done};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
@@ -740,8 +785,6 @@ int ppd_dev_open(int32_t gpu, const ppd_model_cfg* cfg, int32_t max_step_tokens,
       cudaEventCreate(&d->xev0) != cudaSuccess || cudaEventCreate(&d->xev1) != cudaSuccess ||
       cudaEventCreateWithFlags(&d->compute_done, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(PPD_ERR_CUDA, "stream/event creation failed"));
-  d->gemm = gemm_create();
-  if (!d->gemm) return bail(fail(PPD_ERR_CUDA, "gemm context creation failed"));
   rc = alloc_workspaces(d);
   if (rc) return bail(rc);
   *out = d;
@@ -767,11 +810,34 @@ int ppd_load_random_weights(ppd_dev* d, uint64_t seed) {
                            align_up(2 * F * dm * 2, 256) + align_up(dm * F * 2, 256) +
                            align_up((qd + 2 * kd) * 4, 256);
   const size_t total = 2 * align_up(V * dm * 2, 256) + align_up(dm * 2, 256) + per_layer * c.n_layers;
-  if (!d->wmem) {
-    CU(cudaMalloc(&d->wmem, total));
-    d->wbytes = total;
+  std::lock_guard<std::mutex> lk(g_weights_mu);
+  SharedWeights* w = nullptr;
+  for (SharedWeights* e : g_weights)
+    if (e->gpu == d->gpu && e->seed == seed && same_cfg(e->cfg, c)) w = e;
+  const bool fresh = w == nullptr;
+  if (d->wshared && d->wshared != w) {  // re-seeding: drop the old set first
+    SharedWeights* old = d->wshared;
+    d->wshared = nullptr;
+    if (--old->refs == 0) {
+      cudaFree(old->mem);
+      g_weights.erase(std::find(g_weights.begin(), g_weights.end(), old));
+      delete old;
+    }
   }
-  uint8_t* p = static_cast<uint8_t*>(d->wmem);
+  if (fresh) {
+    w = new SharedWeights{d->gpu, c, seed, nullptr, total, 0};
+    if (cudaMalloc(&w->mem, total) != cudaSuccess) {
+      cudaGetLastError();
+      delete w;
+      return fail(PPD_ERR_OOM, "weights: cudaMalloc of " + std::to_string(total) + " bytes failed");
+    }
+    g_weights.push_back(w);
+  }
+  if (d->wshared != w) {
+    d->wshared = w;
+    w->refs += 1;
+  }
+  uint8_t* p = static_cast<uint8_t*>(w->mem);
   auto take = [&](size_t bytes) {
     uint8_t* r = p;
     p += align_up(bytes, 256);
@@ -781,26 +847,37 @@ int ppd_load_random_weights(ppd_dev* d, uint64_t seed) {
   d->embed = reinterpret_cast<bf16*>(take(V * dm * 2));
   d->lm_head = reinterpret_cast<bf16*>(take(V * dm * 2));
   d->ones = reinterpret_cast<bf16*>(take(dm * 2));
-  CU(launch_fill_random(d->embed, V * dm, seed, 0, 0, s));
-  CU(launch_fill_matrix(d->lm_head, V, dm, seed, 8, 0, s));
-  CU(launch_fill_const(d->ones, dm, 1.0f, s));
+  if (fresh) {
+    CU(launch_fill_random(d->embed, V * dm, seed, 0, 0, s));
+    CU(launch_fill_matrix(d->lm_head, V, dm, seed, 8, 0, s));
+    CU(launch_fill_const(d->ones, dm, 1.0f, s));
+  }
   d->layers.assign(c.n_layers, Layer{});
   for (int l = 0; l < c.n_layers; ++l) {
-    Layer& w = d->layers[l];
-    w.wqkv = reinterpret_cast<bf16*>(take((qd + 2 * kd) * dm * 2));
-    w.wo = reinterpret_cast<bf16*>(take(dm * qd * 2));
-    w.wgu = reinterpret_cast<bf16*>(take(2 * F * dm * 2));
-    w.wdown = reinterpret_cast<bf16*>(take(dm * F * 2));
+    Layer& lw = d->layers[l];
+    lw.wqkv = reinterpret_cast<bf16*>(take((qd + 2 * kd) * dm * 2));
+    lw.wo = reinterpret_cast<bf16*>(take(dm * qd * 2));
+    lw.wgu = reinterpret_cast<bf16*>(take(2 * F * dm * 2));
+    lw.wdown = reinterpret_cast<bf16*>(take(dm * F * 2));
     float* b = reinterpret_cast<float*>(take((qd + 2 * kd) * 4));
-    w.bqkv = c.qkv_bias ? b : nullptr;
-    CU(launch_fill_qkv(w.wqkv, (int)qd, (int)kd, (int)dm, seed, l, s));
-    CU(launch_fill_matrix(w.wo, dm, qd, seed, 4, l, s));
-    CU(launch_fill_gate_up(w.wgu, (int)F, (int)dm, seed, l, s));
-    CU(launch_fill_matrix(w.wdown, dm, F, seed, 7, l, s));
-    if (c.qkv_bias) CU(launch_fill_bias(w.bqkv, (int)qd, (int)kd, seed, l, s));
+    lw.bqkv = c.qkv_bias ? b : nullptr;
+    if (!fresh) continue;
+    CU(launch_fill_qkv(lw.wqkv, (int)qd, (int)kd, (int)dm, seed, l, s));
+    CU(launch_fill_matrix(lw.wo, dm, qd, seed, 4, l, s));
+    CU(launch_fill_gate_up(lw.wgu, (int)F, (int)dm, seed, l, s));
+    CU(launch_fill_matrix(lw.wdown, dm, F, seed, 7, l, s));
+    if (c.qkv_bias) CU(launch_fill_bias(lw.bqkv, (int)qd, (int)kd, seed, l, s));
   }
   CU(cudaStreamSynchronize(s));
   d->weights_ready = true;
+  return PPD_OK;
+}
+
+int ppd_weights_info(ppd_dev* d, uint64_t* bytes, int32_t* shared_by) {
+  CHECK_ARG(d && bytes && shared_by, "null arg");
+  std::lock_guard<std::mutex> lk(g_weights_mu);
+  *bytes = d->wshared ? d->wshared->bytes : 0;
+  *shared_by = d->wshared ? d->wshared->refs : 0;
   return PPD_OK;
 }
 
@@ -830,6 +907,27 @@ int ppd_kv_pool_ptr(ppd_dev* d, void** ptr, uint64_t* bytes) {
   CHECK_ARG(d && ptr && bytes, "null arg");
   *ptr = d->kv;
   *bytes = d->kv_bytes;
+  return PPD_OK;
+}
+
+int ppd_kv_pool_write(ppd_dev* d, uint64_t offset, const void* host, uint64_t bytes) {
+  CHECK_ARG(d && host, "null arg");
+  CHECK_ARG(d->kv, "KV pool not initialised");
+  CHECK_ARG(offset <= d->kv_bytes && bytes <= d->kv_bytes - offset, "range outside the KV pool");
+  CU(cudaSetDevice(d->gpu));
+  CU(cudaStreamSynchronize(d->compute));
+  CU(cudaMemcpy(reinterpret_cast<uint8_t*>(d->kv) + offset, host, bytes, cudaMemcpyHostToDevice));
+  return PPD_OK;
+}
+
+int ppd_kv_pool_read(ppd_dev* d, uint64_t offset, void* host, uint64_t bytes) {
+  CHECK_ARG(d && host, "null arg");
+  CHECK_ARG(d->kv, "KV pool not initialised");
+  CHECK_ARG(offset <= d->kv_bytes && bytes <= d->kv_bytes - offset, "range outside the KV pool");
+  CU(cudaSetDevice(d->gpu));
+  CU(cudaStreamSynchronize(d->compute));
+  CU(cudaStreamSynchronize(d->xfer));
+  CU(cudaMemcpy(host, reinterpret_cast<const uint8_t*>(d->kv) + offset, bytes, cudaMemcpyDeviceToHost));
   return PPD_OK;
 }
 
@@ -965,39 +1063,59 @@ int ppd_prefill(ppd_dev* d, int32_t kind, const int32_t* tokens, int32_t n_new, 
   return ppd_step(d, &b, out_token, out_ms);
 }
 
-int ppd_kv_copy(ppd_dev* src, ppd_dev* dst, const int32_t* src_block_table,
-                const int32_t* dst_block_table, int32_t n_blocks, int32_t start, int32_t n_tokens,
-                float* out_ms) {
+int ppd_kv_copy_submit(ppd_dev* src, ppd_dev* dst, const int32_t* src_block_table,
+                       const int32_t* dst_block_table, int32_t n_blocks, int32_t start, int32_t n_tokens,
+                       uint64_t* ticket) {
   // reference: kv_transfer_time requires tokens >= 1 (costmodel.cpp:335)
-  CHECK_ARG(src && dst, "null dev");
+  CHECK_ARG(src && dst && ticket, "null arg");
   CHECK_ARG(n_tokens >= 1, "kv_transfer_time: tokens >= 1");
+  CHECK_ARG(n_blocks >= 1 && src_block_table && dst_block_table, "empty block tables");
   CHECK_ARG(start >= 0 && (long)start + n_tokens <= (long)n_blocks * dst->bt, "token range outside block table");
   CHECK_ARG(src->kv && dst->kv && src->bt == dst->bt, "pools not initialised / block size mismatch");
+  CHECK_ARG(same_cfg(src->cfg, dst->cfg), "source and destination model shapes differ");
   for (int j = start / dst->bt; j <= (start + n_tokens - 1) / dst->bt; ++j) {
     CHECK_ARG(src_block_table[j] >= 0 && src_block_table[j] < src->nblocks, "src block id out of range");
     CHECK_ARG(dst_block_table[j] >= 0 && dst_block_table[j] < dst->nblocks, "dst block id out of range");
   }
+  const uint64_t t = dst->copy_head.load(std::memory_order_relaxed);
+  if (t - dst->copy_done.load(std::memory_order_acquire) >= (uint64_t)kCopySlots)
+    return fail(PPD_ERR_STATE, "too many KV copies in flight into this device (wait for older tickets)");
   CU(cudaSetDevice(dst->gpu));
-  if (src->gpu != dst->gpu) {
+  if (src->gpu != dst->gpu && !(dst->peer_mask & (1ull << src->gpu))) {
+    // the copy kernel runs on the destination and pulls from the source pool over NVLink
     cudaError_t e = cudaDeviceEnablePeerAccess(src->gpu, 0);
     if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
       return fail(PPD_ERR_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
     cudaGetLastError();
+    dst->peer_mask |= 1ull << src->gpu;
   }
-  // block tables travel in a small device buffer of the destination worker
-  int32_t* dbt = nullptr;
-  CU(cudaMallocAsync(&dbt, (size_t)n_blocks * 2 * 4, dst->xfer));
-  CU(cudaMemcpyAsync(dbt, src_block_table, (size_t)n_blocks * 4, cudaMemcpyHostToDevice, dst->xfer));
-  CU(cudaMemcpyAsync(dbt + n_blocks, dst_block_table, (size_t)n_blocks * 4, cudaMemcpyHostToDevice,
-                     dst->xfer));
-  // the producer's KV must be complete: fence after the source compute stream
+  CopySlot& c = dst->copy[t % kCopySlots];
+  if (!c.e0) {
+    CU(cudaEventCreate(&c.e0));
+    CU(cudaEventCreate(&c.e1));
+  }
+  if (c.cap < n_blocks) {  // grows rarely (first hops / longer contexts); never per copy
+    if (c.h_bt) cudaFreeHost(c.h_bt);
+    if (c.d_bt) cudaFree(c.d_bt);
+    c.h_bt = nullptr;
+    c.d_bt = nullptr;
+    c.cap = 0;
+    const int cap = std::max(n_blocks, 1024);
+    CU(cudaMallocHost(&c.h_bt, (size_t)cap * 2 * 4));
+    CU(cudaMalloc(&c.d_bt, (size_t)cap * 2 * 4));
+    c.cap = cap;
+  }
+  std::memcpy(c.h_bt, src_block_table, (size_t)n_blocks * 4);
+  std::memcpy(c.h_bt + n_blocks, dst_block_table, (size_t)n_blocks * 4);
+  // the producer's KV must be complete: fence after the source's last submitted step
   CU(cudaStreamWaitEvent(dst->xfer, src->compute_done, 0));
-  CU(cudaEventRecord(dst->xev0, dst->xfer));
+  CU(cudaEventRecord(c.e0, dst->xfer));
+  CU(cudaMemcpyAsync(c.d_bt, c.h_bt, (size_t)n_blocks * 2 * 4, cudaMemcpyHostToDevice, dst->xfer));
   KvCopyParams p{};
   p.src_pool = src->kv;
   p.dst_pool = dst->kv;
-  p.src_blocks = dbt;
-  p.dst_blocks = dbt + n_blocks;
+  p.src_blocks = c.d_bt;
+  p.dst_blocks = c.d_bt + n_blocks;
   p.start = start;
   p.n_tokens = n_tokens;
   p.n_layers = dst->cfg.n_layers;
@@ -1005,13 +1123,95 @@ int ppd_kv_copy(ppd_dev* src, ppd_dev* dst, const int32_t* src_block_table,
   p.block_tokens = dst->bt;
   p.head_dim = dst->cfg.head_dim;
   CU(launch_kv_copy(p, dst->xfer));
-  CU(cudaEventRecord(dst->xev1, dst->xfer));
-  CU(cudaFreeAsync(dbt, dst->xfer));
-  // the decode node's next step starts after the KV has landed
-  CU(cudaStreamWaitEvent(dst->compute, dst->xev1, 0));
-  CU(cudaEventSynchronize(dst->xev1));
-  if (out_ms) CU(cudaEventElapsedTime(out_ms, dst->xev0, dst->xev1));
+  CU(cudaEventRecord(c.e1, dst->xfer));
+  dst->copy_head.store(t + 1, std::memory_order_release);
+  *ticket = t;
   return PPD_OK;
+}
+
+int ppd_kv_copy_wait(ppd_dev* dst, uint64_t ticket, float* out_ms) {
+  CHECK_ARG(dst, "null dev");
+  const uint64_t done = dst->copy_done.load(std::memory_order_acquire);
+  CHECK_ARG(ticket == done && ticket < dst->copy_head.load(std::memory_order_acquire),
+            "tickets must be waited for once each, in submission order");
+  CU(cudaSetDevice(dst->gpu));
+  CopySlot& c = dst->copy[ticket % kCopySlots];
+  CU(cudaEventSynchronize(c.e1));
+  if (out_ms) CU(cudaEventElapsedTime(out_ms, c.e0, c.e1));
+  dst->copy_done.store(ticket + 1, std::memory_order_release);
+  return PPD_OK;
+}
+
+int ppd_kv_copy(ppd_dev* src, ppd_dev* dst, const int32_t* src_block_table,
+                const int32_t* dst_block_table, int32_t n_blocks, int32_t start, int32_t n_tokens,
+                float* out_ms) {
+  CHECK_ARG(dst, "null dev");
+  // earlier asynchronous hops into dst complete first (tickets retire in order)
+  while (dst->copy_done.load() < dst->copy_head.load()) {
+    int rc = ppd_kv_copy_wait(dst, dst->copy_done.load(), nullptr);
+    if (rc) return rc;
+  }
+  uint64_t t = 0;
+  int rc = ppd_kv_copy_submit(src, dst, src_block_table, dst_block_table, n_blocks, start, n_tokens, &t);
+  if (rc) return rc;
+  return ppd_kv_copy_wait(dst, t, out_ms);
+}
+
+// Peer bandwidth probe (bench.py, N > 1): bytes copied from src_gpu to
+// dst_gpu per second, best of `iters`. mode 0: copy engines
+// (cudaMemcpyPeerAsync); mode 1: an SM pull kernel on dst reading src over
+// NVLink (the K7 access pattern: 16 B loads, streaming stores).
+int ppd_p2p_bandwidth(int32_t src_gpu, int32_t dst_gpu, uint64_t bytes, int32_t iters, int32_t mode,
+                      double* gbs) {
+  CHECK_ARG(gbs && iters >= 1 && bytes >= 16 && bytes % 16 == 0 && (mode == 0 || mode == 1), "bad args");
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  CHECK_ARG(src_gpu >= 0 && src_gpu < ndev && dst_gpu >= 0 && dst_gpu < ndev, "gpu index out of range");
+  void *a = nullptr, *b = nullptr;
+  CU(cudaSetDevice(src_gpu));
+  CU(cudaMalloc(&a, bytes));
+  CU(cudaMemset(a, 1, bytes));
+  CU(cudaDeviceSynchronize());
+  CU(cudaSetDevice(dst_gpu));
+  if (src_gpu != dst_gpu) {
+    cudaError_t e = cudaDeviceEnablePeerAccess(src_gpu, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+      cudaFree(a);
+      return fail(PPD_ERR_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+    }
+    cudaGetLastError();
+  }
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int rc = PPD_OK;
+  double best = 0;
+  if (cudaMalloc(&b, bytes) != cudaSuccess || cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+    rc = fail(PPD_ERR_CUDA, "p2p probe: allocation failed");
+  } else {
+    for (int i = 0; i <= iters && rc == PPD_OK; ++i) {  // iteration 0 warms up
+      cudaEventRecord(e0, st);
+      cudaError_t e = mode == 0 ? cudaMemcpyPeerAsync(b, dst_gpu, a, src_gpu, bytes, st)
+                                : launch_pull_copy(static_cast<const uint4*>(a), static_cast<uint4*>(b), bytes / 16, st);
+      cudaEventRecord(e1, st);
+      if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+      if (e != cudaSuccess) {
+        rc = fail(PPD_ERR_CUDA, std::string("p2p probe: ") + cudaGetErrorString(e));
+        break;
+      }
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (i > 0 && ms > 0) best = std::max(best, (double)bytes / (ms * 1e-3) / 1e9);
+    }
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (st) cudaStreamDestroy(st);
+  if (b) cudaFree(b);
+  cudaSetDevice(src_gpu);
+  cudaFree(a);
+  *gbs = best;
+  return rc;
 }
 
 // ------------------------------------------------------------ test entry points
@@ -1129,9 +1329,6 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "gemm_stages") == 0) {
     CHECK_ARG(value >= 0 && value <= 16, "gemm_stages must be in [0, 16]");
     stages = value;
-  } else if (std::strcmp(name, "diag_skip") == 0) {
-    CHECK_ARG(value >= 0 && value <= 63, "diag_skip must be in [0, 63]");
-    g_diag_skip = value;
   } else if (std::strcmp(name, "attn_pf_ctas") == 0) {
     CHECK_ARG(value >= 0 && value <= 146, "attn_pf_ctas must be in [0, 146]");
     g_attn_pf_ctas = value;

@@ -1,5 +1,6 @@
-// gemm.cu — K5 GEMM dispatch: tcgen05 kernel (gemm_tc.cu) by default, cuBLAS
-// as the library reference the tcgen05 path is parity-tested against.
+// gemm.cu — K5 GEMM entry points of the forward step: the tcgen05 kernel
+// (gemm_tc.cu) is the only product path. cuBLAS appears here solely as the
+// library reference ppd_op_gemm exposes to the parity tests.
 #include <cublas_v2.h>
 
 #include <cstdlib>
@@ -12,8 +13,7 @@
 namespace ppdk {
 
 struct GemmContext {
-  cublasHandle_t handle = nullptr;
-  bool tc = true;
+  cublasHandle_t handle = nullptr;  // ppd_op_gemm (test reference) only
 };
 
 GemmContext* gemm_create() {
@@ -22,8 +22,6 @@ GemmContext* gemm_create() {
     delete c;
     return nullptr;
   }
-  const char* e = std::getenv("PPD_GEMM");
-  c->tc = !(e && std::strcmp(e, "cublas") == 0);
   return c;
 }
 
@@ -32,8 +30,6 @@ void gemm_destroy(GemmContext* c) {
   if (c->handle) cublasDestroy(c->handle);
   delete c;
 }
-
-bool gemm_uses_tcgen05(const GemmContext* c) { return c && c->tc; }
 
 cudaError_t gemm_run_cublas(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N,
                             int K, bool out_f32, cudaStream_t s) {
@@ -47,31 +43,20 @@ cudaError_t gemm_run_cublas(GemmContext* c, const __nv_bfloat16* A, const __nv_b
   return st == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown;
 }
 
-cudaError_t gemm_run(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N, int K,
-                     bool out_f32, cudaStream_t s) {
-  if (!c->tc) return gemm_run_cublas(c, A, B, C, M, N, K, out_f32, s);
+cudaError_t gemm_run(const __nv_bfloat16* A, const __nv_bfloat16* B, void* C, int M, int N, int K, bool out_f32,
+                     cudaStream_t s) {
   return gemm_tc_run(A, B, C, M, N, K, out_f32, 1, 0, s);
 }
 
-cudaError_t gemm_run_split(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, float* C, int M, int N,
-                           int K, int max_slices, GemmParts* parts, cudaStream_t s) {
-  if (!c->tc) {
-    *parts = GemmParts{};
-    parts->stride = (size_t)M * N;
-    return gemm_run_cublas(c, A, B, C, M, N, K, true, s);
-  }
+cudaError_t gemm_run_split(const __nv_bfloat16* A, const __nv_bfloat16* B, float* C, int M, int N, int K,
+                           int max_slices, GemmParts* parts, cudaStream_t s) {
   return gemm_tc_run_parts(A, B, C, M, N, K, max_slices, (size_t)M * N, parts, s);
 }
 
-cudaError_t gemm_run_silu(GemmContext* c, const __nv_bfloat16* A, const __nv_bfloat16* B, __nv_bfloat16* m,
-                          float* scratch, int M, int N, int K, cudaStream_t s) {
+cudaError_t gemm_run_silu(const __nv_bfloat16* A, const __nv_bfloat16* B, __nv_bfloat16* m, int M, int N, int K,
+                          cudaStream_t s) {
   if (M == 0) return cudaSuccess;
-  if (c->tc) return gemm_tc_run_silu(A, B, m, M, N, K, s);
-  cudaError_t e = gemm_run_cublas(c, A, B, scratch, M, N, K, true, s);
-  if (e != cudaSuccess) return e;
-  GemmParts one;
-  one.stride = (size_t)M * N;
-  return launch_silu_mul(scratch, one, m, M, N / 2, s);
+  return gemm_tc_run_silu(A, B, m, M, N, K, s);
 }
 
 }  // namespace ppdk

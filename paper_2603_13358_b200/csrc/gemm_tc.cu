@@ -655,7 +655,7 @@ Shape shape_for(int T, int N, int K, int extra_smem = 0, bool force_single = fal
   sh.unit_t = sh.bn * sh.n_sub;
   const double tiles1 = double((N + kBM - 1) / kBM) * ((T + sh.unit_t - 1) / sh.unit_t);
   const bool auto_pair =
-      T >= kPairMinT && (tiles1 >= kPairMinTilesPerSm * 148 || (sh.n_sub > 1 && K >= kSubPairMinK));
+      T >= kPairMinT && (tiles1 >= kPairMinTilesPerSm * device_sms() || (sh.n_sub > 1 && K >= kSubPairMinK));
   const bool want_occ2 = sh.n_sub == 1 && extra_smem == 0 && (g_occ2 == 1 || (g_occ2 < 0 && T <= kOcc2MaxT));
   sh.pair = !force_single && (g_pair_mode == 1 || (g_pair_mode < 0 && auto_pair && !want_occ2));
   sh.rows = sh.pair ? 2 * kBM : kBM;
@@ -667,7 +667,7 @@ Shape shape_for(int T, int N, int K, int extra_smem = 0, bool force_single = fal
   if (g_stage_cap > 0 && g_stage_cap < stages) stages = g_stage_cap;
   sh.stages = stages;
   sh.smem = 1024 + stages * sh.stage_bytes + kBarBytes + extra_smem;
-  sh.slots = 148 * sh.occ;
+  sh.slots = device_sms() * sh.occ;
   if (sh.pair) {
     sh.slots = max_pair_slots(sh.smem, sh.occ);
     if (sh.slots <= 0) return shape_for(T, N, K, extra_smem, true);  // no co-resident pair fits: single-CTA kernel

@@ -108,6 +108,7 @@ struct KvCopyParams {
   int n_layers, n_kv_heads, block_tokens, head_dim;
 };
 cudaError_t launch_kv_copy(const KvCopyParams& p, cudaStream_t s);
+cudaError_t launch_pull_copy(const uint4* src, uint4* dst, long n16, cudaStream_t s);
 
 }  // namespace ppdk
 

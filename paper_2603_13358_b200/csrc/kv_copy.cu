@@ -54,9 +54,30 @@ cudaError_t launch_kv_copy(const KvCopyParams& p, cudaStream_t s) {
   if (p.n_tokens <= 0) return cudaSuccess;
   const int BT = p.block_tokens;
   long units = (long)((p.start + p.n_tokens - 1) / BT - p.start / BT + 1) * p.n_layers * 2 * p.n_kv_heads;
-  long warps = units < 148L * 64 ? units : 148L * 64;
+  const long cap = (long)device_sms() * 64;
+  long warps = units < cap ? units : cap;
   int blocks = (int)((warps + 7) / 8);
   kv_copy_kernel<<<blocks, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// Peer-bandwidth probe: a flat pull of n16 16-byte words (src may be a peer
+// pointer), the same access pattern as kv_copy_kernel's runs.
+__global__ void pull_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, long n16) {
+  const long stride = (long)gridDim.x * blockDim.x;
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 7 * stride < n16; i += 8 * stride) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcs(src + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) __stcs(dst + i + k * stride, v[k]);
+  }
+  for (; i < n16; i += stride) __stcs(dst + i, __ldcs(src + i));
+}
+
+cudaError_t launch_pull_copy(const uint4* src, uint4* dst, long n16, cudaStream_t s) {
+  pull_copy_kernel<<<device_sms() * 8, 256, 0, s>>>(src, dst, n16);
   return cudaGetLastError();
 }
 

@@ -41,7 +41,7 @@ __global__ void fill_random_kernel(bf16* dst, uint64_t n, uint64_t seed, int ten
 }
 cudaError_t launch_fill_random(bf16* dst, uint64_t n, uint64_t seed, int tensor, int layer,
                                cudaStream_t s) {
-  fill_random_kernel<<<148 * 8, 256, 0, s>>>(dst, n, seed, tensor, layer);
+  fill_random_kernel<<<device_sms() * 8, 256, 0, s>>>(dst, n, seed, tensor, layer);
   return cudaGetLastError();
 }
 
@@ -53,7 +53,7 @@ __global__ void fill_matrix_kernel(bf16* dst, uint64_t n, uint64_t seed, int ten
 }
 cudaError_t launch_fill_matrix(bf16* dst, uint64_t N, uint64_t K, uint64_t seed, int tensor, int layer,
                                cudaStream_t s) {
-  fill_matrix_kernel<<<148 * 8, 256, 0, s>>>(dst, N * K, seed, tensor, layer);
+  fill_matrix_kernel<<<device_sms() * 8, 256, 0, s>>>(dst, N * K, seed, tensor, layer);
   return cudaGetLastError();
 }
 
@@ -71,7 +71,7 @@ __global__ void fill_qkv_kernel(bf16* dst, int qd, int kd, int d, uint64_t seed,
   }
 }
 cudaError_t launch_fill_qkv(bf16* dst, int qd, int kd, int d, uint64_t seed, int layer, cudaStream_t s) {
-  fill_qkv_kernel<<<148 * 8, 256, 0, s>>>(dst, qd, kd, d, seed, layer);
+  fill_qkv_kernel<<<device_sms() * 8, 256, 0, s>>>(dst, qd, kd, d, seed, layer);
   return cudaGetLastError();
 }
 
@@ -102,7 +102,7 @@ __global__ void fill_gate_up_kernel(bf16* dst, int F, int d, uint64_t seed, int 
   }
 }
 cudaError_t launch_fill_gate_up(bf16* dst, int F, int d, uint64_t seed, int layer, cudaStream_t s) {
-  fill_gate_up_kernel<<<148 * 8, 256, 0, s>>>(dst, F, d, seed, layer);
+  fill_gate_up_kernel<<<device_sms() * 8, 256, 0, s>>>(dst, F, d, seed, layer);
   return cudaGetLastError();
 }
 
@@ -112,7 +112,7 @@ __global__ void fill_const_kernel(bf16* dst, uint64_t n, float v) {
     dst[i] = f2bf(v);
 }
 cudaError_t launch_fill_const(bf16* dst, uint64_t n, float v, cudaStream_t s) {
-  fill_const_kernel<<<148, 256, 0, s>>>(dst, n, v);
+  fill_const_kernel<<<device_sms(), 256, 0, s>>>(dst, n, v);
   return cudaGetLastError();
 }
 
@@ -396,7 +396,7 @@ __global__ void f32_to_bf16_kernel(const float* in, bf16* out, uint64_t n) {
     out[i] = f2bf(in[i]);
 }
 cudaError_t launch_f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStream_t s) {
-  f32_to_bf16_kernel<<<148 * 4, 256, 0, s>>>(in, out, n);
+  f32_to_bf16_kernel<<<device_sms() * 4, 256, 0, s>>>(in, out, n);
   return cudaGetLastError();
 }
 
