@@ -93,42 +93,51 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU port
-def cpu_port_decode(batch: int, ctx: int, layers_full: int, n_rep: int = 1):
-    """Times the CPU port (oracle/model_oracle.c, all host threads) of one
-    Llama-3-8B-shape decode step: measures a 1-layer and a 2-layer model
-    step of `batch` rows at context `ctx` and extrapolates
-    t = t_head + layers_full * t_layer. Returns (tok/s, sample, seconds)."""
-    from oracle import oracle as O
-    t_sum = 0.0
-    times = {}
-    cfg = O.MoCfg(2, 4096, 32, 8, 128, 14336, 128256, 1e-5, 5e5, 0)
-    m = O.Model(cfg, SEED)
-    nbps = (ctx + 1 + 15) // 16
-    pool = O.KvPool(cfg, batch * nbps)
-    rng = np.random.default_rng(1)
-    pool.data[...] = O.f32_to_bf16((rng.standard_normal(pool.data.shape, dtype=np.float32) * 0.5))
-    bts = np.arange(batch * nbps, dtype=np.int32).reshape(batch, nbps)
-    toks = rng.integers(0, cfg.vocab, batch).astype(np.int32)
-    for nl in (1, 2):
-        m.set_active_layers(nl)
-        best = None
-        for _ in range(n_rep):
+class CpuPortStep:
+    """The CPU port (oracle/model_oracle.c, all host threads) of one
+    Llama-3-8B-shape decode step of `batch` rows at context `ctx`. One sample
+    times a 1-layer and a 2-layer step (bounded: ~1-2 s) and extrapolates
+    t = t_head + layers_full * t_layer (t_layer = t2 - t1)."""
+
+    def __init__(self, batch: int, ctx: int, layers_full: int = 32):
+        from oracle import oracle as O
+        self.O, self.batch, self.ctx, self.layers_full = O, batch, ctx, layers_full
+        cfg = O.MoCfg(2, 4096, 32, 8, 128, 14336, 128256, 1e-5, 5e5, 0)
+        self.cfg = cfg
+        self.m = O.Model(cfg, SEED)
+        nbps = (ctx + 1 + 15) // 16
+        self.pool = O.KvPool(cfg, batch * nbps)
+        rng = np.random.default_rng(1)
+        self.pool.data[...] = O.f32_to_bf16((rng.standard_normal(self.pool.data.shape, dtype=np.float32) * 0.5))
+        self.bts = np.arange(batch * nbps, dtype=np.int32).reshape(batch, nbps)
+        self.toks = rng.integers(0, cfg.vocab, batch).astype(np.int32)
+
+    def sample(self):
+        times = {}
+        for nl in (1, 2):
+            self.m.set_active_layers(nl)
             t0 = time.perf_counter()
-            m.step(pool, [1] * batch, [ctx] * batch, toks, bts, want_logits=False)
-            dt = time.perf_counter() - t0
-            best = dt if best is None else min(best, dt)
-            t_sum += dt
-        times[nl] = best
-    del m
-    t_layer = max(times[2] - times[1], 1e-9)
-    t_head = max(times[1] - t_layer, 0.0)
-    t_full = t_head + layers_full * t_layer
-    sample = (f"{batch} decode rows at ctx {ctx}, 1- and 2-layer Llama-3-8B-shape steps timed, "
-              f"extrapolated to {layers_full} layers (t_layer={t_layer*1e3:.1f} ms, t_head={t_head*1e3:.1f} ms)")
-    return batch / t_full, sample, t_sum
+            self.m.step(self.pool, [1] * self.batch, [self.ctx] * self.batch, self.toks, self.bts, want_logits=False)
+            times[nl] = time.perf_counter() - t0
+        t_layer = max(times[2] - times[1], 1e-9)
+        t_head = max(times[1] - t_layer, 0.0)
+        t_full = t_head + self.layers_full * t_layer
+        desc = (f"{self.batch} decode rows at ctx {self.ctx}: a 1- and a 2-layer Llama-3-8B-shape step timed, "
+                f"extrapolated to {self.layers_full} layers (t_layer={t_layer*1e3:.1f} ms, t_head={t_head*1e3:.1f} ms)")
+        return self.batch / t_full, desc, times[1] + times[2]
 
 
-def engine_ttft(gpus, layout: str, quick: bool = False, qps: float = None):
+def cpu_port_decode(batch: int, ctx: int, layers_full: int, n_rep: int = 1):
+    port = CpuPortStep(batch, ctx, layers_full)
+    best, desc, secs = None, "", 0.0
+    for _ in range(n_rep):
+        tps, desc, t = port.sample()
+        best = tps if best is None else max(best, tps)
+        secs += t
+    return best, desc, secs
+
+
+def engine_ttft(gpus, layout: str, quick: bool = False, qps: float = None, clock: str = "device"):
     """Turn-2+ TTFT / TPOT, PD (x=0) vs PPD (x=1), through the host C++ engine
     on the DEVICE clock: every prefill chunk, decode iteration and P->D KV hop
     runs on the GPUs listed (node i -> gpus[i]); each node's clock advances by
@@ -138,17 +147,17 @@ def engine_ttft(gpus, layout: str, quick: bool = False, qps: float = None):
     from paper_2603_13358_b200 import engine as E
     if layout in ("1P_1D", "1R"):
         # BASELINE configs[2]: 4 turns, +2048 tokens of context per turn (1536 in, 512 out)
-        wl = {"id": "cfg3", "turn1": [1536, 512], "turn2plus": [1536, 512], "num_turns": 4,
-              "qps": qps or 1.0, "duration_s": 4.0 if quick else 12.0}
+        wl = cfg2_workload(qps or 1.0, quick)
     else:
         wl = {"id": "cfg4", "turn1": [2048, 128], "turn2plus": [1024, 128], "num_turns": 3,
               "qps": 8.0, "duration_s": 4.0 if quick else 8.0}
     distinct = len(set(gpus)) == len(gpus)
-    out = {"cluster": layout, "workload": wl, "model": "llama-3-8b-shape", "gpus": gpus,
+    out = {"cluster": layout, "workload": wl, "model": "llama-3-8b-shape", "gpus": gpus, "clock": clock,
            "placement": ("one node per GPU" if distinct else "nodes share GPU %s" % sorted(set(gpus)))
-           + "; device clock = per-node CUDA-event durations"}
+           + ("; device clock = per-node CUDA-event durations" if clock == "device" else
+              "; realtime = wall clock, one worker thread per node, asynchronous NVLink KV hops")}
     for x in (0.0, 1.0):
-        job = {"cluster": layout, "x": x, "clock": "device", "seed": 3, "workload": wl,
+        job = {"cluster": layout, "x": x, "clock": clock, "seed": 3, "workload": wl,
                "device": {"model": "llama8b", "weight_seed": SEED, "token_seed": 3, "gpus": gpus,
                           "kv_blocks_per_node": 0, "prefill_chunk": 2048, "record_tokens": False}}
         t0 = time.perf_counter()
@@ -160,7 +169,10 @@ def engine_ttft(gpus, layout: str, quick: bool = False, qps: float = None):
                              "tpot_p50_ms": ms(agg["tpot_p50"]), "success_rate": agg["success_rate"],
                              "decode_tok_s": agg["tps"],
                              "link_transfers": r["link_transfers"], "link_gb": r["link_bytes"] / 1e9,
+                             "link_bytes": r["link_bytes"],
                              "kv_transfer_gbs": r["device"]["kv_transfer"]["gbs"],
+                             "kv_hop_ms_p50": r["device"]["kv_transfer"]["hop_ms_p50"],
+                             "kv_blocks_in_use_at_end": r["device"]["kv_lifecycle"]["blocks_in_use_at_end"],
                              "wall_s": time.perf_counter() - t0}
     p0, p1 = out["x0"]["ttft_t2_p50_ms"], out["x1"]["ttft_t2_p50_ms"]
     if p0 and p1:
@@ -212,6 +224,125 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cfg2_workload(qps: float, quick: bool = False) -> dict:
+    """BASELINE configs[2]: 4 turns of 1536 in / 512 out (+2048 context per turn)."""
+    return {"id": "cfg3", "turn1": [1536, 512], "turn2plus": [1536, 512], "num_turns": 4,
+            "qps": qps, "duration_s": 4.0 if quick else 12.0}
+
+
+def reference_des(cluster: str, wl: dict, seed: int, calib: dict) -> dict:
+    """The UNMODIFIED reference (oracle/_ref/ref_tool = /root/reference/proj/src
+    built by oracle/Makefile) simulating the identical trace: its simulated
+    turn-2+ TTFT / TPOT, link bytes and the DES wall time on this host."""
+    from oracle import oracle as O
+    out = {}
+    for x in (0.0, 1.0):
+        r = O.ref_tool({"op": "simulate", "cluster": cluster, "x": x, "workload": wl, "seed": seed, **calib})
+        a = r["aggregate"]
+        ms = lambda v: None if v is None else v * 1e3
+        # the reference aggregates mean / p99 only; p50 by its own nearest-rank rule (metrics.cpp:43-60)
+        recs = [json.loads(l) for l in r["records_jsonl"].splitlines()[1:]]
+        t2 = sorted(v["first_token"] - v["arrival"] for v in recs
+                    if v["turn_index"] >= 2 and v.get("first_token") is not None and v["status"] == "completed")
+        p50 = t2[max(0, int(np.ceil(0.5 * len(t2))) - 1)] if t2 else None
+        out[f"x{int(x)}"] = {"ttft_t2_p50_ms": ms(p50), "ttft_t2_p99_ms": ms(a.get("ttft_t2_p99")),
+                             "tpot_mean_ms": ms(a.get("tpot_mean")), "decode_tok_s": a.get("tps"),
+                             "link_transfers": r["link_transfers"], "link_bytes": r["link_bytes"],
+                             "des_wall_s": r["wall_s"], "calib_hash": r["calib_hash"]}
+    p0, p1 = out["x0"]["ttft_t2_p50_ms"], out["x1"]["ttft_t2_p50_ms"]
+    if p0 and p1:
+        out["ttft_t2_p50_reduction"] = 1.0 - p1 / p0
+    return out
+
+
+def device_calibration(dev, cfg, inter: dict, B: int, ctx, tok, bts, cal_bt, link_gbs: float) -> dict:
+    """CalibrationTable coefficients fitted from B200 measurements of this run
+    (ppd::cost::fit_from_measurements through the engine's fit_calibration op):
+    decode steps at 4 batch sizes, full prefills at 3 lengths, appends of 1536
+    tokens at 3 cached lengths, the interference sweep's multipliers and the
+    measured KV-hop bandwidth (reference schema: costmodel.cpp:197-316)."""
+    from paper_2603_13358_b200 import engine as E
+    rng = np.random.default_rng(SEED + 7)
+    med = lambda f, n=3: float(np.median([f() for _ in range(n)]))
+    samples = {"decode": [], "full": [], "append": [], "interference": [],
+               "kv_bytes_per_token": 131072.0, "link_bandwidth": link_gbs * 1e9}
+    for b in (8, 50, 100, B):
+        t = med(lambda: dev.step([1] * b, ctx[:b], tok[:b], bts[:b]).ms)
+        samples["decode"].append([b, t * 1e-3])
+    for n in (1024, 2048, 4096):
+        toks = rng.integers(0, cfg.vocab, n).astype(np.int32)
+        t = med(lambda: dev.step([n], [0], toks, cal_bt).ms, 2)
+        samples["full"].append([n, t * 1e-3])
+    for n in (2048, 4096, 6144):
+        toks = rng.integers(0, cfg.vocab, 1536).astype(np.int32)
+        t = med(lambda: dev.step([1536], [n], toks, cal_bt).ms, 2)
+        samples["append"].append([1536, n, t * 1e-3])
+    for conc in (1, 4):
+        c = inter[f"conc{conc}"]
+        samples["interference"].append({"kind": "full", "prefill_tokens": 1024, "concurrent_prefills": conc,
+                                        "decode_batch": B, "tpot_multiplier": c["mult_full"]})
+        samples["interference"].append({"kind": "append", "prefill_tokens": 1024, "concurrent_prefills": conc,
+                                        "decode_batch": B, "tpot_multiplier": c["mult_append"]})
+    fit = E.run({"op": "fit_calibration", "samples": samples})
+    return {"samples": samples, "calib_json": fit["calib_json"], "hash": fit["hash"]}
+
+
+def nvlink_probe(world: int) -> dict:
+    """NVLink roofline (N > 1): GPU0 -> GPU1 copy bandwidth, best of 5 x 1 GiB,
+    through the copy engines and through an SM pull kernel; then the K7 KV-hop
+    kernel (ppd_kv_copy) between two Llama-3-8B-shape pools on GPU 0 and GPU 1
+    at 1536 and 8192 tokens, as a fraction of the best measured peak."""
+    import paper_2603_13358_b200 as ppd
+    out = {"pair": [0, 1]}
+    out["ce_gbs"] = ppd.p2p_bandwidth(0, 1, 1 << 30, 5, 0)
+    out["sm_pull_gbs"] = ppd.p2p_bandwidth(0, 1, 1 << 30, 5, 1)
+    out["hbm_copy_gbs_same_gpu"] = ppd.p2p_bandwidth(0, 0, 1 << 30, 5, 1)
+    peak = max(out["ce_gbs"], out["sm_pull_gbs"])
+    out["peak_gbs"] = peak
+    out["peak_kind"] = "measured (best of copy-engine / SM-pull probe)"
+    out["nominal_gbs"] = 900.0
+    cfg = ppd.llama8b_cfg()
+    devs = [ppd.Device(g, cfg, max_step_tokens=256, max_step_seqs=8) for g in (0, 1)]
+    try:
+        for d in devs:
+            d.kv_pool_init(1024)
+        kvb = ppd.kv_block_bytes(cfg) / 16
+        for n in (1536, 8192):
+            nb = (n + 15) // 16
+            src = np.arange(nb, dtype=np.int32)
+            dst = np.arange(512 - nb // 2, 512 - nb // 2 + nb, dtype=np.int32) % 1024
+            ms = min(ppd.kv_copy(devs[0], devs[1], src, dst, 0, n) for _ in range(5))
+            gbs = n * kvb / (ms * 1e-3) / 1e9
+            out[f"k7_{n}_tokens"] = {"ms": ms, "gbs": gbs, "frac_of_peak": gbs / peak if peak else None,
+                                     "frac_of_nominal": gbs / 900.0}
+    finally:
+        for d in devs:
+            d.close()
+    return out
+
+
+def bench_config(B: int, ctx0: int, world: int) -> dict:
+    return {
+        "workload": f"Llama-3-8B-shape decode step, B={B} requests at ctx {ctx0}+, 1 colocated node per GPU "
+                    "(BASELINE configs[1]); interference sweep beside it",
+        "model": "llama-3-8b-shape (random init)",
+        "global_batch": B * world,
+        "seq_len": ctx0,
+        "parallelism": "replicas (one node per GPU, no collective in the decode step)",
+        "l2_policy": f"inputs larger than L2: {B * ctx0 * 131072 / 1e9:.1f} GB KV + 16.06 GB weights read per step",
+    }
+
+
 # ----------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -225,9 +356,10 @@ def run_ours(args, rank, world, local_rank):
     max_ctx = ctx0 + W + K + 16
     bps = (max_ctx + BT - 1) // BT
     n_inter_blocks = 4 * 64 + 4 * 64 + 8
+    n_cal_blocks = (6144 + 1536) // 16 + 8  # calibration prefills / appends
     dev = ppd.Device(local_rank, cfg, max_step_tokens=max(4096, B + 4 * 1024), max_step_seqs=max(B + 8, 256))
     dev.load_random_weights(SEED)
-    dev.kv_pool_init(B * bps + n_inter_blocks)
+    dev.kv_pool_init(B * bps + n_inter_blocks + n_cal_blocks)
     bts = np.arange(B * bps, dtype=np.int32).reshape(B, bps)
     rng = np.random.default_rng(SEED + rank)
 
@@ -329,11 +461,6 @@ def run_ours(args, rank, world, local_rank):
     inter["reference_anchor_mult"] = {"full_1024_b200": 1.48, "append_1024_b200": 1.02,
                                       "full_1024_conc4": 1.57, "append_1024_conc4": 1.21}
 
-    dev.close()
-    if rank != 0:
-        if world > 1:
-            torch.distributed.barrier()  # rank 0 drives all GPUs for the engine runs
-        return
     def guarded(fn, *a, **k):
         # a failing side measurement is reported in the line, never kills it
         try:
@@ -341,9 +468,20 @@ def run_ours(args, rank, world, local_rank):
         except Exception as e:  # noqa: BLE001
             return {"error": f"{type(e).__name__}: {e}"}
 
+    cal = None
+    if rank == 0 and not args.quick:
+        cal_bt = np.arange(B * bps + n_inter_blocks, B * bps + n_inter_blocks + n_cal_blocks, dtype=np.int32)
+        cal = guarded(device_calibration, dev, cfg, inter, B, ctx, tok, bts, cal_bt, 0.0)
+    dev.close()
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()  # rank 0 drives all GPUs for the engine runs
+        return
+
     qwen = None
     if not args.no_qwen and not args.quick:
         qwen = guarded(qwen_long_decode, local_rank)
+    nvlink = guarded(nvlink_probe, world) if world > 1 else None
     ttft = None
     if not args.no_engine:
         from paper_2603_13358_b200 import dist as D
@@ -352,8 +490,43 @@ def run_ours(args, rank, world, local_rank):
             ttft = [guarded(engine_ttft, [local_rank, local_rank], "1P_1D", quick=args.quick, qps=q)
                     for q in ((1.0,) if args.quick else (1.0, 2.0))]
         else:
-            ttft = [guarded(engine_ttft, D.layout_gpus(lay, world), lay, quick=args.quick)
+            # one node per GPU, wall clock: steps of different nodes run concurrently and
+            # every KV hop overlaps its destination's decode steps
+            ttft = [guarded(engine_ttft, D.layout_gpus(lay, world), lay, quick=args.quick, clock="realtime")
                     for lay in D.node_layouts(world)]
+            if isinstance(nvlink, dict) and nvlink.get("peak_gbs"):
+                for t in ttft:
+                    for x in ("x0", "x1"):
+                        if isinstance(t, dict) and x in t and t[x].get("kv_transfer_gbs"):
+                            t[x]["kv_transfer_frac_of_nvlink_peak"] = t[x]["kv_transfer_gbs"] / nvlink["peak_gbs"]
+    # the reference DES on the identical traces, default and device-fitted calibration
+    des = None
+    if not args.no_cpu and ttft:
+        des = []
+        link_gbs = 0.0
+        for t in ttft:
+            if isinstance(t, dict) and "x0" in t and t["x0"].get("kv_transfer_gbs"):
+                link_gbs = max(link_gbs, t["x0"]["kv_transfer_gbs"])
+        if isinstance(cal, dict) and "samples" in cal and link_gbs > 0:
+            from paper_2603_13358_b200 import engine as E
+            cal["samples"]["link_bandwidth"] = link_gbs * 1e9
+            fit = guarded(E.run, {"op": "fit_calibration", "samples": cal["samples"]})
+            if isinstance(fit, dict) and "calib_json" in fit:
+                cal["calib_json"], cal["hash"] = fit["calib_json"], fit["hash"]
+        for t in ttft:
+            if not (isinstance(t, dict) and "workload" in t):
+                continue
+            row = {"cluster": t["cluster"], "qps": t["workload"]["qps"],
+                   "default_calibration_llama8b_kv": guarded(reference_des, t["cluster"], t["workload"], 3,
+                                                             {"calib_overrides": {"kv_bytes_per_token": 131072}})}
+            if isinstance(cal, dict) and "calib_json" in cal:
+                row["device_fitted_calibration"] = guarded(reference_des, t["cluster"], t["workload"], 3,
+                                                           {"calib_json": cal["calib_json"]})
+            d0 = row["default_calibration_llama8b_kv"]
+            if isinstance(d0, dict) and "x0" in d0:
+                row["link_bytes_equal_device_run"] = all(
+                    d0[x]["link_bytes"] == t[x]["link_bytes"] for x in ("x0", "x1") if x in t)
+            des.append(row)
 
     pk, pk_kind = peaks()
     traffic = None  # dram read+write per launch of the same kernel/config, from the committed ncu capture
@@ -376,7 +549,8 @@ def run_ours(args, rank, world, local_rank):
         nthr = cpu_threads()
         tps, sample, secs = cpu_port_decode(args.cpu_batch, ctx0, cfg.n_layers)
         cpu = {"value": tps, "unit": "tok/s", "cores": nthr, "kind": "port", "sample": sample,
-               "wall_s": secs}
+               "wall_s": secs, "host_cpu_model": cpu_model(), "host_nproc": os.cpu_count(),
+               "reference_des": des}
 
     line = {
         "metric": METRIC,
@@ -391,18 +565,12 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic token ids, random-init bf16 weights (counter hash, std 0.02)",
-        "config": {
-            "workload": f"Llama-3-8B-shape decode step, B={B} requests at ctx {ctx0}+, 1 colocated node per GPU "
-                        "(BASELINE configs[1]); interference sweep beside it",
-            "model": "llama-3-8b-shape (random init)",
-            "global_batch": B * world,
-            "seq_len": ctx0,
-            "parallelism": "replicas (one node per GPU, no collective in the decode step)",
-            "l2_policy": f"inputs larger than L2: {step_bytes_kv/1e9:.1f} GB KV + 16.06 GB weights read per step",
-        },
+        "config": bench_config(B, ctx0, world),
         "tpot_ms": dev_ms_max / K,
         "interference": inter,
         "ttft_pd_vs_ppd": ttft,
+        "nvlink": nvlink,
+        "device_calibration": ({k: v for k, v in cal.items() if k != "calib_json"} if isinstance(cal, dict) else cal),
         "qwen32b_long_decode": qwen,
         "roofline": {
             "kernel": "decode_attention_kernel (K1, balanced persistent paged decode attention)",
@@ -436,19 +604,28 @@ def run_ours(args, rank, world, local_rank):
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the reference prices this step analytically
+    (costmodel.cpp:372-379) and computes no tokens, so its CPU implementation
+    of the step is the oracle port (kind "port"), on all host threads, W + K
+    bounded samples (each ~1-2 s). The unmodified reference DES is run beside
+    it on the configs[2] trace (kind "reference")."""
     if rank != 0:
         return
     nthr = cpu_threads()
-    vals = []
-    t_all = 0.0
-    sample = ""
+    port = CpuPortStep(args.cpu_batch, args.ctx, 32)
     for _ in range(args.warmup):
-        cpu_port_decode(args.cpu_batch, args.ctx, 32)
+        port.sample()
+    vals, sample, t_all = [], "", 0.0
     for _ in range(args.steps):
-        tps, sample, secs = cpu_port_decode(args.cpu_batch, args.ctx, 32)
+        tps, sample, secs = port.sample()
         vals.append(tps)
         t_all += secs
     v = float(np.median(vals))
+    des = None
+    try:
+        des = reference_des("1P_1D", cfg2_workload(1.0), 3, {"calib_overrides": {"kv_bytes_per_token": 131072}})
+    except Exception as e:  # noqa: BLE001
+        des = {"error": f"{type(e).__name__}: {e}"}
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -457,13 +634,18 @@ def run_reference(args, rank, world):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
+        "ms_per_step": float(np.median([args.cpu_batch / x for x in vals])) * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32 (bf16 storage)",
-        "data": "synthetic",
-        "config": {"workload": f"Llama-3-8B-shape decode step at ctx {args.ctx} (CPU port, bounded sample)"},
-        "cpu_baseline": {"value": v, "unit": "tok/s", "cores": nthr, "kind": "port", "sample": sample},
+        "data": "synthetic token ids, random-init bf16 weights (counter hash, std 0.02)",
+        "config": bench_config(args.batch, args.ctx, world),
+        "cpu_baseline": {"value": v, "unit": "tok/s", "cores": nthr, "kind": "port", "sample": sample,
+                         "host_cpu_model": cpu_model(), "samples_s": t_all},
+        "reference_des": {"kind": "reference", "what": "unmodified reference DES (oracle/_ref/ref_tool) on the "
+                          "configs[2] trace, 1P_1D, seed 3, QPS 1, default calibration with Llama-3-8B KV bytes",
+                          "result": des},
         "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference (/root/reference/proj) prices this step analytically "
                 "(costmodel.cpp:372-379) and computes no tokens; its CPU arm is the oracle port",
@@ -491,8 +673,6 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        args.warmup = min(args.warmup, 1)
-        args.steps = min(args.steps, 3)
         run_reference(args, rank, world)
         return
     if world > 1:

@@ -41,6 +41,7 @@ struct DeviceOptions {
   int max_step_tokens = 0;       // 0: prefill_chunk + max_decode_batch + 64
   bool record_steps = false;     // emit the step log (oracle replay)
   bool record_tokens = true;     // emit generated token ids per request
+  bool realtime = false;         // wall-clock run: a worker thread per node, asynchronous KV hops
   static DeviceOptions from_json(const std::string& text);
 };
 

@@ -37,6 +37,8 @@ class BlockPool {
   // Sets covered tokens (allocating as needed); reference prefix_cache[conv] = tokens
   const BlockTable& set_tokens(int conv, long tokens);
   const BlockTable* find(int conv) const;
+  // blocks `ensure(conv, tokens)` would have to take from the pool
+  int blocks_needed(int conv, long tokens) const;
   long tokens(int conv) const;
   void release(int conv);  // returns all blocks of conv to the pool
   const std::map<int, BlockTable>& tables() const { return tables_; }

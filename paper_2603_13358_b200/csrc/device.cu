@@ -119,7 +119,7 @@ struct ppd_dev {
   int max_T = 0, max_S = 0;
   size_t ws_rows = 0;  // token rows of fp32 GEMM-output workspace (holds K-partial slices)
   cudaStream_t compute = nullptr, xfer = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, xev0 = nullptr, xev1 = nullptr, compute_done = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, compute_done = nullptr;
   // weights (possibly shared with other nodes on this GPU)
   SharedWeights* wshared = nullptr;
   bf16 *embed = nullptr, *lm_head = nullptr, *ones = nullptr;
@@ -725,7 +725,7 @@ void free_all(ppd_dev* d) {
     if (p) cudaFree(p);
   if (d->h_meta) cudaFreeHost(d->h_meta);
   if (d->h_tokens_out) cudaFreeHost(d->h_tokens_out);
-  cudaEvent_t evs[] = {d->ev0, d->ev1, d->xev0, d->xev1, d->compute_done};
+  cudaEvent_t evs[] = {d->ev0, d->ev1, d->compute_done};
   for (auto e : evs)
     if (e) cudaEventDestroy(e);
   for (auto e : d->ev_pool) cudaEventDestroy(e);
@@ -782,7 +782,6 @@ int ppd_dev_open(int32_t gpu, const ppd_model_cfg* cfg, int32_t max_step_tokens,
   if (cudaStreamCreateWithFlags(&d->compute, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&d->xfer, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&d->ev0) != cudaSuccess || cudaEventCreate(&d->ev1) != cudaSuccess ||
-      cudaEventCreate(&d->xev0) != cudaSuccess || cudaEventCreate(&d->xev1) != cudaSuccess ||
       cudaEventCreateWithFlags(&d->compute_done, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(PPD_ERR_CUDA, "stream/event creation failed"));
   rc = alloc_workspaces(d);

@@ -419,15 +419,25 @@ std::string op_gateway_tcp(const json& job) {
     std::this_thread::sleep_for(std::chrono::duration<double>(job.value("hold_s", 0.0)));
     long beats = 0;
     for (const auto& w : workers) beats += w->heartbeats();
+    json failed = json::array();
+    if (job.value("stop_server_first", false)) {
+      // the gateway goes away under live agents: their heartbeat threads must
+      // stop cleanly (recorded failure), never terminate the process
+      stop.store(true);
+      srv.join();
+      std::this_thread::sleep_for(std::chrono::duration<double>(job.value("after_stop_s", 0.0)));
+      for (const auto& w : workers) failed.push_back({{"failed", w->failed()}, {"error", w->error()}});
+    }
     workers.clear();
-    out = {{"port", port.load()}, {"worker_ids", ids}, {"replies", replies}, {"heartbeats", beats}};
+    out = {{"port", port.load()}, {"worker_ids", ids}, {"replies", replies}, {"heartbeats", beats},
+           {"after_stop", failed}};
   } catch (...) {
     stop.store(true);
-    srv.join();
+    if (srv.joinable()) srv.join();
     throw;
   }
   stop.store(true);
-  srv.join();
+  if (srv.joinable()) srv.join();
   return out.dump();
 }
 
@@ -454,8 +464,10 @@ std::string run(const std::string& text) {
   const std::uint64_t seed = job.value("seed", std::uint64_t{1});
   const double think = job.value("think_time_s", 0.0);
   const auto t0 = std::chrono::steady_clock::now();
-  if (job.value("clock", std::string("virtual")) == "device") {
+  const std::string clock = job.value("clock", std::string("virtual"));
+  if (clock == "device" || clock == "realtime") {
     engine::DeviceOptions opt = engine::DeviceOptions::from_json(job.value("device", json::object()).dump());
+    opt.realtime = clock == "realtime";
     engine::DeviceRun dr = engine::run_on_device(cfg, convs, qps_replay, seed, think, opt);
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     json out = result_json(dr.sim, job, calib->hash(), wall);

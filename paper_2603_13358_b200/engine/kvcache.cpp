@@ -40,6 +40,13 @@ const BlockTable* BlockPool::find(int conv) const {
   return it == tables_.end() ? nullptr : &it->second;
 }
 
+int BlockPool::blocks_needed(int conv, long tokens) const {
+  const long need = (tokens + block_tokens_ - 1) / block_tokens_;
+  const BlockTable* t = find(conv);
+  const long have = t ? static_cast<long>(t->blocks.size()) : 0;
+  return need > have ? static_cast<int>(need - have) : 0;
+}
+
 long BlockPool::tokens(int conv) const {
   const BlockTable* t = find(conv);
   return t ? t->tokens : 0;

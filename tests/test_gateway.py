@@ -307,3 +307,14 @@ def test_gateway_threadsanitizer(tmp_path):
     assert r.returncode == 0, (r.stdout, r.stderr[-2000:])
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["bad"] == 0 and out["queries"] == 2400 and out["backends"] == 6
+
+
+def test_worker_heartbeats_survive_gateway_shutdown():
+    """the gateway stops under live GPU-worker agents; their
+    heartbeat threads record the closed connection and stop (no
+    std::terminate from an exception escaping the thread)."""
+    workers = [{"role": "D", "gpu": g, "address": f"gpu{g}"} for g in (0, 1)]
+    out = E.run({"op": "gateway_tcp", "x": 1.0, "workers": workers, "messages": ['{"kind":"stats"}'],
+                 "heartbeat_s": 0.01, "hold_s": 0.05, "stop_server_first": True, "after_stop_s": 0.2})
+    assert len(out["after_stop"]) == 2
+    assert all(w["failed"] and "closed" in w["error"] for w in out["after_stop"])

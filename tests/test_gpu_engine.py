@@ -169,3 +169,91 @@ def test_device_eight_node_layouts(gpu, cluster, x):
     assert all(x_["output_tokens_emitted"] == 6 for x_ in recs)
     ref = E.run(dict(job, clock="virtual"))
     assert len(E.records(ref)) == len(recs)
+
+
+def rt_job(cluster, x, **kw):
+    j = dev_job(cluster, x, **kw)
+    j["clock"] = "realtime"
+    return j
+
+
+@pytest.mark.parametrize("x", [0.0, 0.5, 1.0])
+def test_kv_pool_lifecycle_small_pool(gpu, x):
+    """Conversation tables are released at their last turn, admission control
+    waits for room instead of aborting ("KV pool exhausted" in round 1): a
+    pool of 14 blocks per node (two conversations' worth) serves 6
+    conversations, every request completes, the coverage invariant holds at
+    every turn completion and the pools are empty after the trace."""
+    job = dev_job("1P_1D", x, n=6)
+    for i, c in enumerate(job["conversations"]):  # all six in flight together
+        c["arrival"] = 1e-4 * i
+    job["device"]["kv_blocks_per_node"] = 14
+    r = E.run(job)
+    recs = E.records(r)
+    assert len(recs) == 18 and all(v["status"] == "completed" for v in recs)
+    life = r["device"]["kv_lifecycle"]
+    assert life["blocks_in_use_at_end"] == 0 and life["coverage_errors"] == 0
+    assert life["released_tables"] >= 6
+    assert all(n["kv_blocks_peak"] <= 14 for n in r["device"]["nodes"])
+    assert sum(n["admission_waits"] + n["stalled_rows"] for n in r["device"]["nodes"]) > 0
+
+
+def test_flush_and_hop_race_keeps_coverage(gpu):
+    """a turn's completion flush (KV-only row of its last token) may
+    still be in flight on D when the next turn's P-path hop lands. Mixed
+    routing with short P-path turns next to long D-local appends on the same D:
+    the covered-token count must stay exact (no hole, no overrun)."""
+    convs = [{"conv_id": "long", "arrival": 0.0, "turns": [[600, 3], [900, 3], [900, 3]]}]
+    convs += [{"conv_id": f"s{i}", "arrival": 0.0005 * i, "turns": [[20, 2]] * 5} for i in range(6)]
+    for x in (0.0, 0.5):
+        job = {"cluster": "1P_1D", "x": x, "clock": "device", "conversations": convs,
+               "device": {"model": "tiny", "weight_seed": 5, "token_seed": 9, "gpus": [0],
+                          "prefill_chunk": 1024}}
+        r = E.run(job)
+        assert all(v["status"] == "completed" for v in E.records(r))
+        assert r["device"]["kv_lifecycle"]["coverage_errors"] == 0
+
+
+def test_shared_weights_per_gpu(gpu):
+    """Nodes colocated on one GPU with the same model share one weight copy."""
+    r = E.run(dev_job("2P_6D", 1.0, n=2))
+    assert all(n["weights_shared_by"] == 8 for n in r["device"]["nodes"])
+
+
+@pytest.mark.parametrize("cluster,x", [("1P_1D", 0.0), ("1P_1D", 1.0), ("4P_4D", 0.0), ("2P_6D", 0.5)])
+def test_realtime_engine_tokens_match_oracle(gpu, cluster, x):
+    """Wall-clock engine: a worker thread per node submits its steps, P->D hops
+    are asynchronous copies retired by per-destination waiters. Every request
+    completes with its target tokens and the generated ids equal the CPU
+    oracle replaying the step log (copies applied where the engine issued them)."""
+    r = E.run(rt_job(cluster, x, record_steps=True, n=4))
+    recs = E.records(r)
+    assert len(recs) == 12 and all(v["status"] == "completed" for v in recs)
+    assert r["device"]["clock"] == "realtime"
+    assert r["device"]["kv_lifecycle"]["coverage_errors"] == 0
+    assert r["device"]["kv_lifecycle"]["blocks_in_use_at_end"] == 0
+    if x < 1.0:
+        assert r["link_transfers"] > 0 and r["device"]["kv_transfer"]["gbs"] > 0
+    log = r["device"]["step_log"]
+    cfg = O.cfg_from(ppd.tiny_cfg())
+    model = O.Model(cfg, 5)
+    nblocks = max(max(e.get("block_tables", [0]) + e.get("src_blocks", [0]) + e.get("dst_blocks", [0]))
+                  for e in log) + 1
+    pools = {}
+    checked = 0
+    for e in log:
+        if e.get("copy"):
+            src = pools.setdefault(e["src"], O.KvPool(cfg, nblocks)).data
+            dst = pools.setdefault(e["dst"], O.KvPool(cfg, nblocks)).data
+            for p in range(e["start"], e["start"] + e["n"]):
+                dst[e["dst_blocks"][p // 16], :, :, :, p % 16] = src[e["src_blocks"][p // 16], :, :, :, p % 16]
+            continue
+        pool = pools.setdefault(e["node"], O.KvPool(cfg, nblocks))
+        n = len(e["q_len"])
+        bt = np.array(e["block_tables"], dtype=np.int32).reshape(n, e["max_blocks"])
+        t_o, _, margin = model.step(pool, e["q_len"], e["ctx"], e["tokens"], bt, want_logits=False)
+        for i in range(n):
+            if e["want"][i] and margin[i] > MARGIN:
+                assert e["out"][i] == t_o[i], (e["node"], i, e["out"][i], t_o[i], margin[i])
+                checked += 1
+    assert checked > 20
