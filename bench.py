@@ -31,6 +31,14 @@ sys.path.insert(0, REPO)
 
 METRIC = json.load(open(os.path.join(REPO, "BASELINE.json")))["metric"]
 SEED = 20260313
+# Dry run of the N > 1 path on a one-GPU box (tests only): every rank and every
+# engine node maps to GPU 0 and torch.distributed uses gloo. Never set for a
+# measurement: the numbers it prints are not multi-GPU numbers.
+SAME_GPU = os.environ.get("PPD_BENCH_SAME_GPU") == "1"
+
+
+def gpu_of(i: int) -> int:
+    return 0 if SAME_GPU else i
 
 
 def peaks():
@@ -273,7 +281,10 @@ def device_calibration(dev, cfg, inter: dict, B: int, ctx, tok, bts, cal_bt, lin
     measured KV-hop bandwidth (reference schema: costmodel.cpp:197-316)."""
     from paper_2603_13358_b200 import engine as E
     rng = np.random.default_rng(SEED + 7)
-    med = lambda f, n=3: float(np.median([f() for _ in range(n)]))
+    def med(f, n=3):
+        f()
+        f()  # first call of a shape runs eagerly, the second captures its CUDA graph
+        return float(np.median([f() for _ in range(n)]))
     samples = {"decode": [], "full": [], "append": [], "interference": [],
                "kv_bytes_per_token": 131072.0, "link_bandwidth": link_gbs * 1e9}
     for b in (8, 50, 100, B):
@@ -303,16 +314,17 @@ def nvlink_probe(world: int) -> dict:
     kernel (ppd_kv_copy) between two Llama-3-8B-shape pools on GPU 0 and GPU 1
     at 1536 and 8192 tokens, as a fraction of the best measured peak."""
     import paper_2603_13358_b200 as ppd
-    out = {"pair": [0, 1]}
-    out["ce_gbs"] = ppd.p2p_bandwidth(0, 1, 1 << 30, 5, 0)
-    out["sm_pull_gbs"] = ppd.p2p_bandwidth(0, 1, 1 << 30, 5, 1)
-    out["hbm_copy_gbs_same_gpu"] = ppd.p2p_bandwidth(0, 0, 1 << 30, 5, 1)
+    g0, g1 = gpu_of(0), gpu_of(1)
+    out = {"pair": [g0, g1], "dry_run_same_gpu": SAME_GPU}
+    out["ce_gbs"] = ppd.p2p_bandwidth(g0, g1, 1 << 30, 5, 0)
+    out["sm_pull_gbs"] = ppd.p2p_bandwidth(g0, g1, 1 << 30, 5, 1)
+    out["hbm_copy_gbs_same_gpu"] = ppd.p2p_bandwidth(g0, g0, 1 << 30, 5, 1)
     peak = max(out["ce_gbs"], out["sm_pull_gbs"])
     out["peak_gbs"] = peak
     out["peak_kind"] = "measured (best of copy-engine / SM-pull probe)"
     out["nominal_gbs"] = 900.0
     cfg = ppd.llama8b_cfg()
-    devs = [ppd.Device(g, cfg, max_step_tokens=256, max_step_seqs=8) for g in (0, 1)]
+    devs = [ppd.Device(g, cfg, max_step_tokens=256, max_step_seqs=8) for g in (g0, g1)]
     try:
         for d in devs:
             d.kv_pool_init(1024)
@@ -348,6 +360,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import paper_2603_13358_b200 as ppd
 
+    local_rank = gpu_of(local_rank)
     torch.cuda.set_device(local_rank)
     cfg = ppd.llama8b_cfg()
     B, ctx0 = args.batch, args.ctx
@@ -413,7 +426,7 @@ def run_ours(args, rank, world, local_rank):
     st = dev.stats()
     dev_ms = float(np.sum(step_ms))
     h2d_bytes = 4 * (B + 1 + B + B + B * bps + B + B + B) + 48 * B * 2
-    times = torch.tensor([dev_ms, wall * 1e3], dtype=torch.float64, device="cuda")
+    times = torch.tensor([dev_ms, wall * 1e3], dtype=torch.float64, device="cpu" if SAME_GPU else "cuda")
     if dist:
         torch.distributed.all_reduce(times, op=torch.distributed.ReduceOp.MAX)
     dev_ms_max, wall_ms_max = times.tolist()
@@ -492,7 +505,8 @@ def run_ours(args, rank, world, local_rank):
         else:
             # one node per GPU, wall clock: steps of different nodes run concurrently and
             # every KV hop overlaps its destination's decode steps
-            ttft = [guarded(engine_ttft, D.layout_gpus(lay, world), lay, quick=args.quick, clock="realtime")
+            ttft = [guarded(engine_ttft, [gpu_of(g) for g in D.layout_gpus(lay, world)], lay, quick=args.quick,
+                            clock="realtime")
                     for lay in D.node_layouts(world)]
             if isinstance(nvlink, dict) and nvlink.get("peak_gbs"):
                 for t in ttft:
@@ -677,9 +691,9 @@ def main():
         return
     if world > 1:
         import torch
-        torch.cuda.set_device(local_rank)
+        torch.cuda.set_device(gpu_of(local_rank))
         import datetime
-        torch.distributed.init_process_group("nccl", timeout=datetime.timedelta(minutes=30))
+        torch.distributed.init_process_group("gloo" if SAME_GPU else "nccl", timeout=datetime.timedelta(minutes=30))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch

@@ -37,7 +37,8 @@ struct DeviceOptions {
   std::uint64_t token_seed = 1;
   std::vector<int> gpus = {0};   // node i runs on gpus[i % gpus.size()]
   int kv_blocks_per_node = 0;    // 0: sized from the trace
-  int prefill_chunk = 2048;      // prefill tokens per iteration
+  int prefill_chunk = 2048;      // prefill tokens per iteration (D / R nodes: rides with decode rows)
+  int p_prefill_chunk = 8192;    // P nodes (prefill only): tokens per iteration
   int max_step_tokens = 0;       // 0: prefill_chunk + max_decode_batch + 64
   bool record_steps = false;     // emit the step log (oracle replay)
   bool record_tokens = true;     // emit generated token ids per request

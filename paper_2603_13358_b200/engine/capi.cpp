@@ -186,9 +186,27 @@ std::string build_table(const json& job) {
     if (n == 0) return std::nullopt;
     return std::make_pair(ttft / n, tpot / n);
   };
+  if (job.value("clock", std::string("virtual")) == "device") {
+    // Phase 1 on the B200s: every (grid key, x) cell runs through the engine's
+    // device clock (engine::device_benchmark_runner)
+    const engine::DeviceOptions opt = engine::DeviceOptions::from_json(job.value("device", json::object()).dump());
+    const routing::BenchmarkRunner dev = engine::device_benchmark_runner(cluster, opt, calib, seeds);
+    runner = [dev, duration](const routing::GridSpec& g, int x) {
+      routing::GridSpec h = g;
+      h.spec.duration_s = duration;
+      return dev(h, x);
+    };
+  }
+  std::vector<routing::GridSpec> grid = routing::default_grid();
+  if (job.contains("grid_keys")) {  // a subset of the 90 keys (absent keys route x = 0, routing.cpp:233-240)
+    const auto keys = job["grid_keys"].get<std::vector<std::string>>();
+    std::erase_if(grid, [&](const routing::GridSpec& g) {
+      return std::find(keys.begin(), keys.end(), g.key.str()) == keys.end();
+    });
+  }
   routing::SLOWeights w{job.value("w_ttft", 1.0), job.value("w_tpot", 1.0)};
-  const routing::DecisionTable t = routing::build_decision_table(routing::default_grid(), w, runner, calib->hash());
-  return json{{"table_json", t.to_json()}, {"calib_hash", calib->hash()}}.dump();
+  const routing::DecisionTable t = routing::build_decision_table(grid, w, runner, calib->hash());
+  return json{{"table_json", t.to_json()}, {"calib_hash", calib->hash()}, {"grid_keys", grid.size()}}.dump();
 }
 
 // ---- §8f-2 / §8f-4: sweep harness, analyses, trace ingest -----------------

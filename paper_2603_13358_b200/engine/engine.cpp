@@ -63,12 +63,14 @@ DeviceOptions DeviceOptions::from_json(const std::string& text) {
   if (j.contains("gpus")) o.gpus = j["gpus"].get<std::vector<int>>();
   o.kv_blocks_per_node = j.value("kv_blocks_per_node", 0);
   o.prefill_chunk = j.value("prefill_chunk", 2048);
+  o.p_prefill_chunk = j.value("p_prefill_chunk", 8192);
   o.max_step_tokens = j.value("max_step_tokens", 0);
   o.record_steps = j.value("record_steps", false);
   o.record_tokens = j.value("record_tokens", true);
   o.realtime = j.value("realtime", false);
   if (o.gpus.empty()) throw std::invalid_argument("device options: gpus must not be empty");
-  if (o.prefill_chunk < 1) throw std::invalid_argument("device options: prefill_chunk must be >= 1");
+  if (o.prefill_chunk < 1 || o.p_prefill_chunk < 1)
+    throw std::invalid_argument("device options: prefill_chunk and p_prefill_chunk must be >= 1");
   if (o.kv_blocks_per_node < 0) throw std::invalid_argument("device options: kv_blocks_per_node must be >= 0");
   return o;
 }
@@ -357,6 +359,8 @@ class DeviceCluster {
     const int blocks = opt.kv_blocks_per_node > 0 ? opt.kv_blocks_per_node : int(need_blocks);
     max_step_tokens_ = opt.max_step_tokens > 0 ? opt.max_step_tokens
                                                : opt.prefill_chunk + cfg_.max_decode_batch * 2 + 64;
+    // P nodes run prefill only (no decode rows to protect): larger chunks
+    p_step_tokens_ = opt.max_step_tokens > 0 ? opt.max_step_tokens : std::max(opt.p_prefill_chunk, 64);
     auto add = [&](char role, int n) {
       for (int i = 0; i < n; ++i) {
         Node nd;
@@ -372,7 +376,9 @@ class DeviceCluster {
     // a failure part-way releases every device already opened (RAII handles)
     for (Node& n : nodes_) {
       ppd_dev* d = nullptr;
-      check(ppd_dev_open(n.gpu, &mcfg_, max_step_tokens_, cfg_.max_decode_batch * 2 + 8, &d), "dev open");
+      check(ppd_dev_open(n.gpu, &mcfg_, n.role == 'P' ? p_step_tokens_ : max_step_tokens_,
+                         cfg_.max_decode_batch * 2 + 8, &d),
+            "dev open");
       n.dev.reset(d);
       check(ppd_load_random_weights(d, opt.weight_seed), "weights");
       check(ppd_kv_pool_init(d, 16, blocks), "kv pool");
@@ -566,7 +572,8 @@ class DeviceCluster {
   // pressure is recomputed from position 0 on the node instead
   Job append_job(int rid, int node) {
     const Req& r = reqs_[rid];
-    if (nodes_[node].pool.tokens(r.conv) < r.ctx) return Job{true, rid, 0, r.ctx + r.m, 0, now_, r.conv};
+    // (a pending completion flush still counts as cached: it runs before the append)
+    if (r.ctx > 0 && nodes_[node].pool.find(r.conv) == nullptr) return Job{true, rid, 0, r.ctx + r.m, 0, now_, r.conv};
     return Job{false, rid, r.ctx, r.ctx + r.m, r.ctx, now_, r.conv};
   }
   Job full_job(int rid, int key) {
@@ -653,7 +660,8 @@ class DeviceCluster {
     if (n.has_job) {
       Job& j = n.job;
       const Req& r = reqs_[j.req];
-      const long c = std::min<long>(opt_.prefill_chunk, j.end - j.next);
+      const long chunk_cap = n.role == 'P' ? std::min<long>(opt_.p_prefill_chunk, p_step_tokens_) : opt_.prefill_chunk;
+      const long c = std::min<long>(chunk_cap, j.end - j.next);
       if (n.pool.blocks_needed(j.key, j.next + c) <= n.pool.free_blocks()) {
         n.chunk = c;
         n.chunk_final = j.next + n.chunk == j.end;
@@ -1091,7 +1099,7 @@ class DeviceCluster {
   DeviceOptions opt_;
   ppd_model_cfg mcfg_{};
   double kv_tok_bytes_ = 0;
-  int max_step_tokens_ = 0;
+  int max_step_tokens_ = 0, p_step_tokens_ = 0;
   routing::RoutingPolicy policy_;
   routing::SessionTable sessions_;
   std::vector<Node> nodes_;

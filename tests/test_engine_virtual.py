@@ -100,3 +100,34 @@ def test_invalid_config_raises_value_error():
         E.run({"cluster": "2P", "x": 0.0, "conversations": []})
     with pytest.raises(ValueError):
         E.run({"cluster": "1P_1D", "x": 2.0, "conversations": []})
+
+
+def test_device_fit_recovers_exact_coefficients():
+    """fit_from_measurements (the router's device statistics):
+    synthetic samples generated from known coefficients come back exactly, the
+    measured link bandwidth and KV bytes/token replace the defaults, and a
+    measured interference point replaces the reference anchor it coincides
+    with (costmodel.cpp:299-313 schema) while every other anchor stays."""
+    a, b = 2e-5, 3e-9
+    aa, ab = 4e-5, 5e-9
+    c, d = 0.005, 3e-5
+    s = {"full": [[n, a * n + b * n * n] for n in (1000, 2000, 4000)],
+         "append": [[m, n, aa * m + ab * m * (n + m)] for m, n in ((512, 1024), (1536, 2048), (1536, 6144))],
+         "decode": [[B, c + d * B] for B in (1, 50, 100, 200)],
+         "link_bandwidth": 812e9, "kv_bytes_per_token": 131072,
+         "interference": [{"kind": "append", "prefill_tokens": 1024, "concurrent_prefills": 1,
+                           "decode_batch": 200, "tpot_multiplier": 1.07}]}
+    fit = json.loads(E.run({"op": "fit_calibration", "samples": s})["calib_json"])
+    for k, v in (("full_a_lin", a), ("full_b_quad", b), ("append_a_lin", aa), ("append_b_cross", ab),
+                 ("decode_c_base", c), ("decode_d_batch", d), ("link_bandwidth", 812e9),
+                 ("kv_bytes_per_token", 131072)):
+        assert fit[k] == pytest.approx(v, rel=1e-9), k
+    pts = {(p["kind"], p["prefill_tokens"], p["concurrent_prefills"], p["decode_batch"]): p["tpot_multiplier"]
+           for p in fit["interference_points"]}
+    assert pts[("append", 1024, 1, 200)] == 1.07
+    assert pts[("full", 1024, 1, 200)] == 1.48  # untouched reference anchor
+    assert len(pts) == 24
+    # the reference library accepts the fitted table unchanged (schema v1)
+    from oracle import oracle as O
+    ref = O.ref_tool({"op": "calib", "calib_json": json.dumps(fit)})
+    assert ref["hash"] == E.run({"op": "fit_calibration", "samples": s})["hash"]

@@ -26,7 +26,7 @@ def trace(n=3, turns=((40, 6), (24, 5), (17, 4))):
 def dev_job(cluster, x, record_steps=False, **kw):
     return {"cluster": cluster, "x": x, "clock": "device", "conversations": trace(**kw),
             "device": {"model": "tiny", "weight_seed": 5, "token_seed": 9, "gpus": [0],
-                       "prefill_chunk": 32, "record_steps": record_steps}}
+                       "prefill_chunk": 32, "p_prefill_chunk": 48, "record_steps": record_steps}}
 
 
 def test_device_replica_completes(gpu):
@@ -53,6 +53,9 @@ def test_device_transfer_accounting_matches_reference_rule(gpu):
     assert v0["link_transfers"] == x0["link_transfers"] and v0["link_bytes"] == x0["link_bytes"]
     r1 = E.records(x1)
     assert [x["route"] for x in r1 if x["turn_index"] > 1] == ["D_local"] * 6
+    # PPD appends only the new tokens on D (a pending completion flush is not an eviction)
+    d_node = x1["device"]["nodes"][1]
+    assert d_node["prefill_tokens"] == 3 * (24 + 17) and d_node["evictions"] == 0
     assert x1["device"]["kv_transfer"]["gbs"] > 0
 
 
@@ -257,3 +260,23 @@ def test_realtime_engine_tokens_match_oracle(gpu, cluster, x):
                 assert e["out"][i] == t_o[i], (e["node"], i, e["out"][i], t_o[i], margin[i])
                 checked += 1
     assert checked > 20
+
+
+def test_phase1_table_on_device_then_dynamic_routing(gpu):
+    """§8f-1: Phase 1 of Algorithm 1 built with engine::device_benchmark_runner
+    (every (key, x) cell runs on the GPU through the device clock), then the
+    dynamic router consumes that table on the device clock."""
+    import json as _json
+    dev = {"model": "tiny", "weight_seed": 5, "token_seed": 9, "gpus": [0], "prefill_chunk": 512}
+    keys = ["small|balanced|0.5", "small|balanced|1"]
+    t = E.run({"op": "build_table", "clock": "device", "cluster": "1P_1D", "duration_s": 1.0, "grid_keys": keys,
+               "device": dev})
+    entries = _json.loads(t["table_json"])["entries"]
+    assert sorted(entries) == sorted(keys)
+    assert all(e["available"] and e["ttft_x0"] > 0 and e["tpot_x1"] > 0 for e in entries.values())
+    wl = {"id": "w", "turn1": [256, 8], "turn2plus": [256, 8], "num_turns": 3, "qps": 1.0, "duration_s": 2.0}
+    r = E.run({"cluster": "1P_1D", "policy": "dynamic", "table_json": t["table_json"], "clock": "device",
+               "workload": wl, "seed": 1, "device": dev})
+    recs = E.records(r)
+    assert recs and all(v["status"] == "completed" for v in recs)
+    assert sum(r["route_decisions"]) == sum(1 for v in recs if v["route"] == "D_local")
