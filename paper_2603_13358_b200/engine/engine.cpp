@@ -376,8 +376,10 @@ class DeviceCluster {
     // a failure part-way releases every device already opened (RAII handles)
     for (Node& n : nodes_) {
       ppd_dev* d = nullptr;
+      // P nodes run one prefill job per step (serial lane): few sequences
+      const int seqs = cfg_.max_decode_batch * 2 + 8;
       check(ppd_dev_open(n.gpu, &mcfg_, n.role == 'P' ? p_step_tokens_ : max_step_tokens_,
-                         cfg_.max_decode_batch * 2 + 8, &d),
+                         n.role == 'P' ? std::min(seqs, p_step_tokens_) : std::min(seqs, max_step_tokens_), &d),
             "dev open");
       n.dev.reset(d);
       check(ppd_load_random_weights(d, opt.weight_seed), "weights");
