@@ -179,6 +179,7 @@ typedef struct ppd_gemm_parts {
   int32_t n, kbt, slots, rows, bn, n_tiles_t;
   int64_t total;
   uint64_t stride;
+  int32_t dp; /* leading whole-K (data-parallel) tiles; the stream-K ranges cover the rest */
 } ppd_gemm_parts;
 int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t N, int32_t K,
                       int32_t max_slices, ppd_gemm_parts* parts, void* stream);

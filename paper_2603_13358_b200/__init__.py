@@ -67,7 +67,7 @@ class GemmParts(ctypes.Structure):
     """ppd_gemm_parts: how the fp32 GEMM output is spread over K-partial slices."""
     _fields_ = [("n", ctypes.c_int32), ("kbt", ctypes.c_int32), ("slots", ctypes.c_int32),
                 ("rows", ctypes.c_int32), ("bn", ctypes.c_int32), ("n_tiles_t", ctypes.c_int32),
-                ("total", ctypes.c_int64), ("stride", ctypes.c_uint64)]
+                ("total", ctypes.c_int64), ("stride", ctypes.c_uint64), ("dp", ctypes.c_int32)]
 
     def owner(self, x):
         return ((x + 1) * self.slots + self.total - 1) // self.total - 1
@@ -76,8 +76,10 @@ class GemmParts(ctypes.Structure):
         """Valid slice count for output column `col` of token row `tok` (numpy arrays ok)."""
         if self.kbt == 0:
             return col * 0 + tok * 0 + self.n
-        t = (col // self.rows) * self.n_tiles_t + tok // self.bn
-        return self.owner(t * self.kbt + self.kbt - 1) - self.owner(t * self.kbt) + 1
+        t = (col // self.rows) * self.n_tiles_t + tok // self.bn - self.dp
+        tail = t * (t >= 0)  # whole-K tiles [0, dp) have one valid slice
+        v = self.owner(tail * self.kbt + self.kbt - 1) - self.owner(tail * self.kbt) + 1
+        return v * (t >= 0) + 1 * (t < 0)
 
 
 class DevStats(ctypes.Structure):

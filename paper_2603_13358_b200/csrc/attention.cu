@@ -448,6 +448,10 @@ PPD_DEV void decode_body(const CUtensorMap* kv_map, const AttnParams& p, uint8_t
   if (warp == kConsumerWarps) {
     // the 16 boxes of a stage (4 blocks x K|V x two 64-dim halves): one lane each
     const int b = lane >> 2, is_v = (lane >> 1) & 1, h = lane & 1;
+    // overlap: cached K/V (positions < ctx) was written by earlier steps, so it
+    // streams before the predecessor (RoPE + KV write of this step's rows)
+    // retires; the first stage holding a position >= ctx waits for it
+    bool waited = !p.overlap;
     int g = 0;  // global stage counter across this CTA's segments
     for (int sg = seg0; sg < seg1; ++sg) {
       const AttnItem it = p.items[sg];
@@ -455,11 +459,16 @@ PPD_DEV void decode_body(const CUtensorMap* kv_map, const AttnParams& p, uint8_t
       const int* btab = p.block_tables + (size_t)it.seq * p.max_blocks;
       const int first_blk = it.key_begin / kBT, last_blk = (it.key_end - 1) / kBT;
       const int nst = (last_blk - first_blk) / kStageBlocks + 1;
+      const int new_pos = p.ctx[it.seq];
       for (int st = 0; st < nst; ++st, ++g) {
         const int slot = g % kStages;
         if (g >= kStages) mbar_wait(&empty_bar[slot], ((g / kStages) - 1) & 1);
         const int b0 = first_blk + st * kStageBlocks;
         const int nb = min(kStageBlocks, last_blk - b0 + 1);
+        if (!waited && (b0 + nb) * kBT > new_pos) {
+          pdl_wait();
+          waited = true;
+        }
         if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], nb * 2 * kBlockBytes);
         __syncwarp();
         if (lane < 16 && b < nb) {
@@ -475,6 +484,10 @@ PPD_DEV void decode_body(const CUtensorMap* kv_map, const AttnParams& p, uint8_t
   }
 
   // ---------------- consumer warps ----------------
+  if (p.overlap) {  // q is written by the predecessor
+    pdl_wait();
+    pdl_trigger();
+  }
   const int g8 = lane >> 2, t = lane & 3;
   const float sl2 = p.scale_log2;
   const int tid = warp * 32 + lane;  // 0..127
@@ -651,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     decode_attention_kernel(const __grid_constant__ CUtensorMap kv_map, AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  pdl_wait();
+  if (!p.overlap) pdl_wait();
   decode_body(&kv_map, p, smem, blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31, 0, 1);
 }
 
@@ -687,6 +700,7 @@ __global__ void __launch_bounds__(kMixThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ int s_next;
   pdl_wait();
+  if (p.overlap) pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if ((int)blockIdx.x >= n_pf) {
     // ---------------- decode: two static virtual CTAs, then help with prefill

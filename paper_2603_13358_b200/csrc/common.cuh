@@ -152,4 +152,20 @@ namespace ppdk {
 // weight prefetch overlap this kernel's tail).
 PPD_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 PPD_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// Entry of a light (no shared memory, short) kernel. kEarly: let the next
+// kernel launch BEFORE waiting on our predecessor, so a heavy successor (GEMM /
+// attention) gets its CTAs resident as the heavy predecessor's CTAs retire and
+// starts streaming its weights / cached K/V (inputs this kernel does not
+// write) into that tail. Heavy kernels trigger only after their own wait, so
+// at most heavy -> light -> heavy are in flight (no unbounded launch cascade).
+template <bool kEarly>
+PPD_DEV void pdl_enter() {
+  if (kEarly) {
+    pdl_trigger();
+    pdl_wait();
+  } else {
+    pdl_wait();
+    pdl_trigger();
+  }
+}
 }  // namespace ppdk

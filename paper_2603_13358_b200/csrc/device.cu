@@ -529,6 +529,7 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   p.ws_ml = ws_ml;
   p.counters = counters;
   p.mix_ctr = mix_ctr;
+  p.overlap = pdl_overlap();
   // K2: a mixed step is ONE launch (prefill CTAs + decode CTAs)
   if (n_pf > 0) {
     CU(launch_mixed_attention(kv_map, p, d_items + n_dec, n_pf, (n_items - n_dec) * c.n_kv_heads, n_cta, s));
@@ -1313,6 +1314,7 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
   parts->n_tiles_t = g.n_tiles_t;
   parts->total = g.total;
   parts->stride = g.stride;
+  parts->dp = g.dp;
   return PPD_OK;
 }
 
@@ -1346,6 +1348,15 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "ws_two_slices") == 0) {  // takes effect for devices opened afterwards
     CHECK_ARG(value == 0 || value == 1, "ws_two_slices must be 0 or 1");
     g_ws_two_slices = value != 0;
+  } else if (std::strcmp(name, "gemm_even_tiles") == 0) {
+    CHECK_ARG(value == 0 || value == 1, "gemm_even_tiles must be 0 or 1");
+    gemm_tc_set_even_tiles(value != 0);
+  } else if (std::strcmp(name, "pdl_overlap") == 0) {
+    CHECK_ARG(value == 0 || value == 1, "pdl_overlap must be 0 or 1");
+    set_pdl_overlap(value);
+  } else if (std::strcmp(name, "gemm_l2_pre") == 0) {
+    CHECK_ARG(value >= -1 && value <= 256, "gemm_l2_pre must be in [-1, 256]");
+    gemm_tc_set_l2_pre(value);
   } else if (std::strcmp(name, "mlp_fused") == 0) {
     CHECK_ARG(value >= 0 && value <= 2, "mlp_fused must be 0, 1 or 2");
     g_mlp_fused = value;

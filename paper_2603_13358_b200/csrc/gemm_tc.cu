@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
@@ -48,6 +49,14 @@ PPD_DEV void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint6
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
+}
+
+// prefetch one box of a tensor-mapped matrix into L2 (no smem, no completion)
+PPD_DEV void tma_prefetch_l2(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y)
+               : "memory");
 }
 
 PPD_DEV uint64_t sw128_kmajor_desc(uint32_t saddr) {
@@ -148,14 +157,19 @@ PPD_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
 // A segment is a contiguous k-block range [kb0, kb1) of one (weight tile,
 // token tile) whose accumulator goes to partial slice `slice`.
 //  * uniform: units (tile, split) dealt round-robin to the slots;
-//  * balanced: slot c owns items [c*total/slots, (c+1)*total/slots) of the
-//    flattened (tile, k-block) space (GemmParts documents the slice rule).
+//  * balanced: the first `dp` tiles (whole waves of whole-K units) are dealt
+//    round-robin, so consecutive slots share a weight tile at the same
+//    k-block (its weights come from HBM once, from L2 for the other token
+//    tiles); the remaining (tile, k-block) items, `total` of them, are cut
+//    into `tail_slots` equal contiguous ranges, slot c < tail_slots owning
+//    [c*total/tail_slots, (c+1)*total/tail_slots) (stream-K tail: no wave
+//    quantization). GemmParts documents the slice rule.
 struct Seg {
   int tw, tt, kb0, kb1, slice;
 };
 struct Sched {
   int n_tiles_t, kbt, kb_per, splits, n_units, slots, c, u;
-  int balanced;
+  int balanced, dp, tslots;
   long long total, x, end;
 
   PPD_DEV void begin(const GemmTcParams& p, int rows, int c_, int slots_) {
@@ -168,14 +182,16 @@ struct Sched {
     c = c_;
     u = c_;
     balanced = p.balanced;
+    dp = p.dp;
+    tslots = p.tail_slots;
     total = p.total;
     x = end = 0;
-    if (balanced) {
-      x = (long long)c_ * total / slots_;
-      end = (long long)(c_ + 1) * total / slots_;
+    if (balanced && c_ < tslots) {
+      x = (long long)c_ * total / tslots;
+      end = (long long)(c_ + 1) * total / tslots;
     }
   }
-  PPD_DEV int owner(long long item) const { return (int)(((item + 1) * slots + total - 1) / total) - 1; }
+  PPD_DEV int owner(long long item) const { return (int)(((item + 1) * tslots + total - 1) / total) - 1; }
   PPD_DEV bool next(Seg& s) {
     if (!balanced) {
       if (u >= n_units) return false;
@@ -188,12 +204,21 @@ struct Sched {
       u += slots;
       return true;
     }
+    if (u < dp) {  // data-parallel waves: whole K, slice 0
+      s.tt = u % n_tiles_t;
+      s.tw = u / n_tiles_t;
+      s.kb0 = 0;
+      s.kb1 = kbt;
+      s.slice = 0;
+      u += slots;
+      return true;
+    }
     if (x >= end) return false;
     const long long t = x / kbt;
     s.kb0 = (int)(x - t * kbt);
     s.kb1 = (int)min((long long)kbt, s.kb0 + (end - x));
-    s.tt = (int)(t % n_tiles_t);
-    s.tw = (int)(t / n_tiles_t);
+    s.tt = (int)((t + dp) % n_tiles_t);
+    s.tw = (int)((t + dp) / n_tiles_t);
     s.slice = c - owner(t * kbt);
     x += s.kb1 - s.kb0;
     return true;
@@ -273,7 +298,9 @@ __global__ void __launch_bounds__(kThreads, kOcc)
   if (kPair) cluster_sync_all();  // peer barriers initialised + TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_trigger();  // the next kernel may launch; it waits for our completion itself
+  // the next kernel may launch; it waits for our completion itself. overlap:
+  // only once our own predecessor retired (pdl_enter in common.cuh)
+  if (!p.overlap) pdl_trigger();
 
   const int rows = kBM * kCta;
   const uint32_t full_bar0 = kPair ? mapa_shared(smem_u32(full), 0) : smem_u32(full);
@@ -289,6 +316,10 @@ __global__ void __launch_bounds__(kThreads, kOcc)
       tma_load_2d(dst, map, x, y, &full[s]);
   };
 
+  if (p.overlap && !(warp == 0 && lane == 0) && warp < 4) {  // every thread passes the wait before triggering
+    pdl_wait();
+    pdl_trigger();
+  }
   if (warp == 0) {
     if (lane == 0) {
       Sched sc;
@@ -304,7 +335,21 @@ __global__ void __launch_bounds__(kThreads, kOcc)
           }
         }
       }
+      // and the next l2_pre k-blocks' weights into L2: the HBM pipe stays busy
+      // through the predecessor's tail instead of idling until its outputs land
+      if (p.l2_pre > 0) {
+        Sched pre = sc;
+        int idx = 0, done = 0;
+        while (done < p.l2_pre && pre.next(sg)) {
+          for (int kb = sg.kb0; kb < sg.kb1 && done < p.l2_pre; ++kb, ++idx) {
+            if (idx < npre) continue;
+            tma_prefetch_l2(&map_w, kb * kBK, sg.tw * rows + w_row0);
+            ++done;
+          }
+        }
+      }
       pdl_wait();
+      if (p.overlap) pdl_trigger();
       int it = 0;  // global stage counter across segments
       while (sc.next(sg)) {
         for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++it) {
@@ -377,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, kOcc)
     }
   } else if (warp >= 4) {
     pdl_wait();  // outputs are written only after the predecessor retired
+    if (p.overlap) pdl_trigger();
     const int q = warp & 3;  // TMEM lane quarter owned by this warp
     Sched sc;
     sc.begin(p, rows, slot, n_slots);
@@ -541,6 +587,8 @@ bool get_map(CUtensorMap* out, const void* ptr, int rows, int K, int box_rows) {
 // 0 uniform K split / 1 balanced partition.
 static int g_pair_mode = -1;
 static bool g_multi_sub = true;  // T in (256, 512]: one unit covers both token sub-tiles
+static bool g_even_tiles = true;  // T > 256 in separate token tiles: equal tiles, not 256-row ones
+void gemm_tc_set_even_tiles(bool on) { g_even_tiles = on; }
 // two co-resident single CTAs per SM: -1 auto (<= kOcc2MaxT tokens; measured
 // tools/gemm_knobs.py: +10-20% weight streaming at T = 64 / 128, neutral at
 // T = 200, a loss with CTA pairs), 0 off, 1 whenever the shape allows
@@ -549,6 +597,9 @@ constexpr int kOcc2MaxT = 128;
 constexpr int kOcc2Smem = 113 * 1024;
 static int g_stage_cap = 0;
 static int g_sched = -1;
+static int g_l2_pre = 0;  // measured: neutral to 1.5% slower at 8-32 k-blocks (tools/ab_step.py)
+constexpr int kL2PreAuto = 16;  // weight k-blocks (16 KB each per CTA) prefetched into L2 ahead of the ring
+void gemm_tc_set_l2_pre(int n) { g_l2_pre = n; }
 
 
 
@@ -642,20 +693,30 @@ int max_pair_slots(int smem, int occ) {
 constexpr int kSubPairMinK = 8192;
 Shape shape_for(int T, int N, int K, int extra_smem = 0, bool force_single = false) {
   Shape sh{};
+  // two token sub-tiles per unit only where the weight-tile grid alone keeps
+  // the SMs busy (gate|up) or the K loop is long enough to split (down); the
+  // narrow projections (qkv, o) need the parallelism of separate token tiles
+  // (tools/gemm_mixed.py: qkv at T=456 39 -> 26 us, o 30 -> 19 us)
+  const bool wide = (N + kBM - 1) / kBM >= kPairMinTilesPerSm * device_sms() || K >= kSubPairMinK;
   if (T <= kMaxBN) {
     sh.n_sub = 1;
     sh.bn = ((T + 15) / 16) * 16;
-  } else if (T <= 2 * kMaxBN && g_multi_sub) {
+  } else if (T <= 2 * kMaxBN && g_multi_sub && wide) {
     sh.n_sub = 2;
     sh.bn = (((T + 1) / 2 + 15) / 16) * 16;
   } else {
+    // equal token tiles (T=328: 2 x 176 rather than 256 + 72): shallower
+    // activation stages, so a deeper ring
+    const int ntt = (T + kMaxBN - 1) / kMaxBN;
     sh.n_sub = 1;
-    sh.bn = kMaxBN;
+    sh.bn = g_even_tiles ? (((T + ntt - 1) / ntt + 15) / 16) * 16 : kMaxBN;
   }
   sh.unit_t = sh.bn * sh.n_sub;
   const double tiles1 = double((N + kBM - 1) / kBM) * ((T + sh.unit_t - 1) / sh.unit_t);
+  // long-K (down projection) steps of > 1024 rows pair as well (T=2048: 232 -> 220 us)
   const bool auto_pair =
-      T >= kPairMinT && (tiles1 >= kPairMinTilesPerSm * device_sms() || (sh.n_sub > 1 && K >= kSubPairMinK));
+      T >= kPairMinT && (tiles1 >= kPairMinTilesPerSm * device_sms() || (sh.n_sub > 1 && K >= kSubPairMinK) ||
+                         (T > 4 * kMaxBN && K >= kSubPairMinK));
   const bool want_occ2 = sh.n_sub == 1 && extra_smem == 0 && (g_occ2 == 1 || (g_occ2 < 0 && T <= kOcc2MaxT));
   sh.pair = !force_single && (g_pair_mode == 1 || (g_pair_mode < 0 && auto_pair && !want_occ2));
   sh.rows = sh.pair ? 2 * kBM : kBM;
@@ -680,13 +741,16 @@ struct Plan {
   int splits;       // uniform: K splits
   int slots;        // CTAs (pairs) launched
   int n_slices;     // partial slices written
-  long long total;  // balanced: tiles * kbt
+  long long total;  // balanced: (tiles - dp) * kbt items of the stream-K tail
+  int dp = 0;       // balanced: leading whole-K tiles (whole waves, data-parallel)
+  int tail_slots = 0;
 };
 
 // Persistent CTAs (pairs) each stream their share of the weights; a step
 // costs the busiest slot's bytes:
 //   uniform(s): ceil(tiles*s/slots) units x (W slab / s + partial tile out)
-//   balanced  : ceil(total/slots) k-blocks of W + (segments) partial tiles out
+//   balanced  : dp/slots whole-K units + ceil(total/tail_slots) k-blocks of
+//               the tail, plus the partial tiles out
 // Slices are capped so the callers' workspaces (max_slices slices) hold them.
 Plan plan_for(const Shape& sh, int T, int N, int K, int max_slices) {
   const int tiles = ((N + sh.rows - 1) / sh.rows) * ((T + sh.unit_t - 1) / sh.unit_t);
@@ -705,24 +769,48 @@ Plan plan_for(const Shape& sh, int T, int N, int K, int max_slices) {
       best = Plan{false, s, units < sh.slots ? units : sh.slots, s, 0};
     }
   }
-  if (g_sched != 0 && max_slices >= 2 && !(g_sched < 0 && sh.n_sub > 1)) {
-    const long long total = (long long)tiles * kbt;
-    const int slots = (int)(total < sh.slots ? total : sh.slots);
-    const long long share = (total + slots - 1) / slots;
-    // slices = most ranges touching one tile; segments = most tiles one range touches
-    GemmParts g;
-    g.kbt = kbt;
-    g.slots = slots;
-    g.total = total;
-    int n_slices = 1;
-    for (long long t = 0; t < tiles; ++t) {
-      const int v = g.owner(t * kbt + kbt - 1) - g.owner(t * kbt) + 1;
-      n_slices = v > n_slices ? v : n_slices;
+  // auto: the balanced partition for decode-size steps of the short-K
+  // projections (pure stream-K), and for > 512-row steps as whole waves of
+  // whole-K tiles plus a stream-K tail when that beats the uniform splits
+  // (wave quantization: o / down at T=1224-1736 lost 10-25% to it). Uniform
+  // units keep the token tiles of one weight tile in step, so its weights
+  // stream from HBM once and from L2 for the other tiles; a pure stream-K
+  // partition of a many-token-tile step loses that (qkv at T=4096: 173 vs
+  // 157 us) -- the data-parallel waves keep it for all but the tail.
+  // tools/gemm_mixed.py: uniform measured faster than pure stream-K for
+  // gate|up at T=712 (160 -> 138 us) and down at T=200-456 (4-7%).
+  const bool auto_bal = (sh.n_sub == 1 && T <= kMaxBN && K < kSubPairMinK) || T > 2 * kMaxBN;
+  if (g_sched != 0 && max_slices >= 2 && (g_sched == 1 || auto_bal)) {
+    const int dp = T > kMaxBN ? (tiles / sh.slots) * sh.slots : 0;
+    const long long total = (long long)(tiles - dp) * kbt;
+    // a multi-token-tile step without one whole wave stays uniform: a pure
+    // stream-K cut of it loses the weight reuse through L2 (down at T=1024:
+    // 116 -> 129 us)
+    if (total > 0 && !(T > kMaxBN && dp == 0)) {
+      long long ts = total < sh.slots ? total : sh.slots;
+      // a tail tile may touch at most max_slices ranges: share >= kbt / (max_slices - 1)
+      ts = std::min(ts, (long long)(tiles - dp) * (max_slices - 1));
+      const int tslots = (int)std::max(1LL, ts);
+      const long long share = (total + tslots - 1) / tslots;
+      // slices = most ranges touching one tile; segments = most tiles one range touches
+      GemmParts g;
+      g.kbt = kbt;
+      g.slots = tslots;
+      g.total = total;
+      int n_slices = 1;
+      for (long long t = 0; t < tiles - dp; ++t) {
+        const int v = g.owner(t * kbt + kbt - 1) - g.owner(t * kbt) + 1;
+        n_slices = v > n_slices ? v : n_slices;
+      }
+      const long long segs = (share + kbt - 1) / kbt + 1;
+      const int dp_rounds = dp / sh.slots;
+      const double cost = w_kb * (double(dp_rounds) * kbt + share) + (dp_rounds + segs) * out_tile;
+      const bool want = g_sched == 1 || cost < best_cost * (T > kMaxBN ? 0.97 : 0.95);
+      if (want && n_slices <= max_slices) {
+        best = Plan{true, 1, dp > 0 ? sh.slots : tslots, n_slices, total, dp, tslots};
+        best_cost = cost;
+      }
     }
-    const long long segs = (share + kbt - 1) / kbt + 1;
-    const double cost = w_kb * share + segs * out_tile;
-    const bool want = g_sched == 1 || cost < best_cost * 0.95;
-    if (want && n_slices <= max_slices) best = Plan{true, 1, slots, n_slices, total};
   }
   return best;
 }
@@ -764,6 +852,11 @@ cudaError_t launch(const Shape& sh, const Plan& pl, const bf16* X, const bf16* W
   p.balanced = pl.balanced ? 1 : 0;
   p.slots = pl.slots;
   p.total = pl.total;
+  p.dp = pl.dp;
+  p.tail_slots = pl.tail_slots;
+  // weight-streaming shapes (<= 512 token rows) prefetch ahead into L2
+  p.l2_pre = g_l2_pre >= 0 ? g_l2_pre : (T <= 2 * kMaxBN ? kL2PreAuto : 0);
+  p.overlap = pdl_overlap();
   CUtensorMap mw, mx;
   if (!get_map(&mw, W, N, K, kBM) || !get_map(&mx, X, T, K, sh.pair ? sh.bn / 2 : sh.bn))
     return cudaErrorInvalidValue;
@@ -800,11 +893,12 @@ cudaError_t gemm_tc_run_parts(const bf16* X, const bf16* W, float* out, int T, i
   g.n = pl.n_slices;
   g.stride = split_stride ? split_stride : (size_t)T * N;
   g.kbt = pl.balanced ? (K + kBK - 1) / kBK : 0;
-  g.slots = pl.slots;
+  g.slots = pl.balanced ? pl.tail_slots : pl.slots;
   g.rows = sh.rows;
   g.bn = sh.unit_t;
   g.n_tiles_t = (T + sh.unit_t - 1) / sh.unit_t;
   g.total = pl.balanced ? pl.total : 1;
+  g.dp = pl.balanced ? pl.dp : 0;
   *parts = g;
   return launch(sh, pl, X, W, out, T, N, K, true, g.stride, s);
 }

@@ -12,10 +12,11 @@ typedef __nv_bfloat16 bf16;
 // How a GEMM's fp32 output C[T][N] is stored as partial slices
 // out + j*stride, j < n; C = sum of the slices that are VALID for the element.
 //  * uniform split (kbt == 0): every slice is valid everywhere.
-//  * balanced (stream-K) partition: the flattened (tile, k-block) space of
-//    `total` = tiles*kbt items is cut into `slots` equal contiguous ranges, one
-//    per persistent CTA (pair); the j-th range touching a tile writes slice j,
-//    so a tile has (owner(last item) - owner(first item) + 1) valid slices.
+//  * balanced (stream-K) partition: tiles [0, dp) are whole-K units (one
+//    valid slice); the flattened (tile - dp, k-block) space of the other
+//    tiles, `total` = (tiles - dp)*kbt items, is cut into `slots` equal
+//    contiguous ranges; the j-th range touching a tile writes slice j, so a
+//    tile has (owner(last item) - owner(first item) + 1) valid slices.
 // Slices are summed in order j = 0, 1, ... (fixed order: deterministic).
 struct GemmParts {
   int n = 1;            // slices
@@ -25,7 +26,8 @@ struct GemmParts {
   int rows = 128;       // weight rows (output columns) per tile
   int bn = 256;         // token rows per tile (a unit: all token sub-tiles of one weight stage)
   int n_tiles_t = 1;    // token tiles
-  long long total = 1;  // tiles * kbt
+  long long total = 1;  // (tiles - dp) * kbt
+  int dp = 0;           // leading whole-K (data-parallel) tiles
 
   __host__ __device__ __forceinline__ int owner(long long x) const {
     return (int)(((x + 1) * slots + total - 1) / total) - 1;
@@ -33,7 +35,8 @@ struct GemmParts {
   // valid slices for output column `col` of token row `tok`
   __host__ __device__ __forceinline__ int valid(int col, int tok) const {
     if (kbt == 0) return n;
-    const long long t = (long long)(col / rows) * n_tiles_t + tok / bn;
+    const long long t = (long long)(col / rows) * n_tiles_t + tok / bn - dp;
+    if (t < 0) return 1;
     return owner(t * kbt + kbt - 1) - owner(t * kbt) + 1;
   }
 };
@@ -47,6 +50,10 @@ struct GemmTcParams {
   long long total;      // tiles * k-blocks per tile (balanced)
   int epi;              // 0: write C (fp32 slices / bf16); 1: fused SiLU(gate)*up -> bf16 [T][N/2]
   int n_sub;            // token sub-tiles (of bn rows) per unit: every weight stage feeds n_sub MMAs
+  int dp;               // balanced: leading whole-K tiles dealt round-robin
+  int tail_slots;       // balanced: slots sharing the stream-K tail (<= slots)
+  int l2_pre;           // weight k-blocks beyond the smem ring prefetched into L2 before the PDL wait
+  int overlap;          // 1: trigger the successor only after our own PDL wait (see pdl_enter)
 };
 
 // out[T][N] (+ split slices) = X[T][K] . W[N][K]^T ; splits > 1 needs out_f32
@@ -66,9 +73,14 @@ void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched);
 // T in (256, 512] token rows: one unit per weight tile covering 2 token
 // sub-tiles (default on) vs separate 256-row token tiles (A/B knob)
 void gemm_tc_set_multi_sub(bool on);
+// T > 256 rows in separate token tiles: equal tiles (default) vs 256-row tiles (A/B knob)
+void gemm_tc_set_even_tiles(bool on);
 // two co-resident CTAs per SM (half-depth rings, one accumulator each):
 // -1 auto (small token counts), 0 off, 1 whenever the shape allows
 void gemm_tc_set_occ2(int mode);
+// weight k-blocks each CTA prefetches into L2 (beyond its smem ring) while its
+// predecessor finishes: -1 auto, 0 off, n
+void gemm_tc_set_l2_pre(int n);
 // K-split count that fills the 148 SMs for this shape (1 when the tile grid already does)
 int gemm_tc_plan_splits(int T, int N, int K);
 

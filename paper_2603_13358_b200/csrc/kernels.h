@@ -42,6 +42,7 @@ struct AttnParams {
   // balanced decode schedule: CTA c owns decode segments [seg_start[c], seg_start[c+1])
   const int* seg_start;
   int* mix_ctr;              // K2 queue heads + done counter [3], zero-initialised, self-resetting
+  int overlap;               // decode: stream cached K/V before waiting on the predecessor (pdl_overlap)
 };
 
 // Persistent decode attention over balanced key segments (kv head in item.pad[0]).
@@ -117,6 +118,10 @@ namespace ppdk {
 // kernel may begin while its predecessor drains; kernels call pdl_wait()
 // before consuming predecessor outputs.
 bool pdl_enabled();
+// light kernels trigger their successor before waiting (tuning "pdl_overlap",
+// default off: measured 2.5% slower): see pdl_enter in common.cuh
+int pdl_overlap();
+void set_pdl_overlap(int on);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {

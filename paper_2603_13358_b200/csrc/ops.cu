@@ -117,9 +117,9 @@ cudaError_t launch_fill_const(bf16* dst, uint64_t n, float v, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ embed
+template <bool kEarly>
 __global__ void embed_kernel(const int* tokens, const bf16* embed, bf16* x, int d) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter<kEarly>();
   const int r = blockIdx.x;
   const uint4* src = reinterpret_cast<const uint4*>(embed + (size_t)tokens[r] * d);
   uint4* dst = reinterpret_cast<uint4*>(x + (size_t)r * d);
@@ -127,19 +127,18 @@ __global__ void embed_kernel(const int* tokens, const bf16* embed, bf16* x, int 
 }
 cudaError_t launch_embed(const int* tokens, const bf16* embed, bf16* x, int T, int d, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  return launch_pdl(embed_kernel, dim3(T), dim3(128), 0, s, tokens, embed, x, d);
-  return cudaGetLastError();
+  return launch_pdl(pdl_overlap() ? embed_kernel<true> : embed_kernel<false>, dim3(T), dim3(128), 0, s, tokens,
+                    embed, x, d);
 }
 
 // --------------------------------------------------- residual add + RMSNorm
 // v = x (+ rbf(sum of delta partials) | + delta_bf16); x <- v ; out = rbf(rbf(v) * inv_rms) * w
-template <bool kWriteX>
+template <bool kWriteX, bool kEarly>
 __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
     bf16* x, const float* df, GemmParts parts, const bf16* db, const bf16* w,
     bf16* out, const int* rows, int d, float eps) {
   __shared__ float red[33];
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter<kEarly>();
   const size_t row = rows ? (size_t)rows[blockIdx.x] : (size_t)blockIdx.x;
   const int nc = d / 8;
   float v[kMaxChunks][8];
@@ -195,7 +194,7 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
 cudaError_t launch_add_rmsnorm(bf16* x, const float* delta_f32, const GemmParts& parts, const bf16* delta_bf16,
                                const bf16* w, bf16* h, int T, int d, float eps, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  return launch_pdl(add_rmsnorm_kernel<true>, dim3(T), dim3(kNormThreads), 0, s, x, delta_f32, parts, delta_bf16,
+  return launch_pdl(pdl_overlap() ? add_rmsnorm_kernel<true, true> : add_rmsnorm_kernel<true, false>, dim3(T), dim3(kNormThreads), 0, s, x, delta_f32, parts, delta_bf16,
                     w, h, (const int*)nullptr, d, eps);
 }
 
@@ -203,7 +202,7 @@ cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, const GemmP
                               const bf16* delta_bf16, const int* rows, int n_rows, const bf16* w,
                               bf16* out, int T, int d, float eps, cudaStream_t s) {
   if (n_rows == 0) return cudaSuccess;
-  return launch_pdl(add_rmsnorm_kernel<false>, dim3(n_rows), dim3(kNormThreads), 0, s, const_cast<bf16*>(x),
+  return launch_pdl(pdl_overlap() ? add_rmsnorm_kernel<false, true> : add_rmsnorm_kernel<false, false>, dim3(n_rows), dim3(kNormThreads), 0, s, const_cast<bf16*>(x),
                     delta_f32, parts, delta_bf16, w, out, rows, d, eps);
 }
 
@@ -237,13 +236,13 @@ PPD_DEV void st_bf16x4(bf16* dst, float a, float b, float c, float d) {
   *reinterpret_cast<uint2*>(dst) = make_uint2(pack2(a, b), pack2(c, d));
 }
 
+template <bool kEarly>
 __global__ void rope_kv_kernel(const float* qkv, GemmParts parts, const float* bias,
                                const int* row_seq, const int* row_pos, const int* block_tables,
                                int max_blocks, const float* rope_cos, const float* rope_sin,
                                bf16* q_out, bf16* kv, int Hq, int Hkv, int Dh, int n_layers,
                                int layer, int BT) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter<kEarly>();
   const int r = blockIdx.x;
   const int half = Dh / 2;
   const int qd = Hq * Dh, kd = Hkv * Dh, W = qd + 2 * kd;
@@ -298,7 +297,7 @@ cudaError_t launch_rope_kv_write(const float* qkv, const GemmParts& parts, const
   if (T == 0) return cudaSuccess;
   const size_t W = (size_t)(Hq + 2 * Hkv) * Dh;
   // (row, quarter of the row's rotary/v units): 4 CTAs per token row for memory parallelism
-  return launch_pdl(rope_kv_kernel, dim3(T, 4), dim3(128), 0, s, qkv, parts, bias, row_seq, row_pos,
+  return launch_pdl(pdl_overlap() ? rope_kv_kernel<true> : rope_kv_kernel<false>, dim3(T, 4), dim3(128), 0, s, qkv, parts, bias, row_seq, row_pos,
                     block_tables, max_blocks, rope_cos, rope_sin, q_out, kv_pool, Hq, Hkv, Dh, n_layers, layer,
                     block_tokens);
 }
@@ -306,9 +305,9 @@ cudaError_t launch_rope_kv_write(const float* qkv, const GemmParts& parts, const
 // ------------------------------------------------------------- SiLU * up
 // gate/up come interleaved in 64-column groups (launch_fill_gate_up layout);
 // each thread produces 4 outputs from one float4 of gate and one of up.
+template <bool kEarly>
 __global__ void silu_mul_kernel(const float* gu, GemmParts parts, bf16* m, int F) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter<kEarly>();
   const int r = blockIdx.y;
   const float* row = gu + (size_t)r * 2 * F;
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4) {
@@ -326,13 +325,13 @@ __global__ void silu_mul_kernel(const float* gu, GemmParts parts, bf16* m, int F
 cudaError_t launch_silu_mul(const float* gu, const GemmParts& parts, bf16* m, int T, int F, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   dim3 grid((F / 4 + 255) / 256, T);
-  return launch_pdl(silu_mul_kernel, grid, dim3(256), 0, s, gu, parts, m, F);
+  return launch_pdl(pdl_overlap() ? silu_mul_kernel<true> : silu_mul_kernel<false>, grid, dim3(256), 0, s, gu, parts, m, F);
 }
 
 // ---------------------------------------------------------------- argmax
+template <bool kEarly>
 __global__ void argmax_kernel(const float* logits, int V, int* out) {
-  pdl_wait();
-  pdl_trigger();
+  pdl_enter<kEarly>();
   const float* row = logits + (size_t)blockIdx.x * V;
   float best = -INFINITY;
   int bi = 0x7fffffff;
@@ -387,7 +386,7 @@ __global__ void argmax_kernel(const float* logits, int V, int* out) {
 }
 cudaError_t launch_argmax(const float* logits, int n, int V, int* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  return launch_pdl(argmax_kernel, dim3(n), dim3(1024), 0, s, logits, V, out);
+  return launch_pdl(pdl_overlap() ? argmax_kernel<true> : argmax_kernel<false>, dim3(n), dim3(1024), 0, s, logits, V, out);
 }
 
 __global__ void f32_to_bf16_kernel(const float* in, bf16* out, uint64_t n) {
@@ -403,6 +402,9 @@ cudaError_t launch_f32_to_bf16(const float* in, bf16* out, uint64_t n, cudaStrea
 }  // namespace ppdk
 
 namespace ppdk {
+static int g_pdl_overlap = 0;  // measured: 2.5% slower decode step (tools/ab_step.py)
+int pdl_overlap() { return pdl_enabled() && g_pdl_overlap; }
+void set_pdl_overlap(int on) { g_pdl_overlap = on; }
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("PPD_PDL");

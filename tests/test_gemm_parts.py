@@ -34,3 +34,23 @@ def test_partition_rule_matches_bruteforce():
 def test_uniform_parts_all_valid():
     g = ppd.GemmParts(n=3, kbt=0, slots=148, rows=128, bn=256, n_tiles_t=1, total=1, stride=0)
     assert g.valid(5000, 17) == 3
+
+
+def test_hybrid_partition_whole_waves_then_stream_k():
+    """dp leading tiles are whole-K units (one slice); the tail follows the
+    stream-K rule over tail_slots ranges (gemm_tc.cu Sched)."""
+    rng = random.Random(1)
+    for _ in range(200):
+        slots = rng.randint(1, 80)
+        tiles = rng.randint(1, 300)
+        kbt = rng.randint(4, 70)
+        dp = (tiles // slots) * slots
+        if dp == tiles:
+            continue
+        tslots = rng.randint(1, min(slots, (tiles - dp) * kbt))
+        g = ppd.GemmParts(n=0, kbt=kbt, slots=tslots, rows=128, bn=256, n_tiles_t=1,
+                          total=(tiles - dp) * kbt, stride=0, dp=dp)
+        touching = brute(tiles - dp, kbt, tslots)
+        for t in range(tiles):
+            want = 1 if t < dp else len(touching[t - dp])
+            assert g.valid(t * 128, 0) == want

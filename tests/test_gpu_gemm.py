@@ -122,6 +122,8 @@ def sched_mode(request):
     (200, 300, 4096),     # ragged weight rows
     (328, 28672, 4096),   # decode + append chunk: 2 token sub-tiles per unit
     (456, 4096, 14336),   # 2 sub-tiles, long K
+    (2048, 4096, 14336),  # prefill: whole waves + stream-K tail
+    (1736, 4096, 4096),   # prefill: whole waves + stream-K tail, short K
 ])
 def test_gemm_parts_partition(gpu, sched_mode, M, N, K):
     """The fp32 path the forward step uses: only the slices GemmParts marks
