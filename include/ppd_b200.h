@@ -199,6 +199,12 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
  *   "attn_pf_ctas" K2 prefill CTA count (0 = cost model, default)
  *   "attn_pf_persist" 1 (default): pure prefill steps run a persistent
  *                  tcgen05 kernel over an atomic tile queue; 0: one CTA per tile
+ *   "layer_kernel" 0 (default): per-op kernels; 1: steps of <= 256 token
+ *                  rows on a GPU driven by one device handle run each layer
+ *                  after attention as ONE persistent launch (o, add+norm,
+ *                  gate|up, SiLU, down, add+norm, next qkv, RoPE/KV write)
+ *   "layer_l2_ahead" K8 weight k-blocks prefetched into L2 beyond the ring
+ *   "layer_stages" K8 smem ring depth cap (0 = as deep as fits)
  * Unknown names -> PPD_ERR_INVALID. Every change makes devices re-capture
  * their step graphs with the newly selected kernels. */
 int ppd_set_tuning(const char* name, int32_t value);

@@ -67,6 +67,18 @@ int g_mlp_fused = 2;
 // workspaces sized for two K-partial slices of a max-size step (see alloc_workspaces)
 bool g_ws_two_slices = true;
 constexpr int kMlpFusedMinRows = 512;
+// K8 decode layer kernel (layer_tc.cu) for steps of <= 256 token rows: tuning
+// "layer_kernel" (0 default = the per-op kernels, 1 = K8). Measured slower
+// than the per-op path at B = 16 / 64 / 200 (+24-45%, tools/ab_step.py,
+// tools/k8_trace.py), so it is an option, not the default.
+bool g_layer_kernel = false;
+int g_layer_l2_ahead = 16;  // tuning "layer_l2_ahead"
+int g_layer_stages = 0;     // tuning "layer_stages": ring depth cap (0 = as deep as fits)
+// ppd_devs open per GPU: the layer kernel's grid barrier needs every SM of the
+// GPU for its own CTAs, so it runs only on a GPU driven by ONE node (two
+// nodes' layer kernels launched concurrently could each hold part of the SMs
+// and wait on each other forever)
+std::atomic<int> g_open_on_gpu[64];
 
 struct Layer {
   bf16 *wqkv, *wo, *wgu, *wdown;
@@ -134,6 +146,7 @@ struct ppd_dev {
   // activations / workspaces
   bf16 *x = nullptr, *h = nullptr, *q = nullptr, *attn = nullptr, *m = nullptr, *hl = nullptr;
   float *qkv32 = nullptr, *proj32 = nullptr, *gu32 = nullptr, *down32 = nullptr, *logits = nullptr;
+  unsigned* layer_sync = nullptr;  // K8 grid-barrier counters [n_layers][8], zeroed per step
   float *ws_o = nullptr, *ws_ml = nullptr;
   int* counters = nullptr;
   int ws_slots = 0;
@@ -147,8 +160,9 @@ struct ppd_dev {
   int last_logit_rows = 0;
   // CUDA graphs of the forward pass, keyed by the step's shape (the metadata
   // contents change per step; the pointers and launch parameters do not)
-  std::map<std::tuple<int, int, int, int, int, int>, cudaGraphExec_t> graphs;
-  std::map<std::tuple<int, int, int, int, int, int>, int> shape_seen;
+  using GraphKey = std::tuple<int, int, int, int, int, long long, int>;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GraphKey, int> shape_seen;
   bool use_graphs = true;
   int tuning_epoch = 0;  // ppd_set_tuning generation the cached graphs were captured under
   // instrumentation
@@ -558,11 +572,18 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   return PPD_OK;
 }
 
+bool layer_kernel_ok(const ppd_dev* d, int T);
+
 void count_launches(ppd_dev* d, const StepLayout& L) {
   const long nl = d->cfg.n_layers;
-  // own kernels per layer: add_rmsnorm x2, rope_kv, attention, silu_mul; + embed, final norm, argmax
-  d->stats.own_launches += 5 * nl + 3;
-  d->stats.own_launches += 4 * nl + 1;  // tcgen05 GEMMs
+  if (layer_kernel_ok(d, L.T)) {
+    // embed, add_rmsnorm, qkv GEMM, rope_kv; per layer attention + K8; final norm, lm_head, argmax
+    d->stats.own_launches += 2 * nl + 7;
+  } else {
+    // own kernels per layer: add_rmsnorm x2, rope_kv, attention, silu_mul; + embed, final norm, argmax
+    d->stats.own_launches += 5 * nl + 3;
+    d->stats.own_launches += 4 * nl + 1;  // tcgen05 GEMMs
+  }
   d->stats.attn_launches += nl;
   d->stats.attn_bytes += L.attn_bytes * nl;
 }
@@ -585,6 +606,107 @@ int prof_mark(ppd_dev* d, int kind, bool end) {
     if (_rc) return _rc;                       \
   } while (0)
 
+// Device-side usability of the K8 decode layer kernel for a step of T rows.
+bool layer_kernel_ok(const ppd_dev* d, int T) {
+  const ppd_model_cfg& c = d->cfg;
+  if (!g_layer_kernel || T < 1 || T > 256 || T > 2 * device_sms()) return false;
+  if (g_open_on_gpu[d->gpu].load() != 1) return false;
+  if (c.d_model % 128 != 0 || c.d_model > 8192 || (2 * c.d_ff) % 128 != 0 || c.head_dim != 128) return false;
+  const int W = (c.n_q_heads + 2 * c.n_kv_heads) * c.head_dim;
+  const int max_sl = (int)std::min<size_t>(8, d->ws_rows / (size_t)T);
+  LayerJob j;
+  return layer_plan_job(j, d->proj32, T, c.d_model, c.n_q_heads * c.head_dim, device_sms(), max_sl) &&
+         layer_plan_job(j, d->gu32, T, 2 * c.d_ff, c.d_model, device_sms(), max_sl) &&
+         layer_plan_job(j, d->down32, T, c.d_model, c.d_ff, device_sms(), max_sl) &&
+         layer_plan_job(j, d->qkv32, T, W, c.d_model, device_sms(), max_sl);
+}
+
+// Steps of <= 256 rows: per layer ONE attention launch + ONE K8 layer kernel
+// (o -> add+norm -> gate|up -> SiLU -> down -> add+norm -> next qkv -> RoPE/KV).
+// Same rounding points as the per-op path; the K-partial slices follow the
+// grid-wide stream-K partition (deterministic slice order).
+int forward_layers(ppd_dev* d, const StepLayout& L, int max_sl) {
+  const ppd_model_cfg& c = d->cfg;
+  cudaStream_t s = d->compute;
+  const int Dh = c.head_dim, d_model = c.d_model, F = c.d_ff, T = L.T;
+  const int qd = c.n_q_heads * Dh, kd = c.n_kv_heads * Dh, W = qd + 2 * kd;
+  const int n_cta = device_sms();
+  uint8_t* m = d->d_meta;
+  const int* qstart = at<int>(m, L.off_qstart);
+  const int* ctx = at<int>(m, L.off_ctx);
+  const int* bt = at<int>(m, L.off_bt);
+  const int* rowseq = at<int>(m, L.off_rowseq);
+  const int* rowpos = at<int>(m, L.off_rowpos);
+  const int* outrows = at<int>(m, L.off_outrows);
+  const AttnItem* items = at<AttnItem>(m, L.off_items);
+  int bn = 0, stages = 0, stage_bytes = 0, smem = 0;
+  layer_shape(T, &bn, &stages, &stage_bytes, &smem);
+  if (g_layer_stages > 0 && g_layer_stages < stages) {
+    smem -= (stages - g_layer_stages) * stage_bytes;
+    stages = g_layer_stages;
+  }
+  CU(cudaMemsetAsync(d->layer_sync, 0, (size_t)c.n_layers * 8 * sizeof(unsigned), s));
+  // layer 0's qkv + RoPE/KV write through the per-op kernels
+  GemmParts np_qkv, none;
+  CU(launch_add_rmsnorm(d->x, nullptr, none, nullptr, d->ones, d->h, T, d_model, c.rms_eps, s));
+  PROF(1, false);
+  CU(gemm_run_split(d->h, d->layers[0].wqkv, d->qkv32, T, W, d_model, max_sl, &np_qkv, s));
+  PROF(1, true);
+  CU(launch_rope_kv_write(d->qkv32, np_qkv, d->layers[0].bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos,
+                          d->rope_sin, d->q, d->kv, T, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers, 0, d->bt, s));
+  LayerParams p{};
+  p.T = T;
+  p.bn = bn;
+  p.stages = stages;
+  p.stage_bytes = stage_bytes;
+  p.n_cta = n_cta;
+  p.l2_ahead = g_layer_l2_ahead;
+
+  p.x = d->x;
+  p.h = d->h;
+  p.m = d->m;
+  p.norm_w = d->ones;
+  p.eps = c.rms_eps;
+  p.d_model = d_model;
+  p.F = F;
+  auto job = [&](int j, const bf16* wgt, const bf16* act, float* out, int N, int K) -> int {
+    if (!layer_plan_job(p.job[j], out, T, N, K, n_cta, max_sl)) return fail(PPD_ERR_INVALID, "layer kernel plan");
+    if (!gemm_tc_map(p.map_w[j], wgt, N, K, 128) || !gemm_tc_map(p.map_x[j], act, T, K, bn))
+      return fail(PPD_ERR_CUDA, "cuTensorMapEncodeTiled failed (layer kernel)");
+    return PPD_OK;
+  };
+  for (int l = 0; l < c.n_layers; ++l) {
+    const Layer& w = d->layers[l];
+    PROF(0, false);
+    int rc = run_attention(c, d->kv_map, d->q, d->attn, qstart, ctx, bt, L.maxb, items, L.n_dec, L.n_items,
+                           at<int>(m, L.off_seg), L.n_cta, L.n_pf, l, d->ws_o, d->ws_ml, d->counters,
+                           d->counters + (size_t)d->max_S * c.n_kv_heads, s);
+    if (rc) return rc;
+    PROF(0, true);
+    const bool next = l + 1 < c.n_layers;
+    p.n_jobs = next ? 4 : 3;
+    p.sync = d->layer_sync + (size_t)l * 8;
+    if ((rc = job(0, w.wo, d->attn, d->proj32, d_model, qd)) || (rc = job(1, w.wgu, d->h, d->gu32, 2 * F, d_model)) ||
+        (rc = job(2, w.wdown, d->m, d->down32, d_model, F)))
+      return rc;
+    if (next) {
+      const Layer& wn = d->layers[l + 1];
+      if ((rc = job(3, wn.wqkv, d->h, d->qkv32, W, d_model))) return rc;
+      p.rope = RopeArgs{d->qkv32, p.job[3].parts, wn.bqkv, rowseq, rowpos, bt, L.maxb, d->rope_cos, d->rope_sin,
+                        d->q, d->kv, c.n_q_heads, c.n_kv_heads, Dh, c.n_layers, l + 1, d->bt};
+    }
+    PROF(1, false);
+    CU(launch_decode_layer(p, smem, s));
+    PROF(1, true);
+  }
+  count_launches(d, L);
+  GemmParts none2;
+  CU(launch_final_norm(d->x, nullptr, none2, nullptr, outrows, L.n_out, d->ones, d->hl, T, d_model, c.rms_eps, s));
+  CU(gemm_run(d->hl, d->lm_head, d->logits, L.n_out, c.vocab, d_model, true, s));
+  CU(launch_argmax(d->logits, L.n_out, c.vocab, d->d_tokens_out, s));
+  return PPD_OK;
+}
+
 // The forward pass of one step; metadata already staged in d->d_meta.
 int forward(ppd_dev* d, const StepLayout& L) {
   const ppd_model_cfg& c = d->cfg;
@@ -606,6 +728,7 @@ int forward(ppd_dev* d, const StepLayout& L) {
   GemmParts np_down;
 
   CU(launch_embed(tokens, d->embed, d->x, T, d_model, s));
+  if (layer_kernel_ok(d, T)) return forward_layers(d, L, max_sl);
   for (int l = 0; l < c.n_layers; ++l) {
     GemmParts np_qkv, np_o;
     const Layer& w = d->layers[l];
@@ -671,6 +794,7 @@ int alloc_workspaces(ppd_dev* d) {
   CU(cudaMalloc(&d->gu32, Tp * 2 * c.d_ff * 4));
   CU(cudaMalloc(&d->down32, Tp * c.d_model * 4));
   CU(cudaMalloc(&d->logits, S * c.vocab * 4));
+  CU(cudaMalloc(&d->layer_sync, (size_t)c.n_layers * 8 * sizeof(unsigned)));
   // split-merge counters [S][Hkv] + the K2 queue heads / done counter [4]
   CU(cudaMalloc(&d->counters, (S * c.n_kv_heads + 4) * 4));
   CU(cudaMemset(d->counters, 0, (S * c.n_kv_heads + 4) * 4));
@@ -720,7 +844,7 @@ void free_all(ppd_dev* d) {
     c = CopySlot{};
   }
   void* dev_ptrs[] = {d->kv, d->x, d->h, d->q, d->attn, d->m, d->hl, d->qkv32, d->proj32,
-                      d->gu32, d->down32, d->logits, d->ws_o, d->ws_ml, d->counters, d->d_meta,
+                      d->gu32, d->down32, d->logits, d->layer_sync, d->ws_o, d->ws_ml, d->counters, d->d_meta,
                       d->d_tokens_out, d->rope_cos, d->rope_sin};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
@@ -787,6 +911,7 @@ int ppd_dev_open(int32_t gpu, const ppd_model_cfg* cfg, int32_t max_step_tokens,
     return bail(fail(PPD_ERR_CUDA, "stream/event creation failed"));
   rc = alloc_workspaces(d);
   if (rc) return bail(rc);
+  g_open_on_gpu[gpu].fetch_add(1);
   *out = d;
   return PPD_OK;
 }
@@ -795,6 +920,7 @@ int ppd_dev_close(ppd_dev* d) {
   if (!d) return PPD_OK;
   cudaSetDevice(d->gpu);
   cudaDeviceSynchronize();
+  g_open_on_gpu[d->gpu].fetch_sub(1);
   free_all(d);
   delete d;
   return PPD_OK;
@@ -944,8 +1070,8 @@ int ppd_step_submit(ppd_dev* d, const ppd_batch* b) {
   CU(cudaEventRecord(d->ev0, d->compute));
   // repeated shapes replay a captured graph (decode steps: ~300 launches -> 1)
   // every launch parameter of forward() is a function of these (grids: items, n_dec, n_cta)
-  const auto key = std::make_tuple(L.n, L.T, L.maxb, L.n_out, L.n_items * 4096 + L.n_dec,
-                                   (L.n_ws * 8192 + L.n_cta) * 256 + L.n_pf);
+  const ppd_dev::GraphKey key{L.n, L.T, L.maxb, L.n_out, L.n_items * 4096 + L.n_dec,
+                             ((long long)L.n_ws * 8192 + L.n_cta) * 256 + L.n_pf, layer_kernel_ok(d, L.T) ? 1 : 0};
   if (d->tuning_epoch != g_tuning_epoch) {  // kernels chosen at capture time changed
     clear_graphs(d);
     d->tuning_epoch = g_tuning_epoch;
@@ -1357,6 +1483,15 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "gemm_l2_pre") == 0) {
     CHECK_ARG(value >= -1 && value <= 256, "gemm_l2_pre must be in [-1, 256]");
     gemm_tc_set_l2_pre(value);
+  } else if (std::strcmp(name, "layer_kernel") == 0) {
+    CHECK_ARG(value == 0 || value == 1, "layer_kernel must be 0 or 1");
+    g_layer_kernel = value != 0;
+  } else if (std::strcmp(name, "layer_l2_ahead") == 0) {
+    CHECK_ARG(value >= 0 && value <= 256, "layer_l2_ahead must be in [0, 256]");
+    g_layer_l2_ahead = value;
+  } else if (std::strcmp(name, "layer_stages") == 0) {
+    CHECK_ARG(value >= 0 && value <= 8, "layer_stages must be in [0, 8]");
+    g_layer_stages = value;
   } else if (std::strcmp(name, "mlp_fused") == 0) {
     CHECK_ARG(value >= 0 && value <= 2, "mlp_fused must be 0, 1 or 2");
     g_mlp_fused = value;

@@ -582,6 +582,11 @@ bool get_map(CUtensorMap* out, const void* ptr, int rows, int K, int box_rows) {
 }
 
 }  // namespace
+
+bool gemm_tc_map(void* map_out, const void* ptr, int rows, int K, int box_rows) {
+  return get_map(static_cast<CUtensorMap*>(map_out), ptr, rows, K, box_rows);
+}
+
 // Tuning knobs (ppd_set_tuning): pair = -1 auto / 0 single-CTA / 1 CTA pair;
 // stages = cap on the smem ring depth (0 = as many as fit); sched = -1 auto /
 // 0 uniform K split / 1 balanced partition.

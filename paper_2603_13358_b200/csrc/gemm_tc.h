@@ -81,6 +81,9 @@ void gemm_tc_set_occ2(int mode);
 // weight k-blocks each CTA prefetches into L2 (beyond its smem ring) while its
 // predecessor finishes: -1 auto, 0 off, n
 void gemm_tc_set_l2_pre(int n);
+// 2-D TMA map (128 B) of a K-major bf16 [rows][K] matrix, box = box_rows x 64 K
+// elements, 128 B swizzle (the layout every tcgen05 kernel here consumes)
+bool gemm_tc_map(void* map_out, const void* ptr, int rows, int K, int box_rows);
 // K-split count that fills the 148 SMs for this shape (1 when the tile grid already does)
 int gemm_tc_plan_splits(int T, int N, int K);
 

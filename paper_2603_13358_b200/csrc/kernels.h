@@ -65,6 +65,53 @@ cudaError_t launch_prefill_attention_persistent(const void* kv_map, const AttnPa
 // tcgen05/TMEM prefill tiles (kind 1 items of 128/G tokens)
 cudaError_t launch_prefill_attention_tc(const void* kv_map, const AttnParams& p, int n_items, cudaStream_t stream);
 
+// RoPE + paged KV write: everything one token row needs (ops_dev.cuh rope_kv_unit)
+struct RopeArgs {
+  const float* qkv;  // fp32 partial slices [T][qd + 2kd]
+  GemmParts parts;
+  const float* bias;
+  const int *row_seq, *row_pos, *block_tables;
+  int max_blocks;
+  const float *rope_cos, *rope_sin;
+  bf16 *q_out, *kv;
+  int Hq, Hkv, Dh, n_layers, layer, block_tokens;
+};
+
+// ---- K8 decode layer kernel (layer_tc.cu) ----
+// One persistent launch per layer for steps of <= 256 token rows: o-proj ->
+// residual add + RMSNorm -> gate|up -> SiLU -> down -> residual add + RMSNorm
+// -> the NEXT layer's qkv -> RoPE + KV write. Each GEMM ("job") is a stream-K
+// partition of its (weight tile, k-block) items over the CTAs; the glue
+// between jobs runs after a grid-wide counter barrier, while the TMA producer
+// keeps streaming the next job's weights (they do not depend on the glue).
+constexpr int kLayerMaxJobs = 4;
+struct LayerJob {
+  float* out;       // fp32 K-partial slices, slice j at out + j * parts.stride
+  int N, K, kbt;    // output columns, reduction length, 64-wide k-blocks per weight tile
+  long long total;  // weight tiles * kbt items
+  int ts;           // CTAs sharing the items: CTA c < ts owns [c*total/ts, (c+1)*total/ts)
+  GemmParts parts;  // slice rule the glue reads `out` with
+};
+struct LayerParams {
+  alignas(64) uint8_t map_w[kLayerMaxJobs][128];  // CUtensorMap of each job's weights
+  alignas(64) uint8_t map_x[kLayerMaxJobs][128];  // ... and of its activations
+  LayerJob job[kLayerMaxJobs];
+  int n_jobs, T, bn, stages, stage_bytes, n_cta;
+  int l2_ahead;    // weight k-blocks the producer prefetches into L2 beyond the ring while waiting
+  unsigned* sync;  // [n_jobs][2] epilogue-done / glue-done counters, zeroed per step
+  bf16 *x, *h, *m;
+  const bf16* norm_w;
+  float eps;
+  int d_model, F;
+  RopeArgs rope;  // the next layer's RoPE + KV write (job 3)
+};
+// grid-wide layout of a job for T token rows; false if its partial slices
+// would not fit `max_slices` workspace slices
+bool layer_plan_job(LayerJob& j, float* out, int T, int N, int K, int n_cta, int max_slices);
+// smem ring for T token rows (0 stages: T too large)
+void layer_shape(int T, int* bn, int* stages, int* stage_bytes, int* smem);
+cudaError_t launch_decode_layer(const LayerParams& p, int smem, cudaStream_t s);
+
 // ---- small fused ops (ops.cu) ----
 cudaError_t launch_fill_random(bf16* dst, uint64_t n, uint64_t seed, int tensor, int layer,
                                cudaStream_t s);

@@ -5,6 +5,7 @@
 // oracle/model_oracle.c exactly (IEEE _rn intrinsics, no contraction).
 #include "common.cuh"
 #include "kernels.h"
+#include "ops_dev.cuh"
 
 #include <cstdlib>
 
@@ -149,21 +150,7 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
     if (c < nc) {
       unpack8(reinterpret_cast<const uint4*>(x + row * d)[c], v[k]);
       if (df) {
-        float acc[8];
-        const float* base = df + row * d + (size_t)c * 8;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-        const int n_part = parts.valid(c * 8, (int)row);
-        for (int pp = 0; pp < n_part; ++pp) {
-          float4 a = reinterpret_cast<const float4*>(base + pp * parts.stride)[0];
-          float4 b = reinterpret_cast<const float4*>(base + pp * parts.stride)[1];
-          acc[0] = __fadd_rn(acc[0], a.x); acc[1] = __fadd_rn(acc[1], a.y);
-          acc[2] = __fadd_rn(acc[2], a.z); acc[3] = __fadd_rn(acc[3], a.w);
-          acc[4] = __fadd_rn(acc[4], b.x); acc[5] = __fadd_rn(acc[5], b.y);
-          acc[6] = __fadd_rn(acc[6], b.z); acc[7] = __fadd_rn(acc[7], b.w);
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[k][j] = rbf(__fadd_rn(v[k][j], rbf(acc[j])));
+        add_delta8<false>(v[k], df, parts.stride, parts.valid(c * 8, (int)row), row, d, c);
       } else if (db) {
         float dv[8];
         unpack8(reinterpret_cast<const uint4*>(db + row * d)[c], dv);
@@ -176,18 +163,12 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
     }
   }
   ss = block_sum<kNormThreads>(ss, red);
-  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), eps)));
+  const float inv = rms_inv(ss, d, eps);
   const size_t orow = rows ? (size_t)blockIdx.x : row;
 #pragma unroll
   for (int k = 0; k < kMaxChunks; ++k) {
     int c = threadIdx.x + k * kNormThreads;
-    if (c < nc) {
-      float wv[8], o[8];
-      unpack8(reinterpret_cast<const uint4*>(w)[c], wv);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = __fmul_rn(rbf(__fmul_rn(v[k][j], inv)), wv[j]);
-      reinterpret_cast<uint4*>(out + orow * d)[c] = pack8(o);
-    }
+    if (c < nc) reinterpret_cast<uint4*>(out + orow * d)[c] = norm8(v[k], inv, w, c);
   }
 }
 
@@ -210,83 +191,13 @@ cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, const GemmP
 // One CTA per token row. Each thread owns 4 consecutive rotary pairs (i..i+3,
 // i+64..i+67) of one q/k head, or 4 consecutive dims of one v head, and reads
 // the fp32 GEMM output (all K-split partial slices) with 16-byte loads.
-template <bool kRound = true>
-PPD_DEV float4 ld_sum4(const float* base, const GemmParts& parts, int tok, const float* bias, int col) {
-  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int n_part = parts.valid(col, tok);
-  for (int pp = 0; pp < n_part; ++pp) {
-    const float4 v = *reinterpret_cast<const float4*>(base + pp * parts.stride + col);
-    a.x = __fadd_rn(a.x, v.x);
-    a.y = __fadd_rn(a.y, v.y);
-    a.z = __fadd_rn(a.z, v.z);
-    a.w = __fadd_rn(a.w, v.w);
-  }
-  if (bias) {
-    const float4 b = *reinterpret_cast<const float4*>(bias + col);
-    a.x = __fadd_rn(a.x, b.x);
-    a.y = __fadd_rn(a.y, b.y);
-    a.z = __fadd_rn(a.z, b.z);
-    a.w = __fadd_rn(a.w, b.w);
-  }
-  if (!kRound) return a;
-  return make_float4(rbf(a.x), rbf(a.y), rbf(a.z), rbf(a.w));
-}
-
-PPD_DEV void st_bf16x4(bf16* dst, float a, float b, float c, float d) {
-  *reinterpret_cast<uint2*>(dst) = make_uint2(pack2(a, b), pack2(c, d));
-}
-
 template <bool kEarly>
-__global__ void rope_kv_kernel(const float* qkv, GemmParts parts, const float* bias,
-                               const int* row_seq, const int* row_pos, const int* block_tables,
-                               int max_blocks, const float* rope_cos, const float* rope_sin,
-                               bf16* q_out, bf16* kv, int Hq, int Hkv, int Dh, int n_layers,
-                               int layer, int BT) {
+__global__ void rope_kv_kernel(RopeArgs a, int T) {
   pdl_enter<kEarly>();
   const int r = blockIdx.x;
-  const int half = Dh / 2;
-  const int qd = Hq * Dh, kd = Hkv * Dh, W = qd + 2 * kd;
-  const int pos = row_pos[r], seq = row_seq[r];
-  const int blk = block_tables[(size_t)seq * max_blocks + pos / BT];
-  const int tok = pos % BT;
-  const float* cs = rope_cos + (size_t)pos * half;
-  const float* sn = rope_sin + (size_t)pos * half;
-  const float* row = qkv + (size_t)r * W;
-  const int per_head = half / 4;                 // rotary units per head
-  const int n_rot = (Hq + Hkv) * per_head;
-  const int n_v = kd / 4;
-  for (int u = blockIdx.y * blockDim.x + threadIdx.x; u < n_rot + n_v; u += gridDim.y * blockDim.x) {
-    if (u < n_rot) {
-      const int head = u / per_head, i = (u % per_head) * 4;
-      const int col = head * Dh + i;  // k heads follow q heads in the fused layout
-      const float4 x1 = ld_sum4(row, parts, r, bias, col);
-      const float4 x2 = ld_sum4(row, parts, r, bias, col + half);
-      const float4 c = *reinterpret_cast<const float4*>(cs + i);
-      const float4 sv = *reinterpret_cast<const float4*>(sn + i);
-      const float a0 = rbf(__fsub_rn(__fmul_rn(x1.x, c.x), __fmul_rn(x2.x, sv.x)));
-      const float a1 = rbf(__fsub_rn(__fmul_rn(x1.y, c.y), __fmul_rn(x2.y, sv.y)));
-      const float a2 = rbf(__fsub_rn(__fmul_rn(x1.z, c.z), __fmul_rn(x2.z, sv.z)));
-      const float a3 = rbf(__fsub_rn(__fmul_rn(x1.w, c.w), __fmul_rn(x2.w, sv.w)));
-      const float b0 = rbf(__fadd_rn(__fmul_rn(x2.x, c.x), __fmul_rn(x1.x, sv.x)));
-      const float b1 = rbf(__fadd_rn(__fmul_rn(x2.y, c.y), __fmul_rn(x1.y, sv.y)));
-      const float b2 = rbf(__fadd_rn(__fmul_rn(x2.z, c.z), __fmul_rn(x1.z, sv.z)));
-      const float b3 = rbf(__fadd_rn(__fmul_rn(x2.w, c.w), __fmul_rn(x1.w, sv.w)));
-      bf16* dst;
-      if (head < Hq) {
-        dst = q_out + ((size_t)r * Hq + head) * Dh;
-      } else {
-        dst = kv + ((((size_t)blk * n_layers + layer) * 2 + 0) * Hkv + (head - Hq)) * BT * Dh + (size_t)tok * Dh;
-      }
-      st_bf16x4(dst + i, a0, a1, a2, a3);
-      st_bf16x4(dst + i + half, b0, b1, b2, b3);
-    } else {
-      const int v = (u - n_rot) * 4;
-      const int hk = v / Dh, dd = v % Dh;
-      const float4 x = ld_sum4(row, parts, r, bias, qd + kd + v);
-      bf16* dst = kv + ((((size_t)blk * n_layers + layer) * 2 + 1) * Hkv + hk) * BT * Dh + (size_t)tok * Dh + dd;
-      st_bf16x4(dst, x.x, x.y, x.z, x.w);
-    }
-  }
+  const int n = rope_units_per_row(a);
+  for (int u = blockIdx.y * blockDim.x + threadIdx.x; u < n; u += gridDim.y * blockDim.x)
+    rope_kv_unit<false>(a, r, u, a.parts.valid(rope_unit_col(a, u), r));
 }
 
 cudaError_t launch_rope_kv_write(const float* qkv, const GemmParts& parts, const float* bias, const int* row_seq,
@@ -295,11 +206,10 @@ cudaError_t launch_rope_kv_write(const float* qkv, const GemmParts& parts, const
                                  bf16* kv_pool, int T, int Hq, int Hkv, int Dh, int n_layers,
                                  int layer, int block_tokens, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  const size_t W = (size_t)(Hq + 2 * Hkv) * Dh;
+  const RopeArgs a{qkv,     parts, bias, row_seq, row_pos, block_tables, max_blocks, rope_cos, rope_sin,
+                   q_out,   kv_pool, Hq,  Hkv,     Dh,      n_layers,     layer,      block_tokens};
   // (row, quarter of the row's rotary/v units): 4 CTAs per token row for memory parallelism
-  return launch_pdl(pdl_overlap() ? rope_kv_kernel<true> : rope_kv_kernel<false>, dim3(T, 4), dim3(128), 0, s, qkv, parts, bias, row_seq, row_pos,
-                    block_tables, max_blocks, rope_cos, rope_sin, q_out, kv_pool, Hq, Hkv, Dh, n_layers, layer,
-                    block_tokens);
+  return launch_pdl(pdl_overlap() ? rope_kv_kernel<true> : rope_kv_kernel<false>, dim3(T, 4), dim3(128), 0, s, a, T);
 }
 
 // ------------------------------------------------------------- SiLU * up
@@ -309,18 +219,8 @@ template <bool kEarly>
 __global__ void silu_mul_kernel(const float* gu, GemmParts parts, bf16* m, int F) {
   pdl_enter<kEarly>();
   const int r = blockIdx.y;
-  const float* row = gu + (size_t)r * 2 * F;
-  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4) {
-    const int grp = j >> 6, within = j & 63;
-    const float4 g = ld_sum4<false>(row, parts, r, nullptr, grp * 128 + within);
-    const float4 u = ld_sum4<false>(row, parts, r, nullptr, grp * 128 + 64 + within);
-    const float gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
-    float o[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e)  // fast exp/div: within 2 ulp of the oracle's fp32, rounded to bf16 next
-      o[e] = __fmul_rn(__fdividef(gv[e], __fadd_rn(1.0f, __expf(-gv[e]))), uv[e]);
-    st_bf16x4(m + (size_t)r * F + j, o[0], o[1], o[2], o[3]);
-  }
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4)
+    silu4<false>(gu, parts.stride, parts.valid((j >> 6) * 128, r), m, F, r, j);
 }
 cudaError_t launch_silu_mul(const float* gu, const GemmParts& parts, bf16* m, int T, int F, cudaStream_t s) {
   if (T == 0) return cudaSuccess;

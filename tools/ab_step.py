@@ -21,7 +21,8 @@ import numpy as np  # noqa: E402
 import paper_2603_13358_b200 as ppd  # noqa: E402
 
 DEFAULTS = {"gemm_pair": -1, "gemm_sched": -1, "gemm_stages": 0, "mlp_fused": 2, "attn_fused": 1,
-            "gemm_occ2": -1, "gemm_multi_sub": 1, "attn_pf_ctas": 0, "pdl_overlap": 0, "gemm_l2_pre": 0}
+            "gemm_occ2": -1, "gemm_multi_sub": 1, "attn_pf_ctas": 0, "pdl_overlap": 0, "gemm_l2_pre": 0,
+            "layer_kernel": 0, "layer_l2_ahead": 16, "layer_stages": 0}
 
 
 def parse(spec):
@@ -54,8 +55,8 @@ def main():
     cfgs = parse(os.environ.get("PPD_AB", "base:;nofuse:mlp_fused=0"))
     rounds = int(os.environ.get("PPD_AB_ROUNDS", "8"))
     steps = int(os.environ.get("PPD_AB_STEPS", "4"))
-    B, ctx0, BT = 200, 1024, 16
-    cfg = ppd.llama8b_cfg()
+    B, ctx0, BT = int(os.environ.get("PPD_AB_B", "200")), int(os.environ.get("PPD_AB_CTX", "1024")), 16
+    cfg = ppd.qwen32b_cfg() if os.environ.get("PPD_AB_MODEL") == "qwen32b" else ppd.llama8b_cfg()
     max_ctx = ctx0 + rounds * len(cfgs) * (steps + 2) + 16
     bps = (max_ctx + BT - 1) // BT
     mix = [tuple(int(x) for x in it.split(":")) for it in filter(None, os.environ.get("PPD_AB_MIX", "").split(","))]
