@@ -362,6 +362,25 @@ int plan_mixed_split(double dec_bytes, const std::vector<double>& tile_cost, int
 }
 
 bool g_attn_fused = true;  // tuning "attn_fused": K2 one-launch mixed attention
+
+// K2 pays when the step's prefill tiles fit under its decode rows' K/V
+// streaming (the decode-append mix of a large decode batch: B=200 + a
+// 128-token append 12.7 vs 13.4 ms); when the prefill dominates (a turn-2+
+// append of 1536 tokens beside a handful of decode rows, the PPD D node at
+// low load) the persistent tcgen05 prefill kernel on all SMs after the
+// decode kernel is faster (B=9 + 1536 over 2048: 31 vs 40 ms per step).
+// Estimates: decode at 5.6 TB/s; prefill causal FLOPs at 0.7 PFLOP/s.
+bool mixed_step_fits_k2(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_heads, int G,
+                        const std::vector<AttnItem>& items, int n_dec) {
+  double dec_bytes = 0, pf_flop = 0;
+  for (int s = 0; s < n; ++s)
+    if (q_len[s] == 1) dec_bytes += (double)(ctx[s] + 1) * n_kv_heads * 2 * 128 * 2;
+  for (size_t i = n_dec; i < items.size(); ++i) {
+    const AttnItem& it = items[i];
+    pf_flop += 4.0 * it.n_q * G * (ctx[it.seq] + it.q_tok0 + it.n_q) * 128.0 * n_kv_heads;
+  }
+  return pf_flop / 0.7e15 <= dec_bytes / 5.6e12;
+}
 int g_attn_pf_ctas = 0;          // tuning "attn_pf_ctas": force the K2 prefill CTA count (0 = cost model)
 bool g_attn_pf_persist = true;  // tuning "attn_pf_persist": persistent tile queue for pure prefill steps
 
@@ -380,11 +399,15 @@ void plan_attention(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_he
       return ctx[a.seq] + a.q_tok0 + a.n_q > ctx[b.seq] + b.q_tok0 + b.n_q;
     });
   }
-  if (attention_tc_enabled() && g_attn_fused && n_dec > 0 && (int)items.size() > n_dec) {
-    // longest prefill tiles first (round-robin dealing in mixed_attention_kernel)
+  if (attention_tc_enabled() && n_dec > 0 && (int)items.size() > n_dec) {
+    // longest prefill tiles first: the tile queues (K2 and the persistent
+    // prefill kernel) hand them out in this order
     std::stable_sort(items.begin() + n_dec, items.end(), [&](const AttnItem& a, const AttnItem& b) {
       return ctx[a.seq] + a.q_tok0 + a.n_q > ctx[b.seq] + b.q_tok0 + b.n_q;
     });
+  }
+  if (attention_tc_enabled() && g_attn_fused && n_dec > 0 && (int)items.size() > n_dec &&
+      mixed_step_fits_k2(n, q_len, ctx, n_kv_heads, G, items, n_dec)) {
     std::vector<double> cost;
     for (size_t i = n_dec; i < items.size(); ++i) {
       const AttnItem& it = items[i];
@@ -558,8 +581,8 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   if (n_items > n_dec) {
     if (attention_tc_enabled()) {
       p.items = d_items + n_dec;
-      if (n_dec == 0 && g_attn_pf_persist)
-        CU(launch_prefill_attention_persistent(kv_map, p, d_items, n_items, s));
+      if (g_attn_pf_persist)  // after the decode kernel on a mixed step that does not fit K2
+        CU(launch_prefill_attention_persistent(kv_map, p, d_items + n_dec, n_items - n_dec, s));
       else
         CU(launch_prefill_attention_tc(kv_map, p, n_items - n_dec, s));
     } else if (n_cta > 0) {

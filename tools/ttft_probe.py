@@ -24,7 +24,7 @@ def main():
         recs = E.records(r)
         t2 = sorted([(rc["arrival"], rc["turn_index"], (rc["first_token"] - rc["arrival"]) * 1e3)
                      for rc in recs if rc["turn_index"] >= 2 and rc.get("first_token") is not None])
-        steps = [s for s in r.get("step_log", []) if not s.get("copy")]
+        steps = [s for s in r.get("device", {}).get("step_log", []) if not s.get("copy")]
         big = [(s["node"], sum(q for q in s["q_len"] if q > 1), len(s["q_len"]), round(s["ms"], 2)) for s in steps
                if max(s["q_len"]) > 1]
         dec = [s["ms"] for s in steps if max(s["q_len"]) == 1]
