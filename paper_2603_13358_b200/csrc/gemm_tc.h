@@ -30,6 +30,11 @@ struct GemmParts {
   int dp = 0;           // leading whole-K (data-parallel) tiles
 
   __host__ __device__ __forceinline__ int owner(long long x) const {
+    // 32-bit division when the product fits (every shape this library plans:
+    // tiles * k-blocks * slots < 2^31); the consumers call this per element
+    // group, where a 64-bit division made the small ops instruction-bound
+    if ((total + 1) * (long long)slots < (1LL << 31))
+      return (int)(((unsigned)(x + 1) * (unsigned)slots + (unsigned)total - 1u) / (unsigned)total) - 1;
     return (int)(((x + 1) * slots + total - 1) / total) - 1;
   }
   // valid slices for output column `col` of token row `tok`
