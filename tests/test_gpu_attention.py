@@ -77,8 +77,17 @@ def test_append_prefill(gpu):
     run_case(cfg_of(32, 8), [17, 64], [1000, 1], seed=4)
 
 
-def test_mixed_decode_and_append_one_launch(gpu):
+def test_mixed_decode_and_append(gpu):
+    # prefill work exceeds the decode rows' K/V streaming: the decode kernel
+    # then the persistent tcgen05 prefill queue (device.cu mixed_step_fits_k2)
     run_case(cfg_of(32, 8), [1, 1, 50, 1, 130], [700, 3, 400, 64, 0], seed=5)
+
+
+def test_mixed_small_decode_large_append(gpu):
+    """The PPD D node's shape at low load: a few decode rows beside a long
+    append over a long cached context (split path), Llama and Qwen groups."""
+    run_case(cfg_of(32, 8), [1, 1, 1, 300], [2100, 40, 900, 1700], seed=10)
+    run_case(cfg_of(40, 8), [1, 1, 260], [700, 3000, 1200], seed=11)
 
 
 def test_qwen_group_of_5(gpu):
