@@ -15,6 +15,7 @@
 #include "ppd/costmodel.hpp"
 #include "ppd/engine.hpp"
 #include "ppd/gateway.hpp"
+#include "ppd/kvcache.hpp"
 #include "ppd/md5.hpp"
 #include "ppd/metrics.hpp"
 #include "ppd/routing.hpp"
@@ -459,6 +460,37 @@ std::string op_gateway_tcp(const json& job) {
   return out.dump();
 }
 
+// The KV manager alone (ppd::kv::BlockPool): a script of ensure / set_tokens /
+// release operations; replies each table after each op (exact block ids).
+std::string op_kv_pool_script(const json& job) {
+  kv::BlockPool pool(job.at("num_blocks").get<int>(), job.value("block_tokens", 16));
+  json out = json::array();
+  for (const json& it : job.at("script")) {
+    const std::string what = it.at("do").get<std::string>();
+    const int conv = it.at("conv").get<int>();
+    json r = {{"do", what}, {"conv", conv}};
+    try {
+      if (what == "ensure") {
+        pool.ensure(conv, it.at("tokens").get<long>());
+      } else if (what == "set_tokens") {
+        pool.set_tokens(conv, it.at("tokens").get<long>());
+      } else if (what == "release") {
+        pool.release(conv);
+      } else {
+        throw std::invalid_argument("kv_pool_script: unknown op " + what);
+      }
+    } catch (const std::runtime_error& e) {
+      r["error"] = e.what();
+    }
+    const kv::BlockTable* t = pool.find(conv);
+    r["blocks"] = t ? json(t->blocks) : json::array();
+    r["tokens"] = pool.tokens(conv);
+    r["free_blocks"] = pool.free_blocks();
+    out.push_back(r);
+  }
+  return out.dump();
+}
+
 std::string run(const std::string& text) {
   const json job = json::parse(text);
   const std::string op = job.value("op", std::string("simulate"));
@@ -472,6 +504,7 @@ std::string run(const std::string& text) {
   if (op == "ingest_trace") return op_ingest_trace(job);
   if (op == "gateway") return op_gateway(job);
   if (op == "gateway_tcp") return op_gateway_tcp(job);
+  if (op == "kv_pool_script") return op_kv_pool_script(job);
   auto calib = std::make_shared<const cost::CalibrationTable>(calib_from(job));
   sim::ClusterConfig cfg = sim::ClusterConfig::from_name(job.at("cluster").get<std::string>(), policy_from(job), calib);
   if (job.contains("max_decode_batch")) cfg.max_decode_batch = job["max_decode_batch"].get<int>();

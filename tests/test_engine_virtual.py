@@ -4,6 +4,8 @@ makespan, prefill waits, node busy times and the calibration hash, on every
 golden case generated from the unmodified reference (tests/golden/). The KV
 manager's block tables are checked against an independent restatement."""
 import json
+
+import numpy as np
 import os
 
 import pytest
@@ -131,3 +133,78 @@ def test_device_fit_recovers_exact_coefficients():
     from oracle import oracle as O
     ref = O.ref_tool({"op": "calib", "calib_json": json.dumps(fit)})
     assert ref["hash"] == E.run({"op": "fit_calibration", "samples": s})["hash"]
+
+
+class _PoolRestatement:
+    """Python restatement of the KV manager's allocator (kvcache.hpp): ids
+    never handed out are taken in order; released ids are reused lowest first."""
+
+    def __init__(self, n, bt=16):
+        self.n, self.bt, self.fresh, self.returned, self.tables, self.tok = n, bt, 0, set(), {}, {}
+
+    def take(self):
+        if self.returned:
+            b = min(self.returned)
+            self.returned.remove(b)
+            return b
+        if self.fresh >= self.n:
+            raise RuntimeError("exhausted")
+        self.fresh += 1
+        return self.fresh - 1
+
+    def ensure(self, conv, tokens):
+        t = self.tables.setdefault(conv, [])
+        while len(t) < (tokens + self.bt - 1) // self.bt:
+            t.append(self.take())
+
+    def do(self, op):
+        c = op["conv"]
+        err = None
+        try:
+            if op["do"] == "ensure":
+                self.ensure(c, op["tokens"])
+            elif op["do"] == "set_tokens":
+                self.ensure(c, op["tokens"])
+                self.tok[c] = op["tokens"]
+            else:
+                self.returned.update(self.tables.pop(c, []))
+                self.tok.pop(c, None)
+        except RuntimeError:
+            err = True
+        free = self.n - self.fresh + len(self.returned)
+        return self.tables.get(c, []), self.tok.get(c, 0), free, err
+
+
+def test_kv_block_pool_exact_with_release_and_reuse():
+    """The KV manager's exact block ids under growth, release, reuse and
+    exhaustion (row a4), against the restatement: conversations grow by
+    prefill / append / decode, finish (release) and new ones reuse the
+    lowest freed ids; a request past capacity raises "KV pool exhausted" (the
+    blocks it took before running out stay with it, identically in both; the
+    engine's admission control checks blocks_needed first and never issues one)."""
+    rng = np.random.default_rng(11)
+    script, live = [], {}
+    for step in range(400):
+        r = rng.random()
+        if live and r < 0.2:
+            c = int(rng.choice(list(live)))
+            script.append({"do": "release", "conv": c})
+            live.pop(c)
+        else:
+            c = int(rng.integers(0, 40))
+            n = live.get(c, 0) + int(rng.choice([1, 1, 1, 7, 16, 33, 200]))
+            live[c] = n
+            script.append({"do": "set_tokens" if rng.random() < 0.7 else "ensure", "conv": c, "tokens": n})
+    got = E.run({"op": "kv_pool_script", "num_blocks": 300, "script": script})
+    ref = _PoolRestatement(300)
+    errors = 0
+    for op, g in zip(script, got):
+        blocks, tokens, free, err = ref.do(op)
+        assert g["blocks"] == blocks, (op, g, blocks)
+        assert g["free_blocks"] == free
+        assert ("error" in g) == bool(err)
+        errors += bool(err)
+        if op["do"] == "set_tokens" and not err:
+            assert g["tokens"] == tokens
+    assert errors > 0  # the script reaches exhaustion at least once
+    assert any(op["do"] == "release" for op in script)
