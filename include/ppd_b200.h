@@ -195,7 +195,10 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
  *   "gemm_occ2"    -1 auto (<= 128 token rows), 0 off, 1 on: two co-resident
  *                  CTAs per SM with half-depth rings
  *   "attn_fused"   1 (default): a mixed decode + prefill step runs its
- *                  attention as ONE launch (K2); 0: decode and prefill launches
+ *                  attention as ONE launch (K2) when its prefill tiles fit
+ *                  under the decode rows' K/V streaming, else the decode
+ *                  kernel then the persistent prefill queue; 2: K2 for every
+ *                  mixed step; 0: never K2
  *   "attn_pf_ctas" K2 prefill CTA count (0 = cost model, default)
  *   "attn_pf_persist" 1 (default): pure prefill steps run a persistent
  *                  tcgen05 kernel over an atomic tile queue; 0: one CTA per tile

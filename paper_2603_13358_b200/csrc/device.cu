@@ -361,7 +361,10 @@ int plan_mixed_split(double dec_bytes, const std::vector<double>& tile_cost, int
   return best;
 }
 
-bool g_attn_fused = true;  // tuning "attn_fused": K2 one-launch mixed attention
+// tuning "attn_fused": 1 (default) K2 one-launch mixed attention when the
+// prefill fits under the decode (mixed_step_fits_k2), 2 K2 for every mixed
+// step (A/B), 0 never
+int g_attn_fused = 1;
 
 // K2 pays when the step's prefill tiles fit under its decode rows' K/V
 // streaming (the decode-append mix of a large decode batch: B=200 + a
@@ -407,7 +410,7 @@ void plan_attention(int n, const int32_t* q_len, const int32_t* ctx, int n_kv_he
     });
   }
   if (attention_tc_enabled() && g_attn_fused && n_dec > 0 && (int)items.size() > n_dec &&
-      mixed_step_fits_k2(n, q_len, ctx, n_kv_heads, G, items, n_dec)) {
+      (g_attn_fused == 2 || mixed_step_fits_k2(n, q_len, ctx, n_kv_heads, G, items, n_dec))) {
     std::vector<double> cost;
     for (size_t i = n_dec; i < items.size(); ++i) {
       const AttnItem& it = items[i];
@@ -1486,8 +1489,8 @@ int ppd_set_tuning(const char* name, int32_t value) {
     CHECK_ARG(value == 0 || value == 1, "attn_pf_persist must be 0 or 1");
     g_attn_pf_persist = value != 0;
   } else if (std::strcmp(name, "attn_fused") == 0) {
-    CHECK_ARG(value == 0 || value == 1, "attn_fused must be 0 or 1");
-    g_attn_fused = value != 0;
+    CHECK_ARG(value >= 0 && value <= 2, "attn_fused must be 0, 1 or 2");
+    g_attn_fused = value;
   } else if (std::strcmp(name, "gemm_occ2") == 0) {
     CHECK_ARG(value >= -1 && value <= 1, "gemm_occ2 must be -1, 0 or 1");
     gemm_tc_set_occ2(value);
