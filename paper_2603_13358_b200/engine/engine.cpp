@@ -687,7 +687,11 @@ class DeviceCluster {
     if (opt_.record_steps) {
       n.log_idx = step_log_.size();
       step_log_.push_back({{"node", ni}, {"q_len", q_len}, {"ctx", ctx}, {"tokens", toks}, {"block_tables", bt},
-                           {"max_blocks", maxb}, {"want", want}});
+                           {"max_blocks", maxb}, {"want", want}, {"t_start", now_}});
+      if (n.chunk > 0) {  // the prefill chunk's request: when it arrived, which turn
+        const Req& r = reqs_[n.job.req];
+        step_log_.back()["chunk_req"] = {{"arrival", r.arrival}, {"turn", r.turn}, {"final", n.chunk_final}};
+      }
     }
     if (opt_.realtime) {
       ++inflight_steps_;

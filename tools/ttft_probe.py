@@ -28,6 +28,11 @@ def main():
         big = [(s["node"], sum(q for q in s["q_len"] if q > 1), len(s["q_len"]), round(s["ms"], 2)) for s in steps
                if max(s["q_len"]) > 1]
         dec = [s["ms"] for s in steps if max(s["q_len"]) == 1]
+        # per final prefill chunk on a D node: queue wait (step start - arrival) and the step itself
+        waits = [(s["chunk_req"]["turn"], round((s["t_start"] - s["chunk_req"]["arrival"]) * 1e3, 2), round(s["ms"], 2),
+                  len(s["q_len"]) - 1)
+                 for s in steps if s.get("chunk_req") and s["chunk_req"]["final"] and s["chunk_req"]["turn"] >= 2]
+        print(json.dumps({"x": x, "turn2plus_final_chunks(turn,wait_ms,step_ms,decode_rows)": waits[:60]}))
         print(json.dumps({"x": x, "ttft_ms": [round(t[2], 1) for t in t2], "turns": [t[1] for t in t2],
                           "p50": float(np.median([t[2] for t in t2])),
                           "decode_step_ms_p50": float(np.median(dec)) if dec else None,
