@@ -107,7 +107,9 @@ struct DevCloser {
 };
 using DevPtr = std::unique_ptr<ppd_dev, DevCloser>;
 
-enum class Ev { issue, iter_done, transfer_done, timeout };
+// kick: a node picks its next iteration only after every event of the current
+// instant (see iter_done)
+enum class Ev { issue, iter_done, transfer_done, timeout, kick };
 struct Event {
   double t;
   std::uint64_t seq;
@@ -427,6 +429,7 @@ class DeviceCluster {
       case Ev::iter_done: iter_done(e.a); break;
       case Ev::transfer_done: transfer_done(e.a); break;
       case Ev::timeout: timeout(e.a); break;
+      case Ev::kick: start_iter(e.a); break;
     }
   }
 
@@ -805,7 +808,13 @@ class DeviceCluster {
                                   }) == n.rows.end())
         still.push_back(rid);
     n.running = std::move(still);
-    start_iter(ni);
+    // The next iteration is assembled after every event of this instant has
+    // been handled: the next turn of a conversation that completed in this
+    // step (issued at now + think, think 0 in the configs' traces) joins it
+    // instead of waiting a whole step behind it. With the reference's separate
+    // prefill lane (simulator.cpp:319-339) such an append starts at once; in
+    // the fused step it can only start at an iteration boundary, this one.
+    push(now_, Ev::kick, ni);
   }
 
   // token 1 exists (sampled from the prefill's last row): the request is live on its decode node
