@@ -98,6 +98,23 @@ PPD_DEV float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
+// explicit shared-state-space accesses: the smem carve-up goes through
+// generic pointers, for which the compiler emits generic LD.E / ST.E; the
+// per-block max exchange sits on the softmax critical path, so use LDS / STS
+PPD_DEV void sts_f32(const void* p, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
+}
+PPD_DEV float lds_f32(const void* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+PPD_DEV void sts_u128(void* p, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
 // shared-memory carve-up of one prefill CTA (smem 1024-byte aligned)
 struct Smem {
   uint8_t *q_s, *k_s, *v_s, *p_s;
@@ -312,7 +329,7 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
 #pragma unroll
       for (int c = (16 / NH) * h; c < (16 / NH) * (h + 1); ++c) {
         const uint4 v = src ? src[c] : make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(q_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v;
+        sts_u128(q_s + (c >> 3) * (kTile / 2) + r * 128 + (((c & 7) ^ (r & 7)) << 4), v);
       }
       fence_proxy_async();
       __syncwarp();
@@ -363,11 +380,11 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
       float mx;
       if constexpr (kXchgSmem) {
         float* slot = S.xchg + ((j & 1) * 128 + r) * NH;
-        slot[h] = mh;
+        sts_f32(slot + h, mh);
         named_barrier_sync(pair_bar, 32 * NH);
-        mx = slot[0];
+        mx = lds_f32(slot);
 #pragma unroll
-        for (int i = 1; i < NH; ++i) mx = fmaxf(mx, slot[i]);  // identical in every part
+        for (int i = 1; i < NH; ++i) mx = fmaxf(mx, lds_f32(slot + i));  // identical in every part
       } else {
         uint32_t v = __float_as_uint(mh);
         asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(
@@ -471,11 +488,11 @@ PPD_DEV void tile(const CUtensorMap* kv_map, const AttnParams& p, const Smem& S,
     float lsum;
     if constexpr (kXchgSmem) {
       float* slot = S.xchg + (2 * 128 + r) * NH;
-      slot[h] = l;
+      sts_f32(slot + h, l);
       named_barrier_sync(pair_bar, 32 * NH);
-      lsum = slot[0];
+      lsum = lds_f32(slot);
 #pragma unroll
-      for (int i = 1; i < NH; ++i) lsum += slot[i];  // same order in every part
+      for (int i = 1; i < NH; ++i) lsum += lds_f32(slot + i);  // same order in every part
     } else {
       uint32_t v = __float_as_uint(l);
       asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + lane_base + kXchgCol + 2 * NH + h),

@@ -459,9 +459,11 @@ __global__ void __launch_bounds__(kThreads, kOcc)
           uint32_t r[32];
           tmem_ld32(t_acc + (uint32_t)c0, r);
           float* xb = xchg + buf * 2048;
-          if (q >= 2) {
+          if (q >= 2) {  // explicit st.shared (a generic store through xchg would be ST.E)
+            const uint32_t xa = smem_u32(xb + (q - 2) * 1024 + lane);
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) xb[(q - 2) * 1024 + jj * 32 + lane] = __uint_as_float(r[jj]);
+            for (int jj = 0; jj < 32; ++jj)
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(xa + 128u * jj), "r"(r[jj]) : "memory");
           }
           named_barrier_sync(1, 128);
           if (q < 2 && grp * kBM < p.N) {
@@ -471,7 +473,8 @@ __global__ void __launch_bounds__(kThreads, kOcc)
             for (int jj = 0; jj < 32; ++jj) {
               if (jj < nj) {
                 const float g = __uint_as_float(r[jj]);
-                const float u = xb[q * 1024 + jj * 32 + lane];
+                float u;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(u) : "r"(smem_u32(xb + q * 1024 + jj * 32 + lane)) : "memory");
                 dst[(size_t)jj * p.ldo] = __float2bfloat16_rn(__fmul_rn(__fdividef(g, __fadd_rn(1.0f, __expf(-g))), u));
               }
             }
