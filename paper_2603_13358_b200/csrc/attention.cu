@@ -593,26 +593,20 @@ PPD_DEV void decode_body(const CUtensorMap* kv_map, const AttnParams& p, uint8_t
     if (g8 < G) {
       float* ow = mo + (warp * kDecMaxG + g8) * kDh;
 #pragma unroll
-      for (int nt = 0; nt < 16; ++nt) {
-        ow[nt * 8 + 2 * t] = o[nt][0];
-        ow[nt * 8 + 2 * t + 1] = o[nt][1];
-      }
-      if (t == 0) {
-        mml[(warp * kDecMaxG + g8) * 2 + 0] = m0;
-        mml[(warp * kDecMaxG + g8) * 2 + 1] = l0;
-      }
+      for (int nt = 0; nt < 16; ++nt) sts_f32x2(ow + nt * 8 + 2 * t, o[nt][0], o[nt][1]);
+      if (t == 0) sts_f32x2(mml + (warp * kDecMaxG + g8) * 2, m0, l0);
     }
     named_barrier_sync(bar_cons, kConsumerWarps * 32);
     const bool split = it.n_splits > 1;
     for (int r = 0; r < G; ++r) {
       float mm = -INFINITY;
-      for (int w = 0; w < kConsumerWarps; ++w) mm = fmaxf(mm, mml[(w * kDecMaxG + r) * 2]);
+      for (int w = 0; w < kConsumerWarps; ++w) mm = fmaxf(mm, lds_f32(mml + (w * kDecMaxG + r) * 2));
       const float base = mm == -INFINITY ? 0.f : mm;
       float ll = 0.f, acc = 0.f;
       for (int w = 0; w < kConsumerWarps; ++w) {
-        const float f = exp2f(mml[(w * kDecMaxG + r) * 2] - base);
-        ll += mml[(w * kDecMaxG + r) * 2 + 1] * f;
-        acc += mo[(w * kDecMaxG + r) * kDh + tid] * f;
+        const float f = exp2f(lds_f32(mml + (w * kDecMaxG + r) * 2) - base);
+        ll += lds_f32(mml + (w * kDecMaxG + r) * 2 + 1) * f;
+        acc += lds_f32(mo + (w * kDecMaxG + r) * kDh + tid) * f;
       }
       if (!split) {
         p.out[((size_t)q_base * p.n_q_heads + kvh * G + r) * kDh + tid] = f2bf(acc / ll);

@@ -98,23 +98,6 @@ PPD_DEV float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-// explicit shared-state-space accesses: the smem carve-up goes through
-// generic pointers, for which the compiler emits generic LD.E / ST.E; the
-// per-block max exchange sits on the softmax critical path, so use LDS / STS
-PPD_DEV void sts_f32(const void* p, float v) {
-  asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
-}
-PPD_DEV float lds_f32(const void* p) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-PPD_DEV void sts_u128(void* p, const uint4& v) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
-               : "memory");
-}
-
 // shared-memory carve-up of one prefill CTA (smem 1024-byte aligned)
 struct Smem {
   uint8_t *q_s, *k_s, *v_s, *p_s;

@@ -128,6 +128,26 @@ PPD_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint
       : "memory");
 }
 
+// explicit shared-state-space accesses: shared buffers carved out of the
+// dynamic smem go through generic pointers, for which the compiler emits
+// generic LD.E / ST.E (slower than LDS / STS on the same smem)
+PPD_DEV void sts_f32(const void* p, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(smem_u32(p)), "f"(v) : "memory");
+}
+PPD_DEV void sts_f32x2(const void* p, float a, float b) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(smem_u32(p)), "f"(a), "f"(b) : "memory");
+}
+PPD_DEV float lds_f32(const void* p) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+PPD_DEV void sts_u128(void* p, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
 PPD_DEV void named_barrier_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
