@@ -135,7 +135,7 @@ cudaError_t launch_embed(const int* tokens, const bf16* embed, bf16* x, int T, i
 // --------------------------------------------------- residual add + RMSNorm
 // v = x (+ rbf(sum of delta partials) | + delta_bf16); x <- v ; out = rbf(rbf(v) * inv_rms) * w
 template <bool kWriteX, bool kEarly>
-__global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
+__global__ void __launch_bounds__(kNormThreads, 2) add_rmsnorm_kernel(
     bf16* x, const float* df, GemmParts parts, const bf16* db, const bf16* w,
     bf16* out, const int* rows, int d, float eps) {
   __shared__ float red[33];
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kNormThreads) add_rmsnorm_kernel(
     if (c < nc) {
       unpack8(reinterpret_cast<const uint4*>(x + row * d)[c], v[k]);
       if (df) {
-        add_delta8<false>(v[k], df, parts.stride, parts.valid(c * 8, (int)row), row, d, c);
+        add_delta8<false, kMaxSlices>(v[k], df, parts.stride, parts.valid(c * 8, (int)row), row, d, c);
       } else if (db) {
         float dv[8];
         unpack8(reinterpret_cast<const uint4*>(db + row * d)[c], dv);
@@ -197,7 +197,7 @@ __global__ void rope_kv_kernel(RopeArgs a, int T) {
   const int r = blockIdx.x;
   const int n = rope_units_per_row(a);
   for (int u = blockIdx.y * blockDim.x + threadIdx.x; u < n; u += gridDim.y * blockDim.x)
-    rope_kv_unit<false>(a, r, u, a.parts.valid(rope_unit_col(a, u), r));
+    rope_kv_unit<false, 4>(a, r, u, a.parts.valid(rope_unit_col(a, u), r));
 }
 
 cudaError_t launch_rope_kv_write(const float* qkv, const GemmParts& parts, const float* bias, const int* row_seq,
