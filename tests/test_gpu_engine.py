@@ -280,3 +280,21 @@ def test_phase1_table_on_device_then_dynamic_routing(gpu):
     recs = E.records(r)
     assert recs and all(v["status"] == "completed" for v in recs)
     assert sum(r["route_decisions"]) == sum(1 for v in recs if v["route"] == "D_local")
+
+
+def test_next_turn_joins_the_next_iteration(gpu):
+    """Iteration boundary (engine.cpp iter_done -> Ev::kick): a conversation's
+    next turn, issued at the instant its predecessor completes (think time 0),
+    rides in the very next step of its decode node instead of waiting one
+    step behind it: every D-local append's final chunk starts at its arrival
+    whenever the node was not already busy with another prefill chunk."""
+    wl = {"id": "kick", "turn1": [48, 12], "turn2plus": [40, 12], "num_turns": 3, "qps": 4.0, "duration_s": 2.0}
+    job = {"cluster": "1P_1D", "x": 1.0, "clock": "device", "seed": 5, "workload": wl,
+           "device": {"model": "tiny", "weight_seed": 3, "token_seed": 4, "gpus": [0, 0], "kv_blocks_per_node": 0,
+                      "prefill_chunk": 64, "record_tokens": False, "record_steps": True}}
+    r = E.run(job)
+    steps = [st for st in r["device"]["step_log"] if not st.get("copy")]
+    appends = [st for st in steps if st.get("chunk_req") and st["chunk_req"]["turn"] >= 2 and st["chunk_req"]["final"]]
+    assert len(appends) >= 5
+    waits = [st["t_start"] - st["chunk_req"]["arrival"] for st in appends]
+    assert sum(w < 1e-9 for w in waits) >= 0.8 * len(waits), waits
