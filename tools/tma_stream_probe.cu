@@ -13,6 +13,9 @@
 //      4 x K=16, fp32 accumulator in TMEM; the stage is released by
 //      tcgen05.commit): the decode GEMM's main loop without its epilogue
 //   G  F with N=104
+//   H  F + the epilogue of one 128 x 208 fp32 accumulator at the end (4
+//      warps: tcgen05.ld 32x32b + coalesced st.global, 104 KB per CTA): the
+//      drain every decode GEMM launch pays once
 // Each CTA streams a contiguous range of (row tile, k block) items through an
 // S-stage mbarrier ring (one elected thread issues; a consumer thread releases
 // each stage as soon as it lands). Prints GB/s per pattern and ring depth.
@@ -57,22 +60,30 @@ __device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
 }
 
 template <int kMode>
-__global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUtensorMap map, const uint8_t* lin,
+__global__ void __launch_bounds__(192) stream_kernel(const __grid_constant__ CUtensorMap map, const uint8_t* lin,
                                                     int stages, unsigned long long* sink,
-                                                    const __grid_constant__ CUtensorMap xmap, int xbytes) {
+                                                    const __grid_constant__ CUtensorMap xmap, int xbytes,
+                                                    float* out) {
   extern __shared__ uint8_t raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
   const int sb = kBox + xbytes;  // stage bytes
   uint64_t* full = (uint64_t*)(smem + stages * sb);
   uint64_t* empty = full + stages;
+  __shared__ uint64_t acc_done;
+  __shared__ uint32_t tslot_s;
+  uint32_t& tslot = tslot_s;
+  if (kMode >= 5 && threadIdx.x >= 32 && threadIdx.x < 64) ppdk::tc::alloc(&tslot_s, 256);
   if (threadIdx.x == 0) {
+    bar_init(&acc_done, 1);
     for (int i = 0; i < stages; ++i) {
       bar_init(&full[i], 1);
       bar_init(&empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  ppdk::tc::fence_before();
   __syncthreads();
+  ppdk::tc::fence_after();
   const long long x0 = (long long)blockIdx.x * kItems / gridDim.x, x1 = (long long)(blockIdx.x + 1) * kItems / gridDim.x;
   const int n = (int)(x1 - x0);
   if (threadIdx.x == 0) {
@@ -110,10 +121,7 @@ __global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUte
     }
   } else if (kMode >= 5) {
     // MMA issuer (warp 1): the decode GEMM's per-stage tcgen05 work
-    __shared__ uint32_t tslot;
-    if (threadIdx.x >= 32) {
-      ppdk::tc::alloc(&tslot, 256);
-      __syncwarp();
+    if (threadIdx.x >= 32 && threadIdx.x < 64) {
       const uint32_t tmem = tslot;
       if (threadIdx.x == 32) {
         const int N = xbytes / 128;
@@ -128,12 +136,32 @@ __global__ void __launch_bounds__(64) stream_kernel(const __grid_constant__ CUte
           for (int k = 0; k < 4; ++k) ppdk::tc::mma_bf16_ss(tmem, da + 2 * k, db + 2 * k, idesc, (i > 0) || (k > 0));
           ppdk::tc::commit(&empty[s]);
         }
-        ppdk::tc::commit(&full[0]);  // drain marker (phase not waited; kernel end fences)
+        ppdk::tc::commit(&acc_done);  // all MMAs retired
       }
       __syncwarp();
-      ppdk::tc::fence_before();
-      ppdk::tc::dealloc(tmem, 256);
     }
+  }
+  if (kMode == 7 && threadIdx.x >= 64) {  // epilogue warps 2..5 (TMEM lane quarters 2,3,0,1)
+    const int w = threadIdx.x >> 5, lq = w & 3, ln = threadIdx.x & 31;
+    wait(&acc_done, 0);
+    ppdk::tc::fence_after();
+    const int N = xbytes / 128;
+    const uint32_t tbase = tslot + ((uint32_t)(lq * 32) << 16);
+    float* dst = out + (size_t)blockIdx.x * 128 * N + lq * 32 + ln;
+    for (int c0 = 0; c0 < 200; c0 += 32) {
+      uint32_t r[32];
+      ppdk::tc::ld32x32(tbase + (uint32_t)c0, r);
+      ppdk::tc::wait_ld();
+      const int nj = min(32, 200 - c0);
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj)
+        if (jj < nj) dst[(size_t)(c0 + jj) * 128] = __uint_as_float(r[jj]);
+    }
+  }
+  if (kMode >= 5) {
+    ppdk::tc::fence_before();
+    __syncthreads();
+    if (threadIdx.x >= 32 && threadIdx.x < 64) ppdk::tc::dealloc(tslot, 256);
   }
   if (kMode < 5 && threadIdx.x == 32) {
     unsigned long long acc = 0;
@@ -157,6 +185,7 @@ static bool make_map(CUtensorMap* m, void* base, uint64_t rows, uint64_t cols, i
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static float* g_out = nullptr;
 template <int kMode>
 static int run(const char* name, const CUtensorMap& map, const uint8_t* lin, int grid, int stages,
                unsigned long long* sink, const CUtensorMap& xmap, int xbytes) {
@@ -165,11 +194,11 @@ static int run(const char* name, const CUtensorMap& map, const uint8_t* lin, int
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int w = 0; w < 3; ++w) stream_kernel<kMode><<<grid, 64, smem>>>(map, lin, stages, sink, xmap, xbytes);
+  for (int w = 0; w < 3; ++w) stream_kernel<kMode><<<grid, 192, smem>>>(map, lin, stages, sink, xmap, xbytes, g_out);
   CK(cudaDeviceSynchronize());
   const int iters = 10;
   cudaEventRecord(a);
-  for (int i = 0; i < iters; ++i) stream_kernel<kMode><<<grid, 64, smem>>>(map, lin, stages, sink, xmap, xbytes);
+  for (int i = 0; i < iters; ++i) stream_kernel<kMode><<<grid, 192, smem>>>(map, lin, stages, sink, xmap, xbytes, g_out);
   cudaEventRecord(b);
   CK(cudaEventSynchronize(b));
   float ms = 0;
@@ -190,6 +219,7 @@ int main() {
   CK(cudaMalloc(&w, bytes));
   CK(cudaMalloc(&t, bytes));
   CK(cudaMalloc(&sink, 8));
+  CK(cudaMalloc(&g_out, (size_t)148 * 128 * 208 * 4 * 2));
   CK(cudaMemset(w, 1, bytes));
   CK(cudaMemset(t, 1, bytes));
   int sms = 0;
@@ -213,6 +243,7 @@ int main() {
     if (run<4>("E_weights_plus_act104", m_rm, w, sms, stages, sink, m_x104, 104 * 128)) return 1;
     if (run<5>("F_D_plus_mma_n208", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
     if (run<6>("G_E_plus_mma_n104", m_rm, w, sms, stages, sink, m_x104, 104 * 128)) return 1;
+    if (run<7>("H_F_plus_final_epilogue", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
   }
   return 0;
 }
