@@ -16,6 +16,9 @@
 //   H  F + the epilogue of one 128 x 208 fp32 accumulator at the end (4
 //      warps: tcgen05.ld 32x32b + coalesced st.global, 104 KB per CTA): the
 //      drain every decode GEMM launch pays once
+//   I  H with the TMEM loads only (no stores)   J  H with the stores only (no TMEM loads)
+//   K  H with the tile staged in shared memory (st.shared) and written by ONE
+//      1-D TMA bulk store (cp.async.bulk.global.shared::cta) per CTA
 // Each CTA streams a contiguous range of (row tile, k block) items through an
 // S-stage mbarrier ring (one elected thread issues; a consumer thread releases
 // each stage as soon as it lands). Prints GB/s per pattern and ring depth.
@@ -141,21 +144,53 @@ __global__ void __launch_bounds__(192) stream_kernel(const __grid_constant__ CUt
       __syncwarp();
     }
   }
-  if (kMode == 7 && threadIdx.x >= 64) {  // epilogue warps 2..5 (TMEM lane quarters 2,3,0,1)
+  if (kMode >= 7 && threadIdx.x >= 64) {  // epilogue warps 2..5 (TMEM lane quarters 2,3,0,1)
     const int w = threadIdx.x >> 5, lq = w & 3, ln = threadIdx.x & 31;
     wait(&acc_done, 0);
     ppdk::tc::fence_after();
     const int N = xbytes / 128;
     const uint32_t tbase = tslot + ((uint32_t)(lq * 32) << 16);
     float* dst = out + (size_t)blockIdx.x * 128 * N + lq * 32 + ln;
+    unsigned acc = 0;
     for (int c0 = 0; c0 < 200; c0 += 32) {
       uint32_t r[32];
-      ppdk::tc::ld32x32(tbase + (uint32_t)c0, r);
-      ppdk::tc::wait_ld();
-      const int nj = min(32, 200 - c0);
+      if (kMode != 9) {
+        ppdk::tc::ld32x32(tbase + (uint32_t)c0, r);
+        ppdk::tc::wait_ld();
+      } else {
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj)
-        if (jj < nj) dst[(size_t)(c0 + jj) * 128] = __uint_as_float(r[jj]);
+        for (int jj = 0; jj < 32; ++jj) r[jj] = jj + c0;
+      }
+      const int nj = min(32, 200 - c0);
+      if (kMode == 10) {  // stage [token][row] in the (now idle) stage ring
+        float* st = reinterpret_cast<float*>(smem) + lq * 32 + ln;
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj)
+          if (jj < nj) {
+            const uint32_t a = su32(st + (c0 + jj) * 128);
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(r[jj]) : "memory");
+          }
+      } else if (kMode == 8) {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) acc += r[jj];
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj)
+          if (jj < nj) dst[(size_t)(c0 + jj) * 128] = __uint_as_float(r[jj]);
+      }
+    }
+    if (acc == 0xFFFFFFFFu) *sink = acc;
+    if (kMode == 10) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 64) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                         out + (size_t)blockIdx.x * 128 * N),
+                     "r"(su32(smem)), "r"(200 * 128 * 4)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      }
     }
   }
   if (kMode >= 5) {
@@ -244,6 +279,9 @@ int main() {
     if (run<5>("F_D_plus_mma_n208", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
     if (run<6>("G_E_plus_mma_n104", m_rm, w, sms, stages, sink, m_x104, 104 * 128)) return 1;
     if (run<7>("H_F_plus_final_epilogue", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
+    if (run<8>("I_H_tmem_loads_only", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
+    if (run<9>("J_H_stores_only", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
+    if (run<10>("K_H_smem_staged_tma_bulk_store", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
   }
   return 0;
 }
