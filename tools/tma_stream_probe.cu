@@ -19,6 +19,8 @@
 //   I  H with the TMEM loads only (no stores)   J  H with the stores only (no TMEM loads)
 //   K  H with the tile staged in shared memory (st.shared) and written by ONE
 //      1-D TMA bulk store (cp.async.bulk.global.shared::cta) per CTA
+//   L  H writing only the first 104 tokens (half the bytes)
+//   M  H with streaming stores (st.global.cs)
 // Each CTA streams a contiguous range of (row tile, k block) items through an
 // S-stage mbarrier ring (one elected thread issues; a consumer thread releases
 // each stage as soon as it lands). Prints GB/s per pattern and ring depth.
@@ -152,7 +154,8 @@ __global__ void __launch_bounds__(192) stream_kernel(const __grid_constant__ CUt
     const uint32_t tbase = tslot + ((uint32_t)(lq * 32) << 16);
     float* dst = out + (size_t)blockIdx.x * 128 * N + lq * 32 + ln;
     unsigned acc = 0;
-    for (int c0 = 0; c0 < 200; c0 += 32) {
+    const int ntok = kMode == 11 ? 104 : 200;
+    for (int c0 = 0; c0 < ntok; c0 += 32) {
       uint32_t r[32];
       if (kMode != 9) {
         ppdk::tc::ld32x32(tbase + (uint32_t)c0, r);
@@ -173,10 +176,15 @@ __global__ void __launch_bounds__(192) stream_kernel(const __grid_constant__ CUt
       } else if (kMode == 8) {
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) acc += r[jj];
-      } else {
+      } else if (kMode == 12) {
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj)
-          if (jj < nj) dst[(size_t)(c0 + jj) * 128] = __uint_as_float(r[jj]);
+          if (jj < nj) __stcs(dst + (size_t)(c0 + jj) * 128, __uint_as_float(r[jj]));
+      } else {
+        const int nn = min(nj, ntok - c0);
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj)
+          if (jj < nn) dst[(size_t)(c0 + jj) * 128] = __uint_as_float(r[jj]);
       }
     }
     if (acc == 0xFFFFFFFFu) *sink = acc;
@@ -282,6 +290,8 @@ int main() {
     if (run<8>("I_H_tmem_loads_only", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
     if (run<9>("J_H_stores_only", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
     if (run<10>("K_H_smem_staged_tma_bulk_store", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
+    if (run<11>("L_H_half_bytes", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
+    if (run<12>("M_H_streaming_stores", m_rm, w, sms, stages, sink, m_x208, 208 * 128)) return 1;
   }
   return 0;
 }
