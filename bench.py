@@ -273,6 +273,28 @@ def reference_des(cluster: str, wl: dict, seed: int, calib: dict) -> dict:
     return out
 
 
+def reference_sweep() -> dict:
+    """the reference's default sweep plan (9,180 DES cells) with
+    parallelism = nproc, run by the UNMODIFIED reference (oracle/_ref/ref_tool,
+    sweep.cpp run_sweep) and by the engine's own sweep (engine/sweep) on the
+    same plan: wall times and whether the two cell CSVs are byte-identical."""
+    import time as _t
+    from oracle import oracle as O
+    from paper_2603_13358_b200 import engine as E
+    plan = json.loads(E.run({"op": "plan_default"})["plan_json"])
+    par = os.cpu_count() or 1
+    t0 = _t.perf_counter()
+    r = O.ref_tool({"op": "sweep", "plan": plan, "parallelism": par})
+    t_ref = _t.perf_counter() - t0
+    t0 = _t.perf_counter()
+    m = E.run({"op": "sweep", "plan": plan, "parallelism": par})
+    t_ours = _t.perf_counter() - t0
+    return {"plan": "reference default plan", "cells": len(r["cells"]), "parallelism": par,
+            "host_cpu_model": cpu_model(), "reference_wall_s": t_ref, "engine_wall_s": t_ours,
+            "plan_hash": r["plan_hash"], "csv_identical": r["csv"] == m["csv"],
+            "winner_cells": r["winner"]["cells"]}
+
+
 def device_calibration(dev, cfg, inter: dict, B: int, ctx, tok, bts, cal_bt, link_gbs: float) -> dict:
     """CalibrationTable coefficients fitted from B200 measurements of this run
     (ppd::cost::fit_from_measurements through the engine's fit_calibration op):
@@ -565,6 +587,10 @@ def run_ours(args, rank, world, local_rank):
         cpu = {"value": tps, "unit": "tok/s", "cores": nthr, "kind": "port", "sample": sample,
                "wall_s": secs, "host_cpu_model": cpu_model(), "host_nproc": os.cpu_count(),
                "reference_des": des}
+        try:
+            cpu["reference_sweep"] = reference_sweep()
+        except Exception as e:  # noqa: BLE001
+            cpu["reference_sweep"] = {"error": f"{type(e).__name__}: {e}"}
 
     line = {
         "metric": METRIC,
@@ -640,6 +666,10 @@ def run_reference(args, rank, world):
         des = reference_des("1P_1D", cfg2_workload(1.0), 3, {"calib_overrides": {"kv_bytes_per_token": 131072}})
     except Exception as e:  # noqa: BLE001
         des = {"error": f"{type(e).__name__}: {e}"}
+    try:
+        sweep = reference_sweep()
+    except Exception as e:  # noqa: BLE001
+        sweep = {"error": f"{type(e).__name__}: {e}"}
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -660,6 +690,7 @@ def run_reference(args, rank, world):
         "reference_des": {"kind": "reference", "what": "unmodified reference DES (oracle/_ref/ref_tool) on the "
                           "configs[2] trace, 1P_1D, seed 3, QPS 1, default calibration with Llama-3-8B KV bytes",
                           "result": des},
+        "reference_sweep": sweep,
         "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference (/root/reference/proj) prices this step analytically "
                 "(costmodel.cpp:372-379) and computes no tokens; its CPU arm is the oracle port",
