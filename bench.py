@@ -365,6 +365,14 @@ def nvlink_probe(world: int) -> dict:
     return out
 
 
+_HOST_GROUP = None
+
+
+def host_group():
+    """A gloo group over the same ranks, created by every rank right after init."""
+    return _HOST_GROUP
+
+
 def bench_config(B: int, ctx0: int, world: int) -> dict:
     return {
         "workload": f"Llama-3-8B-shape decode step, B={B} requests at ctx {ctx0}+, 1 colocated node per GPU "
@@ -471,7 +479,9 @@ def run_ours(args, rank, world, local_rank):
     for i in range(4):
         dev.step([1024 - m_app], [0], rng.integers(0, cfg.vocab, 1024 - m_app), ib(4 + i))
 
-    def timed(extra_q, extra_ctx, extra_bt, n=3):
+    def timed(extra_q, extra_ctx, extra_bt, n=5, warm=2):
+        # the first call of a step shape runs eagerly and the second captures its CUDA
+        # graph (device.cu run_step); both are warm-up, the median is over graph replays
         q = [1] * B + extra_q
         c = list(ctx) + extra_ctx
         bt = np.zeros((B + len(extra_q), bps + 64), dtype=np.int32)
@@ -480,9 +490,11 @@ def run_ours(args, rank, world, local_rank):
             bt[B + j, :64] = e
         want = [1] * B + [0] * len(extra_q)
         ms = []
-        for _ in range(n):
+        for i in range(warm + n):
             toks = np.concatenate([tok, rng.integers(0, cfg.vocab, int(np.sum(extra_q)))]).astype(np.int32)
-            ms.append(dev.step(q, c, toks, bt, want).ms)
+            t = dev.step(q, c, toks, bt, want).ms
+            if i >= warm:
+                ms.append(t)
         return float(np.median(ms))
 
     alone = timed([], [], [])
@@ -510,7 +522,9 @@ def run_ours(args, rank, world, local_rank):
     dev.close()
     if rank != 0:
         if world > 1:
-            torch.distributed.barrier()  # rank 0 drives all GPUs for the engine runs
+            # rank 0 drives all GPUs for the engine runs: wait on the CPU (gloo), since an
+            # NCCL barrier would spin a kernel on this GPU and time-slice against rank 0's work
+            torch.distributed.barrier(group=host_group())
         return
 
     qwen = None
@@ -640,7 +654,7 @@ def run_ours(args, rank, world, local_rank):
     }
     print(json.dumps(line), flush=True)
     if world > 1:
-        torch.distributed.barrier()
+        torch.distributed.barrier(group=host_group())
 
 
 def run_reference(args, rank, world):
@@ -725,6 +739,8 @@ def main():
         torch.cuda.set_device(gpu_of(local_rank))
         import datetime
         torch.distributed.init_process_group("gloo" if SAME_GPU else "nccl", timeout=datetime.timedelta(minutes=30))
+        global _HOST_GROUP
+        _HOST_GROUP = torch.distributed.new_group(backend="gloo", timeout=datetime.timedelta(minutes=60))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch
