@@ -192,6 +192,9 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
  *                  partials + a separate SiLU kernel
  *   "gemm_multi_sub" 1 (default): 257..512 token rows run as one unit of two
  *                  token sub-tiles per weight stage; 0: separate 256-row tiles
+ *   "gemm_epi_pipe" 1 (default): the plain GEMM epilogue keeps the next
+ *                  32-column TMEM load in flight while it stores the current
+ *                  chunk; 0: load, wait, store per chunk
  *   "gemm_occ2"    -1 auto (<= 128 token rows), 0 off, 1 on: two co-resident
  *                  CTAs per SM with half-depth rings
  *   "attn_fused"   1 (default): a mixed decode + prefill step runs its

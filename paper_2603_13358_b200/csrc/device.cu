@@ -1497,6 +1497,9 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "gemm_multi_sub") == 0) {
     CHECK_ARG(value == 0 || value == 1, "gemm_multi_sub must be 0 or 1");
     gemm_tc_set_multi_sub(value != 0);
+  } else if (std::strcmp(name, "gemm_epi_pipe") == 0) {
+    CHECK_ARG(value == 0 || value == 1, "gemm_epi_pipe must be 0 or 1");
+    gemm_tc_set_epi_pipe(value != 0);
   } else if (std::strcmp(name, "ws_two_slices") == 0) {  // takes effect for devices opened afterwards
     CHECK_ARG(value == 0 || value == 1, "ws_two_slices must be 0 or 1");
     g_ws_two_slices = value != 0;

@@ -98,6 +98,42 @@ PPD_DEV void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// the same load without the wait: the registers are valid only after wait_tmem_ld()
+PPD_DEV void tmem_ld32_async(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+PPD_DEV void wait_tmem_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// store 32 token columns of one output row (fp32 or bf16), token stride ldo;
+// one running pointer (32 precomputed 64-bit addresses cost 64 registers)
+template <bool kF32>
+PPD_DEV void store_cols32(void* base, size_t ldo, const uint32_t* r, int nj) {
+  if (kF32) {
+    float* d = static_cast<float*>(base);
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      if (jj < nj) *d = __uint_as_float(r[jj]);
+      d += ldo;
+    }
+  } else {
+    __nv_bfloat16* d = static_cast<__nv_bfloat16*>(base);
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      if (jj < nj) *d = __float2bfloat16_rn(__uint_as_float(r[jj]));
+      d += ldo;
+    }
+  }
+}
+
 // ---- CTA-pair (cta_group::2) primitives ------------------------------------
 PPD_DEV uint32_t cluster_ctarank() {
   uint32_t r;
@@ -480,31 +516,44 @@ __global__ void __launch_bounds__(kThreads, kOcc)
             }
           }
         }
+      } else if (kOcc == 1 && p.epi_pipe) {
+        // two register buffers: the TMEM load of chunk c+32 is in flight while
+        // chunk c is stored (a load + wait per chunk serialised ~4 us of TMEM
+        // latency per 100 KB epilogue, tools/tma_stream_probe.cu mode I)
+        uint32_t ra[32], rb[32];
+        const bool in = row < p.N;
+        const size_t off = (size_t)t0 * p.ldo + row;
+        void* base = p.out_f32 ? static_cast<void*>(out32 + off) : static_cast<void*>(out16 + off);
+        const size_t step = (size_t)32 * p.ldo * (p.out_f32 ? 4 : 2);
+        tmem_ld32_async(t_acc, ra);
+        wait_tmem_ld();
+        for (int c0 = 0; c0 < ncols; c0 += 64) {
+          if (c0 + 32 < ncols) tmem_ld32_async(t_acc + (uint32_t)(c0 + 32), rb);
+          if (in) {
+            if (p.out_f32) store_cols32<true>(base, p.ldo, ra, ncols - c0);
+            else store_cols32<false>(base, p.ldo, ra, ncols - c0);
+          }
+          base = static_cast<uint8_t*>(base) + step;
+          wait_tmem_ld();
+          if (c0 + 32 >= ncols) break;
+          if (c0 + 64 < ncols) tmem_ld32_async(t_acc + (uint32_t)(c0 + 64), ra);
+          if (in) {
+            if (p.out_f32) store_cols32<true>(base, p.ldo, rb, ncols - c0 - 32);
+            else store_cols32<false>(base, p.ldo, rb, ncols - c0 - 32);
+          }
+          base = static_cast<uint8_t*>(base) + step;
+          wait_tmem_ld();
+        }
       } else
       for (int c0 = 0; c0 < ncols; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(t_acc + (uint32_t)c0, r);
         if (row < p.N) {
-          const int nj = min(32, ncols - c0);
-          if (p.out_f32) {
-            float* dst = out32 + (size_t)(t0 + c0) * p.ldo + row;
-            if (kOcc == 2) {  // one running pointer: fits the 128-register budget of 2 CTAs per SM
-#pragma unroll
-              for (int jj = 0; jj < 32; ++jj) {
-                if (jj < nj) *dst = __uint_as_float(r[jj]);
-                dst += p.ldo;
-              }
-            } else {
-#pragma unroll
-              for (int jj = 0; jj < 32; ++jj)
-                if (jj < nj) dst[(size_t)jj * p.ldo] = __uint_as_float(r[jj]);
-            }
-          } else {
-            __nv_bfloat16* dst = out16 + (size_t)(t0 + c0) * p.ldo + row;
-#pragma unroll
-            for (int jj = 0; jj < 32; ++jj)
-              if (jj < nj) dst[(size_t)jj * p.ldo] = __float2bfloat16_rn(__uint_as_float(r[jj]));
-          }
+          const size_t off = (size_t)(t0 + c0) * p.ldo + row;
+          if (p.out_f32)
+            store_cols32<true>(out32 + off, p.ldo, r, ncols - c0);
+          else
+            store_cols32<false>(out16 + off, p.ldo, r, ncols - c0);
         }
       }
       }  // token sub-tiles
@@ -595,6 +644,7 @@ bool gemm_tc_map(void* map_out, const void* ptr, int rows, int K, int box_rows) 
 // 0 uniform K split / 1 balanced partition.
 static int g_pair_mode = -1;
 static bool g_multi_sub = true;  // T in (256, 512]: one unit covers both token sub-tiles
+static bool g_epi_pipe = true;   // plain epilogue: TMEM load of the next 32 columns in flight during the stores
 static bool g_even_tiles = true;  // T > 256 in separate token tiles: equal tiles, not 256-row ones
 void gemm_tc_set_even_tiles(bool on) { g_even_tiles = on; }
 // two co-resident single CTAs per SM: -1 auto (<= kOcc2MaxT tokens; measured
@@ -619,6 +669,7 @@ constexpr int kPairMinT = 48;
 constexpr double kPairMinTilesPerSm = 1.4;
 
 void gemm_tc_set_multi_sub(bool on) { g_multi_sub = on; }
+void gemm_tc_set_epi_pipe(bool on) { g_epi_pipe = on; }
 void gemm_tc_set_occ2(int mode) { g_occ2 = mode; }
 
 void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched) {
@@ -865,6 +916,7 @@ cudaError_t launch(const Shape& sh, const Plan& pl, const bf16* X, const bf16* W
   // weight-streaming shapes (<= 512 token rows) prefetch ahead into L2
   p.l2_pre = g_l2_pre >= 0 ? g_l2_pre : (T <= 2 * kMaxBN ? kL2PreAuto : 0);
   p.overlap = pdl_overlap();
+  p.epi_pipe = g_epi_pipe ? 1 : 0;
   CUtensorMap mw, mx;
   if (!get_map(&mw, W, N, K, kBM) || !get_map(&mx, X, T, K, sh.pair ? sh.bn / 2 : sh.bn))
     return cudaErrorInvalidValue;

@@ -59,6 +59,7 @@ struct GemmTcParams {
   int tail_slots;       // balanced: slots sharing the stream-K tail (<= slots)
   int l2_pre;           // weight k-blocks beyond the smem ring prefetched into L2 before the PDL wait
   int overlap;          // 1: trigger the successor only after our own PDL wait (see pdl_enter)
+  int epi_pipe;         // 1: plain epilogue double-buffers its TMEM loads (gemm_tc_set_epi_pipe)
 };
 
 // out[T][N] (+ split slices) = X[T][K] . W[N][K]^T ; splits > 1 needs out_f32
@@ -78,6 +79,7 @@ void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched);
 // T in (256, 512] token rows: one unit per weight tile covering 2 token
 // sub-tiles (default on) vs separate 256-row token tiles (A/B knob)
 void gemm_tc_set_multi_sub(bool on);
+void gemm_tc_set_epi_pipe(bool on);
 // T > 256 rows in separate token tiles: equal tiles (default) vs 256-row tiles (A/B knob)
 void gemm_tc_set_even_tiles(bool on);
 // two co-resident CTAs per SM (half-depth rings, one accumulator each):
