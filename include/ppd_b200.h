@@ -191,7 +191,10 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
  *   "mlp_fused"    1 gate|up GEMM with the SiLU epilogue, 0 (default) fp32
  *                  partials + a separate SiLU kernel
  *   "gemm_multi_sub" 1 (default): 257..512 token rows run as one unit of two
- *                  token sub-tiles per weight stage; 0: separate 256-row tiles
+ *                  token sub-tiles per weight stage for the wide projections
+ *                  and for narrow ones whose CTA-pair tiles fill the SMs in one
+ *                  round; 2: every projection; 3: wide ones only; 0: separate
+ *                  token tiles
  *   "gemm_epi_pipe" 1 (default): the plain GEMM epilogue keeps the next
  *                  32-column TMEM load in flight while it stores the current
  *                  chunk; 0: load, wait, store per chunk

@@ -1495,8 +1495,8 @@ int ppd_set_tuning(const char* name, int32_t value) {
     CHECK_ARG(value >= -1 && value <= 1, "gemm_occ2 must be -1, 0 or 1");
     gemm_tc_set_occ2(value);
   } else if (std::strcmp(name, "gemm_multi_sub") == 0) {
-    CHECK_ARG(value == 0 || value == 1, "gemm_multi_sub must be 0 or 1");
-    gemm_tc_set_multi_sub(value != 0);
+    CHECK_ARG(value >= 0 && value <= 3, "gemm_multi_sub must be 0, 1, 2 or 3");
+    gemm_tc_set_multi_sub(value);
   } else if (std::strcmp(name, "gemm_epi_pipe") == 0) {
     CHECK_ARG(value == 0 || value == 1, "gemm_epi_pipe must be 0 or 1");
     gemm_tc_set_epi_pipe(value != 0);

@@ -643,7 +643,9 @@ bool gemm_tc_map(void* map_out, const void* ptr, int rows, int K, int box_rows) 
 // stages = cap on the smem ring depth (0 = as many as fit); sched = -1 auto /
 // 0 uniform K split / 1 balanced partition.
 static int g_pair_mode = -1;
-static bool g_multi_sub = true;  // T in (256, 512]: one unit covers both token sub-tiles
+// T in (256, 512]: one unit covers both token sub-tiles. 1 auto (wide shapes +
+// narrow ones whose pair tiles fill the SMs), 2 every shape (paired), 3 wide only
+static int g_multi_sub = 1;
 static bool g_epi_pipe = true;   // plain epilogue: TMEM load of the next 32 columns in flight during the stores
 static bool g_even_tiles = true;  // T > 256 in separate token tiles: equal tiles, not 256-row ones
 void gemm_tc_set_even_tiles(bool on) { g_even_tiles = on; }
@@ -668,7 +670,7 @@ void gemm_tc_set_l2_pre(int n) { g_l2_pre = n; }
 constexpr int kPairMinT = 48;
 constexpr double kPairMinTilesPerSm = 1.4;
 
-void gemm_tc_set_multi_sub(bool on) { g_multi_sub = on; }
+void gemm_tc_set_multi_sub(int mode) { g_multi_sub = mode; }
 void gemm_tc_set_epi_pipe(bool on) { g_epi_pipe = on; }
 void gemm_tc_set_occ2(int mode) { g_occ2 = mode; }
 
@@ -757,10 +759,22 @@ Shape shape_for(int T, int N, int K, int extra_smem = 0, bool force_single = fal
   // narrow projections (qkv, o) need the parallelism of separate token tiles
   // (tools/gemm_mixed.py: qkv at T=456 39 -> 26 us, o 30 -> 19 us)
   const bool wide = (N + kBM - 1) / kBM >= kPairMinTilesPerSm * device_sms() || K >= kSubPairMinK;
+  // a narrow projection takes the paired two-sub-tile unit too when some
+  // uniform K split of its 256-row pair tiles fills >= 90% of the pair slots in
+  // ONE round (qkv, 24 pair tiles x 3: T=328 22.9 -> 20.2 us, T=456 25.2 ->
+  // 23.3 us; o-proj, 16 x 4 = 64 of 74, stays on separate token tiles:
+  // 16.4 -> 16.6 / 17.2 -> 19.5 us; tools/gemm_mixed.py)
+  bool narrow_fill = false;
+  {
+    const int pt = (N + 2 * kBM - 1) / (2 * kBM), pslots = device_sms() / 2;
+    for (int sp = 1; sp <= 8; ++sp)
+      if (pt * sp <= pslots && pt * sp >= 0.9 * pslots) narrow_fill = true;
+  }
+  const bool narrow_pair = g_multi_sub == 2 || (g_multi_sub == 1 && narrow_fill && g_pair_mode != 0);
   if (T <= kMaxBN) {
     sh.n_sub = 1;
     sh.bn = ((T + 15) / 16) * 16;
-  } else if (T <= 2 * kMaxBN && g_multi_sub && wide) {
+  } else if (T <= 2 * kMaxBN && g_multi_sub && (wide || narrow_pair)) {
     sh.n_sub = 2;
     sh.bn = (((T + 1) / 2 + 15) / 16) * 16;
   } else {
@@ -775,6 +789,7 @@ Shape shape_for(int T, int N, int K, int extra_smem = 0, bool force_single = fal
   // long-K (down projection) steps of > 1024 rows pair as well (T=2048: 232 -> 220 us)
   const bool auto_pair =
       T >= kPairMinT && (tiles1 >= kPairMinTilesPerSm * device_sms() || (sh.n_sub > 1 && K >= kSubPairMinK) ||
+                         (sh.n_sub > 1 && narrow_pair) ||
                          (T > 4 * kMaxBN && K >= kSubPairMinK));
   const bool want_occ2 = sh.n_sub == 1 && extra_smem == 0 && (g_occ2 == 1 || (g_occ2 < 0 && T <= kOcc2MaxT));
   sh.pair = !force_single && (g_pair_mode == 1 || (g_pair_mode < 0 && auto_pair && !want_occ2));

@@ -78,7 +78,7 @@ cudaError_t gemm_tc_run_silu(const bf16* X, const bf16* W, bf16* m, int T, int N
 void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched);
 // T in (256, 512] token rows: one unit per weight tile covering 2 token
 // sub-tiles (default on) vs separate 256-row token tiles (A/B knob)
-void gemm_tc_set_multi_sub(bool on);
+void gemm_tc_set_multi_sub(int mode);
 void gemm_tc_set_epi_pipe(bool on);
 // T > 256 rows in separate token tiles: equal tiles (default) vs 256-row tiles (A/B knob)
 void gemm_tc_set_even_tiles(bool on);
