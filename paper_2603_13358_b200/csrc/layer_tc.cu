@@ -176,8 +176,9 @@ PPD_DEV int glue_kind(int j) { return j == 1 ? kGlueSilu : j == 3 ? kGlueRope : 
 // which made the glue instruction-bound when evaluated per element).
 
 // x += sum of the job's delta slices; h = RMSNorm(x), for rows c and c + n_cta.
-// Per-row thread/chunk mapping and reduction order equal add_rmsnorm_kernel's
-// (256 threads), so the sums are the same.
+// 256 threads per row: the sum of squares is reduced in a different order from
+// add_rmsnorm_kernel's (one chunk per thread at d <= 4096), so inv_rms may
+// differ in the last fp32 bit (the K8 tests compare within tolerance).
 PPD_DEV void glue_add_norm(const LayerParams& p, const LayerJob& J, int c, int et, float* red, const uint8_t* nsl) {
   const int d = p.d_model, nc = d / 8;
   const int warp = et >> 5, lane = et & 31;

@@ -7,15 +7,16 @@
 #include "kernels.h"
 #include "ops_dev.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace ppdk {
 
 namespace {
-constexpr int kNormThreads = 256;
-constexpr int kMaxChunks = 4;  // d <= 256 * 8 * 4 = 8192
+constexpr int kNormMaxThreads = 640;  // add_rmsnorm: at most 640 threads; one 8-element chunk each up to d = 4096
+constexpr int kNormPre = 4;           // K-partial slices whose loads are issued together (decode: <= 4)
 
-template <int N>
+// sum over the CTA (any multiple of 32 threads up to 1024)
 PPD_DEV float block_sum(float v, float* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -23,7 +24,7 @@ PPD_DEV float block_sum(float v, float* red) {
   __syncthreads();
   float r = 0.f;
   if (threadIdx.x < 32) {
-    r = threadIdx.x < N / 32 ? red[threadIdx.x] : 0.f;
+    r = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
     r = warp_sum(r);
     if (threadIdx.x == 0) red[32] = r;
   }
@@ -134,57 +135,83 @@ cudaError_t launch_embed(const int* tokens, const bf16* embed, bf16* x, int T, i
 
 // --------------------------------------------------- residual add + RMSNorm
 // v = x (+ rbf(sum of delta partials) | + delta_bf16); x <- v ; out = rbf(rbf(v) * inv_rms) * w
-template <bool kWriteX, bool kEarly>
-__global__ void __launch_bounds__(kNormThreads, 2) add_rmsnorm_kernel(
+// One CTA per row; thread t owns the 8-element chunks t, t + blockDim, ...
+// (kCh of them: one at d <= 4096, so every chunk's loads are in flight at once).
+template <bool kWriteX, bool kEarly, int kCh>
+__global__ void __launch_bounds__(kCh == 1 ? 512 : kNormMaxThreads, kCh == 1 ? 2 : 1) add_rmsnorm_kernel(
     bf16* x, const float* df, GemmParts parts, const bf16* db, const bf16* w,
     bf16* out, const int* rows, int d, float eps) {
   __shared__ float red[33];
   pdl_enter<kEarly>();
   const size_t row = rows ? (size_t)rows[blockIdx.x] : (size_t)blockIdx.x;
   const int nc = d / 8;
-  float v[kMaxChunks][8];
+  float v[kCh][8];
   float ss = 0.f;
+  // every chunk's loads are issued before the first store of x (a store in
+  // between would order the next chunk's loads behind it: x may alias df)
 #pragma unroll
-  for (int k = 0; k < kMaxChunks; ++k) {
-    int c = threadIdx.x + k * kNormThreads;
+  for (int k = 0; k < kCh; ++k) {
+    int c = threadIdx.x + k * blockDim.x;
     if (c < nc) {
       unpack8(reinterpret_cast<const uint4*>(x + row * d)[c], v[k]);
       if (df) {
-        add_delta8<false, kMaxSlices>(v[k], df, parts.stride, parts.valid(c * 8, (int)row), row, d, c);
+        add_delta8<false, kNormPre>(v[k], df, parts.stride, parts.valid(c * 8, (int)row), row, d, c);
       } else if (db) {
         float dv[8];
         unpack8(reinterpret_cast<const uint4*>(db + row * d)[c], dv);
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[k][j] = rbf(__fadd_rn(v[k][j], dv[j]));
       }
-      if (kWriteX && (df || db)) reinterpret_cast<uint4*>(x + row * d)[c] = pack8(v[k]);
 #pragma unroll
       for (int j = 0; j < 8; ++j) ss += v[k][j] * v[k][j];
     }
   }
-  ss = block_sum<kNormThreads>(ss, red);
+  if (kWriteX && (df || db)) {
+#pragma unroll
+    for (int k = 0; k < kCh; ++k) {
+      int c = threadIdx.x + k * blockDim.x;
+      if (c < nc) reinterpret_cast<uint4*>(x + row * d)[c] = pack8(v[k]);
+    }
+  }
+  ss = block_sum(ss, red);
   const float inv = rms_inv(ss, d, eps);
   const size_t orow = rows ? (size_t)blockIdx.x : row;
 #pragma unroll
-  for (int k = 0; k < kMaxChunks; ++k) {
-    int c = threadIdx.x + k * kNormThreads;
+  for (int k = 0; k < kCh; ++k) {
+    int c = threadIdx.x + k * blockDim.x;
     if (c < nc) reinterpret_cast<uint4*>(out + orow * d)[c] = norm8(v[k], inv, w, c);
   }
+}
+
+template <bool kWriteX>
+cudaError_t launch_norm(int n_rows, bf16* x, const float* df, const GemmParts& parts, const bf16* db,
+                        const bf16* w, bf16* out, const int* rows, int d, float eps, cudaStream_t s) {
+  const int nc = d / 8;
+  const int ch = nc <= 512 ? 1 : std::max(2, (nc + kNormMaxThreads - 1) / kNormMaxThreads);
+  const int threads = ((nc + ch - 1) / ch + 31) / 32 * 32;
+  const bool early = pdl_overlap();
+#define PPD_NORM(CH)                                                                                      \
+  if (ch <= CH)                                                                                           \
+    return launch_pdl(early ? add_rmsnorm_kernel<kWriteX, true, CH> : add_rmsnorm_kernel<kWriteX, false, CH>, \
+                      dim3(n_rows), dim3(threads), 0, s, x, df, parts, db, w, out, rows, d, eps);
+  PPD_NORM(1)
+  PPD_NORM(2)
+  PPD_NORM(4)
+#undef PPD_NORM
+  return cudaErrorInvalidValue;  // d > 20480
 }
 
 cudaError_t launch_add_rmsnorm(bf16* x, const float* delta_f32, const GemmParts& parts, const bf16* delta_bf16,
                                const bf16* w, bf16* h, int T, int d, float eps, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  return launch_pdl(pdl_overlap() ? add_rmsnorm_kernel<true, true> : add_rmsnorm_kernel<true, false>, dim3(T), dim3(kNormThreads), 0, s, x, delta_f32, parts, delta_bf16,
-                    w, h, (const int*)nullptr, d, eps);
+  return launch_norm<true>(T, x, delta_f32, parts, delta_bf16, w, h, nullptr, d, eps, s);
 }
 
 cudaError_t launch_final_norm(const bf16* x, const float* delta_f32, const GemmParts& parts,
                               const bf16* delta_bf16, const int* rows, int n_rows, const bf16* w,
                               bf16* out, int T, int d, float eps, cudaStream_t s) {
   if (n_rows == 0) return cudaSuccess;
-  return launch_pdl(pdl_overlap() ? add_rmsnorm_kernel<false, true> : add_rmsnorm_kernel<false, false>, dim3(n_rows), dim3(kNormThreads), 0, s, const_cast<bf16*>(x),
-                    delta_f32, parts, delta_bf16, w, out, rows, d, eps);
+  return launch_norm<false>(n_rows, const_cast<bf16*>(x), delta_f32, parts, delta_bf16, w, out, rows, d, eps, s);
 }
 
 // ------------------------------------------------------- RoPE + KV write
@@ -208,23 +235,37 @@ cudaError_t launch_rope_kv_write(const float* qkv, const GemmParts& parts, const
   if (T == 0) return cudaSuccess;
   const RopeArgs a{qkv,     parts, bias, row_seq, row_pos, block_tables, max_blocks, rope_cos, rope_sin,
                    q_out,   kv_pool, Hq,  Hkv,     Dh,      n_layers,     layer,      block_tokens};
-  // (row, quarter of the row's rotary/v units): 4 CTAs per token row for memory parallelism
-  return launch_pdl(pdl_overlap() ? rope_kv_kernel<true> : rope_kv_kernel<false>, dim3(T, 4), dim3(128), 0, s, a, T);
+  // (row, eighth of the row's rotary/v units): 8 CTAs per token row, one unit
+  // per thread at the Llama-3-8B shape (896 units), for memory parallelism
+  return launch_pdl(pdl_overlap() ? rope_kv_kernel<true> : rope_kv_kernel<false>, dim3(T, 8), dim3(128), 0, s, a, T);
 }
 
 // ------------------------------------------------------------- SiLU * up
 // gate/up come interleaved in 64-column groups (launch_fill_gate_up layout);
 // each thread produces 4 outputs from one float4 of gate and one of up.
+// Each thread produces kSiluQ quads (256 * 4 columns apart) and issues all of
+// their slice loads before the first store.
+constexpr int kSiluQ = 2;
 template <bool kEarly>
 __global__ void silu_mul_kernel(const float* gu, GemmParts parts, bf16* m, int F) {
   pdl_enter<kEarly>();
   const int r = blockIdx.y;
-  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) * 4; j < F; j += gridDim.x * blockDim.x * 4)
-    silu4<false>(gu, parts.stride, parts.valid((j >> 6) * 128, r), m, F, r, j);
+  const int j0 = (blockIdx.x * blockDim.x * kSiluQ + threadIdx.x) * 4;
+  float4 g[kSiluQ], u[kSiluQ];
+#pragma unroll
+  for (int q = 0; q < kSiluQ; ++q) {
+    const int j = j0 + q * (int)blockDim.x * 4;
+    if (j < F) silu4_load<false>(gu, parts.stride, parts.valid((j >> 6) * 128, r), F, r, j, g[q], u[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < kSiluQ; ++q) {
+    const int j = j0 + q * (int)blockDim.x * 4;
+    if (j < F) silu4_store(g[q], u[q], m, F, r, j);
+  }
 }
 cudaError_t launch_silu_mul(const float* gu, const GemmParts& parts, bf16* m, int T, int F, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  dim3 grid((F / 4 + 255) / 256, T);
+  dim3 grid((F / 4 + 256 * kSiluQ - 1) / (256 * kSiluQ), T);
   return launch_pdl(pdl_overlap() ? silu_mul_kernel<true> : silu_mul_kernel<false>, grid, dim3(256), 0, s, gu, parts, m, F);
 }
 

@@ -91,17 +91,27 @@ PPD_DEV float rms_inv(float ss, int d, float eps) {
 // partials (64-column groups, launch_fill_gate_up). Fast exp/div: within
 // 2 ulp of the oracle's fp32, rounded to bf16 next.
 // (gate and up of one output share a 128-column weight tile: one slice count n)
+// the two halves of silu4: gather gate / up sums, then compute + store, so a
+// caller can issue several units' loads before the first store
 template <bool kCg>
-PPD_DEV void silu4(const float* gu, size_t stride, int n, bf16* m, int F, int r, int j) {
+PPD_DEV void silu4_load(const float* gu, size_t stride, int n, int F, int r, int j, float4& g, float4& u) {
   const float* row = gu + (size_t)r * 2 * F;
   const int grp = j >> 6, within = j & 63;
-  const float4 g = ld_sum4<false, kCg>(row, stride, n, nullptr, grp * 128 + within);
-  const float4 u = ld_sum4<false, kCg>(row, stride, n, nullptr, grp * 128 + 64 + within);
+  g = ld_sum4<false, kCg>(row, stride, n, nullptr, grp * 128 + within);
+  u = ld_sum4<false, kCg>(row, stride, n, nullptr, grp * 128 + 64 + within);
+}
+PPD_DEV void silu4_store(const float4& g, const float4& u, bf16* m, int F, int r, int j) {
   const float gv[4] = {g.x, g.y, g.z, g.w}, uv[4] = {u.x, u.y, u.z, u.w};
   float o[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) o[e] = __fmul_rn(__fdividef(gv[e], __fadd_rn(1.0f, __expf(-gv[e]))), uv[e]);
   st_bf16x4(m + (size_t)r * F + j, o[0], o[1], o[2], o[3]);
+}
+template <bool kCg>
+PPD_DEV void silu4(const float* gu, size_t stride, int n, bf16* m, int F, int r, int j) {
+  float4 g, u;
+  silu4_load<kCg>(gu, stride, n, F, r, j, g, u);
+  silu4_store(g, u, m, F, r, j);
 }
 
 PPD_DEV int rope_units_per_row(const RopeArgs& a) { return (a.Hq + a.Hkv) * (a.Dh / 8) + a.Hkv * a.Dh / 4; }
