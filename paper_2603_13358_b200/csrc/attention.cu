@@ -74,6 +74,14 @@ PPD_DEV void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint6
       : "memory");
 }
 
+PPD_DEV void tma_load_2d_hint(void* smem, const CUtensorMap* map, int x, int y, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -451,6 +459,7 @@ PPD_DEV void decode_body(const CUtensorMap* kv_map, const AttnParams& p, uint8_t
     // overlap: cached K/V (positions < ctx) was written by earlier steps, so it
     // streams before the predecessor (RoPE + KV write of this step's rows)
     // retires; the first stage holding a position >= ctx waits for it
+    const uint64_t kv_pol = l2_evict_first_policy();
     bool waited = !p.overlap;
     int g = 0;  // global stage counter across this CTA's segments
     for (int sg = seg0; sg < seg1; ++sg) {
@@ -474,8 +483,11 @@ PPD_DEV void decode_body(const CUtensorMap* kv_map, const AttnParams& p, uint8_t
         if (lane < 16 && b < nb) {
           const int blk = btab[b0 + b];
           const int row = (((blk * p.n_layers + p.layer) * 2 + is_v) * p.n_kv_heads + kvh) * kBT;
-          tma_load_2d(stage_base + slot * kStageBytes + (b * 2 + is_v) * kBlockBytes + h * 2048, kv_map, h * 64,
-                      row, &full_bar[slot]);
+          void* dst = stage_base + slot * kStageBytes + (b * 2 + is_v) * kBlockBytes + h * 2048;
+          if (p.l2_hint)  // cached K/V is read once per step
+            tma_load_2d_hint(dst, kv_map, h * 64, row, &full_bar[slot], kv_pol);
+          else
+            tma_load_2d(dst, kv_map, h * 64, row, &full_bar[slot]);
         }
       }
     }

@@ -119,6 +119,15 @@ PPD_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
   while (!mbar_try_wait(bar, phase)) {
   }
 }
+// L2 eviction policy for streams read exactly once per step (weights, cached
+// K/V): their lines go first, so the step's small working set (K-split
+// partials, activations, residual) stays L2-resident between producer and
+// consumer kernels instead of being evicted by the 40 GB stream
+PPD_DEV uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 // global -> shared bulk copy, completion counted on an mbarrier (bytes % 16 == 0)
 PPD_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

@@ -570,6 +570,7 @@ int run_attention(const ppd_model_cfg& c, const void* kv_map, const bf16* q, bf1
   p.counters = counters;
   p.mix_ctr = mix_ctr;
   p.overlap = pdl_overlap();
+  p.l2_hint = (gemm_tc_l2_hint() >> 1) & 1;
   // K2: a mixed step is ONE launch (prefill CTAs + decode CTAs)
   if (n_pf > 0) {
     CU(launch_mixed_attention(kv_map, p, d_items + n_dec, n_pf, (n_items - n_dec) * c.n_kv_heads, n_cta, s));
@@ -1497,6 +1498,9 @@ int ppd_set_tuning(const char* name, int32_t value) {
   } else if (std::strcmp(name, "gemm_multi_sub") == 0) {
     CHECK_ARG(value >= 0 && value <= 3, "gemm_multi_sub must be 0, 1, 2 or 3");
     gemm_tc_set_multi_sub(value);
+  } else if (std::strcmp(name, "l2_hint") == 0) {
+    CHECK_ARG(value >= 0 && value <= 3, "l2_hint must be in [0, 3]");
+    gemm_tc_set_l2_hint(value);
   } else if (std::strcmp(name, "gemm_epi_pipe") == 0) {
     CHECK_ARG(value == 0 || value == 1, "gemm_epi_pipe must be 0 or 1");
     gemm_tc_set_epi_pipe(value != 0);

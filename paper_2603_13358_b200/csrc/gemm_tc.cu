@@ -51,6 +51,14 @@ PPD_DEV void tma_load_2d(void* smem, const CUtensorMap* map, int x, int y, uint6
       : "memory");
 }
 
+PPD_DEV void tma_load_2d_hint(void* smem, const CUtensorMap* map, int x, int y, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // prefetch one box of a tensor-mapped matrix into L2 (no smem, no completion)
 PPD_DEV void tma_prefetch_l2(const CUtensorMap* map, int x, int y) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
@@ -155,6 +163,14 @@ PPD_DEV void tma_load_2d_pair(void* smem, const CUtensorMap* map, int x, int y, 
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster)
+      : "memory");
+}
+PPD_DEV void tma_load_2d_pair_hint(void* smem, const CUtensorMap* map, int x, int y, uint32_t bar_cluster,
+                                   uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar_cluster), "l"(pol)
       : "memory");
 }
 PPD_DEV void mma_bf16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
@@ -351,6 +367,16 @@ __global__ void __launch_bounds__(kThreads, kOcc)
     else
       tma_load_2d(dst, map, x, y, &full[s]);
   };
+  // weights are read once per step: evict-first in L2 (p.l2_hint)
+  const uint64_t wpol = l2_evict_first_policy();
+  auto load_w = [&](void* dst, int x, int y, int s) {
+    if (!p.l2_hint)
+      load(dst, &map_w, x, y, s);
+    else if (kPair)
+      tma_load_2d_pair_hint(dst, &map_w, x, y, full_bar0 + 8u * s, wpol);
+    else
+      tma_load_2d_hint(dst, &map_w, x, y, &full[s], wpol);
+  };
 
   if (p.overlap && !(warp == 0 && lane == 0) && warp < 4) {  // every thread passes the wait before triggering
     pdl_wait();
@@ -367,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, kOcc)
         while (npre < S && pre.next(sg)) {
           for (int kb = sg.kb0; kb < sg.kb1 && npre < S; ++kb, ++npre) {
             if (leader) mbar_arrive_expect_tx(&full[npre], tx_bytes);
-            load(smem + npre * stage_bytes, &map_w, kb * kBK, sg.tw * rows + w_row0, npre);
+            load_w(smem + npre * stage_bytes, kb * kBK, sg.tw * rows + w_row0, npre);
           }
         }
       }
@@ -399,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, kOcc)
                 mbar_wait(&empty[s], ((it / S) - 1) & 1);
             }
             if (leader) mbar_arrive_expect_tx(&full[s], tx_bytes);
-            load(sw, &map_w, kb * kBK, sg.tw * rows + w_row0, s);
+            load_w(sw, kb * kBK, sg.tw * rows + w_row0, s);
           }
 #pragma unroll
           for (int jx = 0; jx < kNSub; ++jx)
@@ -646,6 +672,7 @@ static int g_pair_mode = -1;
 // T in (256, 512]: one unit covers both token sub-tiles. 1 auto (wide shapes +
 // narrow ones whose pair tiles fill the SMs), 2 every shape (paired), 3 wide only
 static int g_multi_sub = 1;
+static int g_l2_hint = 3;  // bit 0: GEMM weights, bit 1: decode K/V loads evict-first in L2
 static bool g_epi_pipe = true;   // plain epilogue: TMEM load of the next 32 columns in flight during the stores
 static bool g_even_tiles = true;  // T > 256 in separate token tiles: equal tiles, not 256-row ones
 void gemm_tc_set_even_tiles(bool on) { g_even_tiles = on; }
@@ -672,6 +699,8 @@ constexpr double kPairMinTilesPerSm = 1.4;
 
 void gemm_tc_set_multi_sub(int mode) { g_multi_sub = mode; }
 void gemm_tc_set_epi_pipe(bool on) { g_epi_pipe = on; }
+void gemm_tc_set_l2_hint(int mask) { g_l2_hint = mask; }
+int gemm_tc_l2_hint() { return g_l2_hint; }
 void gemm_tc_set_occ2(int mode) { g_occ2 = mode; }
 
 void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched) {
@@ -853,7 +882,12 @@ Plan plan_for(const Shape& sh, int T, int N, int K, int max_slices) {
   // 157 us) -- the data-parallel waves keep it for all but the tail.
   // tools/gemm_mixed.py: uniform measured faster than pure stream-K for
   // gate|up at T=712 (160 -> 138 us) and down at T=200-456 (4-7%).
-  const bool auto_bal = (sh.n_sub == 1 && T <= kMaxBN && K < kSubPairMinK) || T > 2 * kMaxBN;
+  // Two-sub-tile units of the wide short-K projection (gate|up of a 257-512-row
+  // mixed step: 112 pair tiles on 74 pairs) take one whole wave + a stream-K
+  // tail too (tools/ab_sched.sh: T=328 73.7 -> 70.5 us, T=456 91.1 -> 88.3 us;
+  // the narrow projections and the long-K down keep uniform splits)
+  const bool wide_sub = sh.n_sub > 1 && K < kSubPairMinK && (N + kBM - 1) / kBM >= kPairMinTilesPerSm * device_sms();
+  const bool auto_bal = (sh.n_sub == 1 && T <= kMaxBN && K < kSubPairMinK) || T > 2 * kMaxBN || wide_sub;
   if (g_sched != 0 && max_slices >= 2 && (g_sched == 1 || auto_bal)) {
     const int dp = T > kMaxBN ? (tiles / sh.slots) * sh.slots : 0;
     const long long total = (long long)(tiles - dp) * kbt;
@@ -932,6 +966,10 @@ cudaError_t launch(const Shape& sh, const Plan& pl, const bf16* X, const bf16* W
   p.l2_pre = g_l2_pre >= 0 ? g_l2_pre : (T <= 2 * kMaxBN ? kL2PreAuto : 0);
   p.overlap = pdl_overlap();
   p.epi_pipe = g_epi_pipe ? 1 : 0;
+  // evict-first only when every weight tile is read once (one token unit): with
+  // several token tiles the other tiles re-read it from L2 (tools/ab_hint.sh:
+  // B=16 / 64 decode steps -3.8% / -4.0%, B=200 -0.9%, 1536-token mix +0.8%)
+  p.l2_hint = ((g_l2_hint & 1) && T <= sh.unit_t) ? 1 : 0;
   CUtensorMap mw, mx;
   if (!get_map(&mw, W, N, K, kBM) || !get_map(&mx, X, T, K, sh.pair ? sh.bn / 2 : sh.bn))
     return cudaErrorInvalidValue;

@@ -60,6 +60,7 @@ struct GemmTcParams {
   int l2_pre;           // weight k-blocks beyond the smem ring prefetched into L2 before the PDL wait
   int overlap;          // 1: trigger the successor only after our own PDL wait (see pdl_enter)
   int epi_pipe;         // 1: plain epilogue double-buffers its TMEM loads (gemm_tc_set_epi_pipe)
+  int l2_hint;          // 1: weight TMA loads carry an L2 evict-first policy
 };
 
 // out[T][N] (+ split slices) = X[T][K] . W[N][K]^T ; splits > 1 needs out_f32
@@ -80,6 +81,9 @@ void gemm_tc_set_tuning(int pair_mode, int stage_cap, int sched);
 // sub-tiles (default on) vs separate 256-row token tiles (A/B knob)
 void gemm_tc_set_multi_sub(int mode);
 void gemm_tc_set_epi_pipe(bool on);
+// L2 evict-first on streamed-once loads: bit 0 GEMM weights, bit 1 decode K/V
+void gemm_tc_set_l2_hint(int mask);
+int gemm_tc_l2_hint();
 // T > 256 rows in separate token tiles: equal tiles (default) vs 256-row tiles (A/B knob)
 void gemm_tc_set_even_tiles(bool on);
 // two co-resident CTAs per SM (half-depth rings, one accumulator each):

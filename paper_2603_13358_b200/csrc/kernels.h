@@ -43,6 +43,7 @@ struct AttnParams {
   const int* seg_start;
   int* mix_ctr;              // K2 queue heads + done counter [3], zero-initialised, self-resetting
   int overlap;               // decode: stream cached K/V before waiting on the predecessor (pdl_overlap)
+  int l2_hint;               // decode: K/V TMA loads carry an L2 evict-first policy
 };
 
 // Persistent decode attention over balanced key segments (kv head in item.pad[0]).

@@ -97,6 +97,28 @@ def test_gemm_pair_equals_single(gpu):
     assert torch.equal(outs[0], outs[1])
 
 
+def test_l2_hint_does_not_change_results(gpu):
+    """The L2 evict-first policy on the weight stream (knob l2_hint) is a cache
+    hint only: results are bit-identical with and without it."""
+    import torch
+    M, N, K = 200, 6144, 4096
+    A = (torch.randn(M, K, device="cuda") * 0.5).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    outs = []
+    L = ppd.lib()
+    try:
+        for mask in (0, 3):
+            ppd.check(L.ppd_set_tuning(b"l2_hint", mask))
+            C = torch.zeros(3, M, N, device="cuda")
+            ppd.check(L.ppd_op_gemm_tc(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, 1, 3, None))
+            outs.append(C)
+        with pytest.raises(ppd.InvalidArgument):
+            ppd.check(L.ppd_set_tuning(b"l2_hint", 4))
+    finally:
+        ppd.check(L.ppd_set_tuning(b"l2_hint", 3))
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_set_tuning_rejects_unknown(gpu):
     with pytest.raises(ppd.InvalidArgument):
         ppd.check(ppd.lib().ppd_set_tuning(b"no_such_knob", 1))
