@@ -198,6 +198,10 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
  *   "gemm_epi_pipe" 1 (default): the plain GEMM epilogue keeps the next
  *                  32-column TMEM load in flight while it stores the current
  *                  chunk; 0: load, wait, store per chunk
+ *   "l2_hint"      3 (default): TMA loads of streams read once per step carry
+ *                  an L2 evict-first policy -- bit 0 the GEMM weights (steps
+ *                  whose token rows fit one unit), bit 1 the decode K/V;
+ *                  0: no cache hint
  *   "gemm_occ2"    -1 auto (<= 128 token rows), 0 off, 1 on: two co-resident
  *                  CTAs per SM with half-depth rings
  *   "attn_fused"   1 (default): a mixed decode + prefill step runs its
