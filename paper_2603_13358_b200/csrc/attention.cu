@@ -632,33 +632,74 @@ PPD_DEV void decode_body(const CUtensorMap* kv_map, const AttnParams& p, uint8_t
       }
     }
     if (split) {
-      __threadfence();
+      // release / acquire through one thread (the cooperative-groups grid
+      // barrier pattern): the CTA barrier orders every consumer's workspace
+      // stores before thread 0's fence + counter update, and the last
+      // arriver's fence before the barrier that releases its merge reads
       named_barrier_sync(bar_cons, kConsumerWarps * 32);
       if (tid == 0) {
         int* ctr = p.counters + (size_t)s * p.n_kv_heads + kvh;
+        __threadfence();
         const int prev = atomicAdd(ctr, 1);
         const int last = prev == it.n_splits - 1;
-        if (last) *ctr = 0;
+        if (last) {
+          *ctr = 0;
+          __threadfence();
+        }
         *flag = last;
       }
       named_barrier_sync(bar_cons, kConsumerWarps * 32);
       if (*flag) {
-        __threadfence();
         const int ws0 = it.ws_index - it.split;
-        for (int r = 0; r < G; ++r) {
-          float mm = -INFINITY;
-          for (int sp = 0; sp < it.n_splits; ++sp)
-            mm = fmaxf(mm, __ldcg(&p.ws_ml[(((size_t)(ws0 + sp) * p.n_kv_heads + kvh) * G + r) * 2]));
-          const float base = mm == -INFINITY ? 0.f : mm;
-          float ll = 0.f, acc = 0.f;
-          for (int sp = 0; sp < it.n_splits; ++sp) {
-            const size_t wi = ((size_t)(ws0 + sp) * p.n_kv_heads + kvh) * G + r;
-            const float f = exp2f(__ldcg(&p.ws_ml[wi * 2]) - base);
-            ll += __ldcg(&p.ws_ml[wi * 2 + 1]) * f;
-            acc += __ldcg(&p.ws_o[wi * kDh + tid]) * f;
-          }
-          p.out[((size_t)q_base * p.n_q_heads + kvh * G + r) * kDh + tid] = f2bf(acc / ll);
+        const int ns = it.n_splits;
+        // the host cuts at most 2 * 148 ranges: ns * G (m, l) pairs fit the
+        // merge buffer for every kv-head count >= 2 at G <= kDecMaxG
+        if (2 * ns * G > kConsumerWarps * kDecMaxG * kDh) __trap();
+        // every split's (m, l) of every row staged in the (consumed) merge
+        // buffer by one load per thread, then all rows' partial outputs of 4
+        // splits at a time in flight: these were serial L2 round trips per
+        // row and split (~10 us on the last CTA of a split sequence). Same
+        // summation order (split ascending) as a row-by-row merge.
+        for (int i = tid; i < ns * G; i += kConsumerWarps * 32) {
+          const int sp = i / G, r = i - sp * G;
+          const size_t wi = ((size_t)(ws0 + sp) * p.n_kv_heads + kvh) * G + r;
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) + wi);
+          sts_f32x2(mo + 2 * i, ml.x, ml.y);
         }
+        named_barrier_sync(bar_cons, kConsumerWarps * 32);
+        float base[kDecMaxG], ll[kDecMaxG], acc[kDecMaxG];
+#pragma unroll
+        for (int r = 0; r < kDecMaxG; ++r) {
+          float mm = -INFINITY;
+          if (r < G)
+            for (int sp = 0; sp < ns; ++sp) mm = fmaxf(mm, lds_f32(mo + 2 * (sp * G + r)));
+          base[r] = mm == -INFINITY ? 0.f : mm;
+          ll[r] = 0.f;
+          acc[r] = 0.f;
+        }
+        for (int sp0 = 0; sp0 < ns; sp0 += 4) {
+          float v[kDecMaxG][4];
+#pragma unroll
+          for (int r = 0; r < kDecMaxG; ++r)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              v[r][j] = (r < G && sp0 + j < ns)
+                            ? __ldcg(&p.ws_o[(((size_t)(ws0 + sp0 + j) * p.n_kv_heads + kvh) * G + r) * kDh + tid])
+                            : 0.f;
+#pragma unroll
+          for (int r = 0; r < kDecMaxG; ++r)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (r < G && sp0 + j < ns) {
+                const float* ml = mo + 2 * ((sp0 + j) * G + r);
+                const float f = exp2f(lds_f32(ml) - base[r]);
+                ll[r] += lds_f32(ml + 1) * f;
+                acc[r] += v[r][j] * f;
+              }
+        }
+#pragma unroll
+        for (int r = 0; r < kDecMaxG; ++r)
+          if (r < G) p.out[((size_t)q_base * p.n_q_heads + kvh * G + r) * kDh + tid] = f2bf(acc[r] / ll[r]);
       }
     }
     named_barrier_sync(bar_cons, kConsumerWarps * 32);  // merge buffer / flag reused by the next segment
