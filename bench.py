@@ -581,7 +581,7 @@ def run_ours(args, rank, world, local_rank):
     pk, pk_kind = peaks()
     traffic = None  # dram read+write per launch of the same kernel/config, from the committed ncu capture
     try:
-        prof_ncu = json.load(open(os.path.join(REPO, "profiles", "ncu_r02k_kernels.json")))
+        prof_ncu = json.load(open(os.path.join(REPO, "profiles", "ncu_r02l_kernels.json")))
         k0 = prof_ncu["decode_attention_B200_ctx1024_layer0"][0]
         if B == 200 and ctx0 == 1024:
             num = lambda v: float(str(v).split()[0])  # "854.9 Mbyte" or "854.9" (MB)
@@ -635,7 +635,7 @@ def run_ours(args, rank, world, local_rank):
             "unit": "GB/s",
             "frac": (attn_gbs / pk["hbm_gbs"]) if attn_gbs else None,
             "traffic": traffic,
-            "traffic_source": "profiles/ncu_r02k_kernels.json (ncu --set full, dram__bytes_read+write per launch)",
+            "traffic_source": "profiles/ncu_r02l_kernels.json (ncu --set full, dram__bytes_read+write per launch)",
             "algorithmic_bytes_per_launch": prof["attn_bytes"] / max(prof["attn_launches"], 1),
             "attn_share_of_step": prof["attn_ms"] / total_prof_ms if total_prof_ms else None,
             "gemm_share_of_step": prof["gemm_ms"] / total_prof_ms if total_prof_ms else None,
