@@ -202,7 +202,7 @@ int ppd_op_gemm_parts(const void* A, const void* B, void* C, int32_t M, int32_t 
  *                  an L2 evict-first policy -- bit 0 the GEMM weights (steps
  *                  whose token rows fit one unit), bit 1 the decode K/V;
  *                  0: no cache hint
- *   "gemm_occ2"    -1 auto (<= 128 token rows), 0 off, 1 on: two co-resident
+ *   "gemm_occ2"    0 (default) off, -1 auto (<= 128 token rows), 1 on: two co-resident
  *                  CTAs per SM with half-depth rings
  *   "attn_fused"   1 (default): a mixed decode + prefill step runs its
  *                  attention as ONE launch (K2) when its prefill tiles fit

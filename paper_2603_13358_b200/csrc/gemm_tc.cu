@@ -679,7 +679,11 @@ void gemm_tc_set_even_tiles(bool on) { g_even_tiles = on; }
 // two co-resident single CTAs per SM: -1 auto (<= kOcc2MaxT tokens; measured
 // tools/gemm_knobs.py: +10-20% weight streaming at T = 64 / 128, neutral at
 // T = 200, a loss with CTA pairs), 0 off, 1 whenever the shape allows
-static int g_occ2 = -1;
+// Round 2 (r02l, after the L2 evict-first weight policy): the single CTA per
+// SM with the full ring is faster at every measured size (tools/ab_step.py,
+// profiles/ab_small_r02l.log: B=16 -1.5%, B=64 -2.2%, B=128 -5.5%, B=32 +0.3%),
+// so auto is off by default; -1 restores the <= kOcc2MaxT rule
+static int g_occ2 = 0;
 constexpr int kOcc2MaxT = 128;
 constexpr int kOcc2Smem = 113 * 1024;
 static int g_stage_cap = 0;

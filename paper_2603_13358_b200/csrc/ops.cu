@@ -245,8 +245,7 @@ cudaError_t launch_rope_kv_write(const float* qkv, const GemmParts& parts, const
 // each thread produces 4 outputs from one float4 of gate and one of up.
 // Each thread produces kSiluQ quads (256 * 4 columns apart) and issues all of
 // their slice loads before the first store.
-constexpr int kSiluQ = 2;
-template <bool kEarly>
+template <bool kEarly, int kSiluQ>
 __global__ void silu_mul_kernel(const float* gu, GemmParts parts, bf16* m, int F) {
   pdl_enter<kEarly>();
   const int r = blockIdx.y;
@@ -265,8 +264,16 @@ __global__ void silu_mul_kernel(const float* gu, GemmParts parts, bf16* m, int F
 }
 cudaError_t launch_silu_mul(const float* gu, const GemmParts& parts, bf16* m, int T, int F, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  dim3 grid((F / 4 + 256 * kSiluQ - 1) / (256 * kSiluQ), T);
-  return launch_pdl(pdl_overlap() ? silu_mul_kernel<true> : silu_mul_kernel<false>, grid, dim3(256), 0, s, gu, parts, m, F);
+  // small batches: one quad per thread, so the grid still covers the SMs
+  // (T=16: 224 CTAs instead of 112)
+  if (T < 64) {
+    dim3 grid((F / 4 + 255) / 256, T);
+    return launch_pdl(pdl_overlap() ? silu_mul_kernel<true, 1> : silu_mul_kernel<false, 1>, grid, dim3(256), 0, s, gu,
+                      parts, m, F);
+  }
+  dim3 grid((F / 4 + 256 * 2 - 1) / (256 * 2), T);
+  return launch_pdl(pdl_overlap() ? silu_mul_kernel<true, 2> : silu_mul_kernel<false, 2>, grid, dim3(256), 0, s, gu,
+                    parts, m, F);
 }
 
 // ---------------------------------------------------------------- argmax

@@ -21,7 +21,7 @@ import numpy as np  # noqa: E402
 import paper_2603_13358_b200 as ppd  # noqa: E402
 
 DEFAULTS = {"gemm_pair": -1, "gemm_sched": -1, "gemm_stages": 0, "mlp_fused": 2, "attn_fused": 1,
-            "gemm_occ2": -1, "gemm_multi_sub": 1, "attn_pf_ctas": 0, "pdl_overlap": 0, "gemm_l2_pre": 0,
+            "gemm_occ2": 0, "gemm_multi_sub": 1, "attn_pf_ctas": 0, "pdl_overlap": 0, "gemm_l2_pre": 0,
             "layer_kernel": 0, "layer_l2_ahead": 16, "layer_stages": 0, "gemm_epi_pipe": 1, "l2_hint": 3}
 
 

@@ -16,7 +16,7 @@ VARIANTS = [
     {}, {"gemm_occ2": 0}, {"gemm_occ2": 1, "gemm_pair": 0}, {"gemm_multi_sub": 0},
     {"gemm_pair": 0}, {"gemm_pair": 1}, {"gemm_sched": 0}, {"gemm_sched": 1},
 ]
-DEFAULTS = {"gemm_occ2": -1, "gemm_stages": 0, "gemm_pair": -1, "gemm_sched": -1, "gemm_multi_sub": 1}
+DEFAULTS = {"gemm_occ2": 0, "gemm_stages": 0, "gemm_pair": -1, "gemm_sched": -1, "gemm_multi_sub": 1}
 
 
 def main():
